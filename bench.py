@@ -1,0 +1,435 @@
+#!/usr/bin/env python3
+"""bench.py — BASELINE.json metric on B200: PageRank GTEPS per iteration and
+the pull kernel's fraction of the HBM roofline.
+
+Default workload (N=1) is BASELINE.json configs[1] ("C2"): the damping sweep
+on RMAT scale 22 (edge factor 16, a/b/c/d .57/.19/.19/.05, dedup, no
+self-loops, ids permuted from seed 2108), 11 alphas .50..1.00 batched as K=11
+lanes on one GPU, tau 1e-6, L1, max 500 iterations, fp64.
+
+  step      = one full batched sweep on the device-resident graph: every lane
+              iterated to convergence (timing scope = the iteration loop, as
+              pagerank.hpp:83-100 times it), CUDA events on the engine stream
+  value     = GTEPS = sum_k iterations_k * E / step time   (edge relaxations
+              actually performed; frozen lanes are not counted)
+  e2e       = same metric through the C ABI with host buffers: upload of the
+              reference-layout CSR from pinned memory + device relabel +
+              batched run + download of the K rank vectors, every step
+  roofline  = algorithmic bytes of the pull kernel (per launch,
+              active lanes only) / its average launch time, vs the measured HBM
+              copy bandwidth in MEASURED_PEAKS.json
+
+--impl reference times the reference's own pagerank (oracle/_ref, compiled
+from the reference headers; else the oracle/ C port) on this box's host cores.
+Multi-GPU (torchrun): every rank runs an independent replica of the sweep
+(weak scaling, no data-path collective); rank 0 prints the line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 2108
+ALPHAS = [0.50, 0.55, 0.60, 0.65, 0.70, 0.75, 0.80, 0.85, 0.90, 0.95, 1.00]
+METRIC = "PageRank GTEPS per iteration at 1/2/4/8 B200; % of HBM roofline"
+CONFIGS = {
+    "c2": dict(workload="C2 damping sweep: RMAT-22 ef16 a/b/c=.57/.19/.19 seed 2108, "
+                        "K=11 alphas .50..1.00 batched, tau 1e-6, L1, max 500 it, fp64",
+               kind="rmat", scale=22, alphas=ALPHAS, tol=1e-6, norm=0),
+    "c1": dict(workload="C1: RMAT-16 alpha .85 tau 1e-6 L1", kind="rmat", scale=16,
+               alphas=[0.85], tol=1e-6, norm=0),
+    "c3": dict(workload="C3: grid 4096^2 p .6 +1% long-range, alpha .85, all norms to tau 1e-10",
+               kind="grid", side=4096, alphas=[0.85], tol=1e-10, norm=0, stop_mask=7),
+    "c4": dict(workload="C4: RMAT-26 alpha .85 tau 1e-10 Linf", kind="rmat", scale=26,
+               alphas=[0.85], tol=1e-10, norm=2),
+}
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+
+
+def measured_peak_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi SM clocks and throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+def algorithmic_bytes(n, e, n_src, k):
+    """B_iter(K) = 4E + 8(N+1) + 4N + K*16N + K*16*N_src."""
+    return 4 * e + 8 * (n + 1) + 4 * n + k * 16 * n + k * 16 * n_src
+
+
+def bytes_over_run(n, e, n_src, iterations):
+    """Sum over launches of B_iter(active lanes at that launch)."""
+    its = np.asarray(iterations)
+    total = 0
+    for t in range(1, int(its.max()) + 1):
+        total += algorithmic_bytes(n, e, n_src, int(np.sum(its >= t)))
+    return total
+
+
+def cpu_reference_sample(cfg, csr=None, seconds=12.0, kind_pref="reference"):
+    """The reference's pagerank on this box's host cores over a bounded sample:
+    the C2 graph, capped iterations per alpha lane (loop time = the reference's
+    own steady_clock `elapsed`, pagerank.hpp:83-100)."""
+    from pyoracle import REF_SO, Oracle, Ref
+    O = Oracle()
+    use_ref = kind_pref == "reference" and os.path.exists(REF_SO)
+    if csr is None:
+        if cfg["kind"] == "rmat":
+            n, pairs = O.rmat(cfg["scale"], 16, 0.57, 0.19, 0.19, SEED)
+        else:
+            n, pairs = O.grid(cfg["side"], 0.6, 0.01, SEED)
+        g = O.build_csr(n, pairs)
+        del pairs
+        csr = (g.vertex_count, g.in_offsets, g.in_neighbors, g.out_degree)
+    n, off, nbr, deg = csr
+    e = int(off[-1])
+    if use_ref:
+        R = Ref()
+        h = R.csr_from_arrays(n, off, nbr, deg)
+        run = lambda a, it: R.pagerank(h, a, 1e-300, "l1", it, want_ranks=False)  # noqa: E731
+        kind = "reference"
+    else:
+        h = O.L.orc_build_csr  # unused; port path below
+        R = None
+        from pyoracle import _Csr  # noqa: F401
+        hh = O.build_csr_handle(n, _pairs_from_csr(off, nbr))
+        kind = "port"
+
+        def run(a, it):
+            t = time.perf_counter()
+            r = O.pagerank(hh, a, 1e-300, "l1", it)
+            r["elapsed_ms"] = (time.perf_counter() - t) * 1e3
+            return r
+    total_ms, total_it, lanes = 0.0, 0, 0
+    t_end = time.time() + seconds
+    while time.time() < t_end or total_it == 0:
+        a = cfg["alphas"][lanes % len(cfg["alphas"])]
+        r = run(a, 2)
+        total_ms += r["elapsed_ms"]
+        total_it += r["iterations"]
+        lanes += 1
+    if R is not None:
+        R.free_csr(h)
+    gteps = total_it * e / (total_ms / 1e3) / 1e9
+    return dict(value=gteps, unit="GTEPS", cores=1, kind=kind,
+                sample=f"{lanes} alpha lanes x 2 iterations of the reference pagerank loop on the "
+                       f"{cfg['workload'].split(':')[0]} graph (N={n}, E={e}); 1 core "
+                       f"(the reference engine is single-threaded, pagerank.hpp:84-99)",
+                ms_per_iteration=total_ms / total_it)
+
+
+def _pairs_from_csr(off, nbr):
+    n = off.size - 1
+    dst = np.repeat(np.arange(n, dtype=np.uint32), np.diff(off.astype(np.int64)))
+    return np.stack([nbr, dst], axis=1).reshape(-1).astype(np.uint32)
+
+
+# ---------------------------------------------------------------------------
+def run_reference_arm(args, cfg):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=False)
+    steps, warmup = args.steps, args.warmup
+    from pyoracle import REF_SO, Oracle, Ref
+    O = Oracle()
+    if cfg["kind"] == "rmat":
+        n, pairs = O.rmat(cfg["scale"], 16, 0.57, 0.19, 0.19, SEED)
+    else:
+        n, pairs = O.grid(cfg["side"], 0.6, 0.01, SEED)
+    g = O.build_csr(n, pairs)
+    del pairs
+    e = g.edge_count()
+    kind = "reference" if os.path.exists(REF_SO) else "port"
+    if kind == "reference":
+        R = Ref()
+        h = R.csr_from_arrays(n, g.in_offsets, g.in_neighbors, g.out_degree)
+        run = lambda a, it: R.pagerank(h, a, 1e-300, "l1", it, want_ranks=False)  # noqa: E731
+    else:
+        hh = O.build_csr_handle(n, _pairs_from_csr(g.in_offsets, g.in_neighbors))
+
+        def run(a, it):
+            t = time.perf_counter()
+            r = O.pagerank(hh, a, 1e-300, "l1", it)
+            r["elapsed_ms"] = (time.perf_counter() - t) * 1e3
+            return r
+    its_per_step = 2
+    for i in range(warmup):
+        run(cfg["alphas"][i % len(cfg["alphas"])], 1)
+    t0 = time.perf_counter()
+    loop_ms, iters = 0.0, 0
+    for i in range(steps):
+        r = run(cfg["alphas"][i % len(cfg["alphas"])], its_per_step)
+        loop_ms += r["elapsed_ms"]
+        iters += r["iterations"]
+    wall = time.perf_counter() - t0
+    value = iters * e / (loop_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GTEPS", "impl": "reference",
+        "n_gpus": world, "steps": steps, "warmup": warmup,
+        "ms_per_step": loop_ms / steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded RMAT, DESIGN.md)",
+        "config": {"workload": cfg["workload"], "vertices": n, "edges": e,
+                   "step": f"one alpha lane of the sweep, {its_per_step} iterations of the "
+                           "reference pagerank loop (bounded sample)",
+                   "wall_s": wall},
+        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": 1, "kind": kind,
+                         "sample": f"{steps} steps x {its_per_step} iterations, alpha cycling "
+                                   f"{cfg['alphas'][0]}..{cfg['alphas'][-1]}; reference engine is "
+                                   "single-threaded (pagerank.hpp:84-99)"},
+        "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import torch
+    import paper_2108_02997_b200 as prl
+    from paper_2108_02997_b200 import _lib
+
+    rank, world, local = env_rank()
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local if dist else 0
+    torch.cuda.set_device(dev)
+
+    t_build = time.perf_counter()
+    if cfg["kind"] == "rmat":
+        g = prl.generate_rmat(cfg["scale"], 16, 0.57, 0.19, 0.19, SEED, device=dev)
+    else:
+        g = prl.generate_grid(cfg["side"], 0.6, 0.01, SEED, device=dev)
+    build_s = time.perf_counter() - t_build
+    n, e = g.vertex_count, g.edge_count()
+    n_src = n - int(g.info.dangling_count)
+    K = len(cfg["alphas"])
+    sess = prl.Session(g, cfg["alphas"], cfg["tol"], prl.NormKind(cfg["norm"]), 500,
+                       cfg.get("stop_mask", 0))
+    for _ in range(args.warmup):
+        sess.run()
+    res = sess.results(want_ranks=False)
+    iters = res["iterations"]
+    run_its = int(res["run_iterations"])
+    lane_its = int(np.sum(iters))
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if dist:
+            tdist.barrier()
+        torch.cuda.synchronize(dev)
+
+    barrier()
+    launches0 = _lib.launch_count()
+    with ClockSampler(dev) as clk:
+        t0 = time.perf_counter()
+        step_ms = [sess.run() for _ in range(args.steps)]
+        barrier()
+        wall = time.perf_counter() - t0
+    check = sess.results(want_ranks=False)
+    if not np.array_equal(check["iterations"], iters):
+        raise RuntimeError("iteration counts changed between steps (determinism)")
+    total_ms = float(sum(step_ms))
+    if dist:
+        t = torch.tensor([total_ms], device=f"cuda:{dev}", dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * lane_its * e / (ms_per_step / 1e3) / 1e9
+    gpu_launches = args.steps * (1 + run_its)
+
+    # roofline of the pull kernel: per-launch device time measured live (events)
+    per_launch_ms = sess.time_pull(run_its)
+    bytes_run = bytes_over_run(n, e, n_src, iters)
+    achieved_loop = bytes_run / (ms_per_step / 1e3) / 1e9
+    achieved = bytes_run / run_its / (per_launch_ms / 1e3) / 1e9
+    peak, peak_kind = measured_peak_gbs()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                traffic = json.load(f).get(args.config)
+        except Exception:
+            traffic = None
+
+    # e2e through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(args, cfg, g, prl, torch, dev, lane_its)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            off, nbr, deg = g.in_offsets, g.in_neighbors, g.out_degree
+            cpu = cpu_reference_sample(cfg, (n, off, nbr, deg), seconds=args.cpu_seconds)
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": "GTEPS", "cores": 1, "kind": "reference",
+                   "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded RMAT/grid generated on the device (DESIGN.md)",
+            "config": {"workload": cfg["workload"], "vertices": n, "edges": e,
+                       "dangling": int(g.info.dangling_count), "lanes": K,
+                       "iterations_per_lane": iters.tolist(), "iterations_run": run_its,
+                       "lane_iterations": lane_its,
+                       "gteps_all_lanes_per_iteration": K * e * run_its / (ms_per_step / 1e3) / 1e9,
+                       "timed_scope": "iteration loop (pagerank.hpp:83-100), CUDA events",
+                       "l2": "inputs exceed L2 (CSR + contributions > 126 MB); no flush",
+                       "parallelism": "replicas" if world > 1 else "single GPU",
+                       "graph_build_s": build_s, "wall_s": wall},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_kind,
+                         "kernel": "pull_kernel (fused pull + epilogue + finalize)",
+                         "per_launch_ms": per_launch_ms,
+                         "algorithmic_bytes_per_launch": bytes_run / run_its,
+                         "achieved_over_loop": achieved_loop},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        tdist.barrier()
+        tdist.destroy_process_group()
+    return 0
+
+
+def measure_e2e(args, cfg, g, prl, torch, dev, lane_its):
+    """C-ABI call with host buffers: prgpu_graph_from_csr (pinned H2D of the
+    reference-layout CSR + device relabel) -> prgpu_pagerank (K lanes, ranks
+    D2H into pinned memory) -> free, timed end to end on the host per step."""
+    import ctypes as C
+    from paper_2108_02997_b200 import _lib
+    L = _lib.lib()
+    n, e = g.vertex_count, g.edge_count()
+    off = torch.from_numpy(g.in_offsets).pin_memory()
+    nbr = torch.from_numpy(g.in_neighbors).pin_memory()
+    deg = torch.from_numpy(g.out_degree).pin_memory()
+    K = len(cfg["alphas"])
+    ranks = torch.empty((K, n), dtype=torch.float64).pin_memory()
+    its = np.zeros(K, np.int32)
+    conv = np.zeros(K, np.uint8)
+    alphas = (C.c_double * K)(*cfg["alphas"])
+    p = _lib.Params(K, alphas, None, cfg["tol"], cfg["norm"], cfg.get("stop_mask", 0), 500, None)
+    r = _lib.Result(C.cast(ranks.data_ptr(), C.POINTER(C.c_double)),
+                    its.ctypes.data_as(C.POINTER(C.c_int)),
+                    conv.ctypes.data_as(C.POINTER(C.c_uint8)), None, None, 0.0, 0)
+
+    def step():
+        h = C.c_void_p()
+        _lib.check(L.prgpu_graph_from_csr(n, off.data_ptr(), nbr.data_ptr(), deg.data_ptr(), dev,
+                                          C.byref(h)), "graph_from_csr")
+        _lib.check(L.prgpu_pagerank(h, C.byref(p), C.byref(r)), "pagerank")
+        L.prgpu_graph_free(h)
+
+    for _ in range(max(1, args.warmup // 2)):
+        step()
+    steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t0) / steps
+    h2d = 8 * (n + 1) + 4 * e + 4 * n + 8 * K
+    d2h = 8 * K * n + 13 * K
+    return {"value": lane_its * e / dt / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3, "steps": steps,
+            "path": "prgpu_graph_from_csr + prgpu_pagerank (C ABI, pinned host buffers)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

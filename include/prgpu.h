@@ -1,0 +1,155 @@
+/*
+ * prgpu.h — C ABI of libprgpu.so, the B200-native pull-PageRank engine.
+ *
+ * The reference (pagerank-lab, /root/reference/proj) has no FFI: its boundary
+ * is a set of inline C++ functions in namespace pagerank_lab.  Each entry
+ * point below replaces one of them; the C++ drop-in header
+ * include/pagerank_b200/pagerank_lab.hpp and the Python mirror
+ * paper_2108_02997_b200/pagerank_lab.py bind these and keep the reference's
+ * signatures and error behaviour (INTEGRATION.md shows the bindings).
+ *
+ * Conventions: plain pointers and sizes, no exceptions cross the boundary,
+ * every call returns a PRGPU_* status and leaves a message in
+ * prgpu_last_error() (thread-local).  Host pointers are ordinary host memory
+ * unless a name says "device".  A prgpu_graph is immutable after construction
+ * and may be shared by concurrent prgpu_pagerank calls (graph.hpp:44-46,
+ * SPEC.md "engine is reentrant"); each call uses its own stream and scratch.
+ */
+#ifndef PRGPU_H
+#define PRGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PRGPU_API __attribute__((visibility("default")))
+#else
+#define PRGPU_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------- */
+#define PRGPU_OK 0
+#define PRGPU_EINVAL 1 /* maps to std::invalid_argument / ValueError          */
+#define PRGPU_ECUDA 2  /* CUDA runtime or kernel failure                       */
+#define PRGPU_ENCCL 3  /* NCCL failure (multi-GPU)                             */
+#define PRGPU_ENOMEM 4 /* device allocation failed                             */
+
+/* ---- norms (norms.hpp:18 NormKind) -------------------------------------- */
+#define PRGPU_NORM_L1 0
+#define PRGPU_NORM_L2 1
+#define PRGPU_NORM_LINF 2
+
+#define PRGPU_MAX_LANES 16 /* batched rank vectors per run (alpha sweep) */
+
+typedef struct prgpu_graph prgpu_graph;
+typedef struct prgpu_session prgpu_session;
+
+/* Summary of a device graph. */
+typedef struct {
+    uint32_t vertex_count;   /* CsrGraph::vertex_count               graph.hpp:48 */
+    uint64_t edge_count;     /* CsrGraph::edge_count() after dedup   graph.hpp:59 */
+    uint32_t dangling_count; /* |CsrGraph::dangling|                 graph.hpp:52 */
+    uint32_t max_in_degree;
+    uint32_t hub_rows;       /* rows pulled block-per-vertex */
+    uint32_t warp_rows;      /* rows pulled warp-per-vertex */
+    uint32_t thread_rows;    /* rows pulled by a lane group (in-degree >= 1) */
+    uint32_t empty_rows;     /* in-degree 0: rank = c0 */
+    int device;
+} prgpu_graph_info;
+
+/* ---- graph construction (replaces build_csr, graph.hpp:204-234) ---------
+ * Edges are the reference's EdgeList layout: interleaved (source, target)
+ * u32 pairs, duplicates allowed, self-loops kept (graph.hpp:36-39,202-203).
+ * The in-CSR is built on the device (sort by (target, source), unique,
+ * count, scan), then relabelled for the pull kernel. */
+PRGPU_API int prgpu_graph_build(uint32_t n, const uint32_t* edge_pairs, uint64_t m, int device,
+                      prgpu_graph** out);
+/* Same, from pairs already resident on `device`. */
+PRGPU_API int prgpu_graph_build_device(uint32_t n, const uint32_t* d_edge_pairs, uint64_t m, int device,
+                             prgpu_graph** out);
+/* From a reference-layout CsrGraph on the host (graph.hpp:47-60):
+ * in_offsets[n+1], in_neighbors[in_offsets[n]] (ascending per row),
+ * out_degree[n].  Validated on the device. */
+PRGPU_API int prgpu_graph_from_csr(uint32_t n, const uint64_t* in_offsets, const uint32_t* in_neighbors,
+                         const uint32_t* out_degree, int device, prgpu_graph** out);
+/* Synthetic benchmark graphs generated on the device (DESIGN.md "Synthetic
+ * inputs"; bit-identical to oracle/oracle.c's orc_rmat / orc_grid). */
+PRGPU_API int prgpu_graph_generate_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                              uint64_t seed, int device, prgpu_graph** out);
+PRGPU_API int prgpu_graph_generate_grid(uint32_t side, double p, double longrange_frac, uint64_t seed,
+                              int device, prgpu_graph** out);
+
+PRGPU_API int prgpu_graph_get_info(const prgpu_graph* g, prgpu_graph_info* info);
+/* Copies the reference-layout CSR back (any pointer may be NULL):
+ * in_offsets[n+1], in_neighbors[e], out_degree[n], dangling[dangling_count]. */
+PRGPU_API int prgpu_graph_download(const prgpu_graph* g, uint64_t* in_offsets, uint32_t* in_neighbors,
+                         uint32_t* out_degree, uint32_t* dangling);
+PRGPU_API void prgpu_graph_free(prgpu_graph* g);
+
+/* ---- engine (replaces pagerank, pagerank.hpp:70-108) --------------------
+ * K rank vectors ("lanes") run together, one alpha each; every edge visit
+ * feeds all K lanes.  A lane stops when every norm in its stop mask is below
+ * its tolerance (strict, pagerank.hpp:99,105) or at max_iterations; its
+ * ranks then freeze.  K = 1 with stop_mask = 1 << norm is exactly the
+ * reference's pagerank(g, {alpha, tolerance, norm, max_iterations}). */
+typedef struct {
+    int lanes;                /* K, 1..PRGPU_MAX_LANES */
+    const double* alphas;     /* [K] damping factors, each in [0, 1] */
+    const double* tolerances; /* [K] (NULL: use `tolerance` for all lanes) */
+    double tolerance;         /* > 0 */
+    int norm;                 /* PRGPU_NORM_* reported as final_err */
+    uint32_t stop_mask;       /* bit i = norm i must be < tolerance; 0 => 1 << norm */
+    int max_iterations;       /* >= 1 */
+    const double* ref_ranks;  /* optional [n] host, original ids: trace L1 distance to it */
+} prgpu_params;
+
+typedef struct {
+    double* ranks;            /* optional [K][n] host, original vertex ids */
+    int* iterations;          /* optional [K] */
+    uint8_t* converged;       /* optional [K] */
+    double* final_err;        /* optional [K]: err of the last iteration under `norm` */
+    double* err_trace;        /* optional [max_iterations][K][4]: L1, L2, LInf, L1-vs-ref */
+    double loop_ms;           /* out: device time of the iteration loop (CUDA events) */
+    int run_iterations;       /* out: iterations executed (max over lanes) */
+} prgpu_result;
+
+/* One-shot run: allocate, iterate on the device (no per-iteration host sync),
+ * copy results, free. */
+PRGPU_API int prgpu_pagerank(prgpu_graph* g, const prgpu_params* p, prgpu_result* out);
+
+/* Per-iteration observer (pagerank.hpp:51-52,98): called after every
+ * iteration of lane `lane` with its ranks (original ids) and error.  This
+ * path syncs once per iteration and is meant for tests. */
+typedef void (*prgpu_observer_fn)(int iteration, int lane, const double* ranks, uint64_t n,
+                                  double err, void* user);
+PRGPU_API int prgpu_pagerank_observed(prgpu_graph* g, const prgpu_params* p, prgpu_result* out,
+                            prgpu_observer_fn fn, void* user);
+
+/* Reusable device session for repeated runs (bench, sweeps): state and the
+ * CUDA graph are built once; each run re-initialises ranks on the device. */
+PRGPU_API int prgpu_session_create(prgpu_graph* g, const prgpu_params* p, prgpu_session** out);
+PRGPU_API int prgpu_session_run(prgpu_session* s, double* loop_ms);
+PRGPU_API int prgpu_session_results(prgpu_session* s, prgpu_result* out);
+/* Device time of `launches` back-to-back launches of the pull kernel alone
+ * (CUDA events on the session stream), in ms per launch. */
+PRGPU_API int prgpu_session_time_pull(prgpu_session* s, int launches, double* ms_per_launch);
+PRGPU_API void prgpu_session_free(prgpu_session* s);
+
+/* ---- norms (replaces error_norm, norms.hpp:48-78) ----------------------- */
+PRGPU_API int prgpu_error_norm(int norm, const double* r, const double* s, uint64_t n, int device,
+                     double* out);
+
+/* ---- misc ---------------------------------------------------------------- */
+PRGPU_API const char* prgpu_last_error(void);
+PRGPU_API const char* prgpu_version(void);
+/* Number of pull-kernel launches (and other kernels) this process issued. */
+PRGPU_API uint64_t prgpu_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

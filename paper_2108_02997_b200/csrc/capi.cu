@@ -1,0 +1,218 @@
+// capi.cu — extern "C" boundary of libprgpu.so (include/prgpu.h).
+// No exception crosses it: every entry point returns a PRGPU_* status and
+// leaves a thread-local message for prgpu_last_error().
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "common.cuh"
+
+namespace prgpu {
+std::atomic<uint64_t> g_launches{0};
+
+std::unique_ptr<prgpu_graph> graph_build_device(uint32_t, const uint32_t*, uint64_t, int, cudaStream_t);
+std::unique_ptr<prgpu_graph> graph_build_host(uint32_t, const uint32_t*, uint64_t, int, cudaStream_t);
+std::unique_ptr<prgpu_graph> graph_from_csr(uint32_t, const uint64_t*, const uint32_t*,
+                                            const uint32_t*, int, cudaStream_t);
+std::unique_ptr<prgpu_graph> graph_generate_rmat(uint32_t, uint32_t, double, double, double,
+                                                 uint64_t, int, cudaStream_t);
+std::unique_ptr<prgpu_graph> graph_generate_grid(uint32_t, double, double, uint64_t, int,
+                                                 cudaStream_t);
+void graph_download(const prgpu_graph*, uint64_t*, uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
+prgpu_session* session_create(prgpu_graph*, const prgpu_params*, bool);
+void session_destroy(prgpu_session*);
+using SessionPtr = std::unique_ptr<prgpu_session, void (*)(prgpu_session*)>;
+double session_run(prgpu_session*);
+void session_results(prgpu_session*, prgpu_result*);
+void session_observed(prgpu_session*, prgpu_result*, prgpu_observer_fn, void*);
+double session_time_pull(prgpu_session*, int);
+double error_norm_device(int, const double*, const double*, uint64_t, int);
+} // namespace prgpu
+
+namespace {
+thread_local std::string t_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        t_last_error.clear();
+        f();
+        return PRGPU_OK;
+    } catch (const prgpu::Error& e) {
+        t_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        t_last_error = "host allocation failed";
+        return PRGPU_ENOMEM;
+    } catch (const std::exception& e) {
+        t_last_error = e.what();
+        return PRGPU_ECUDA;
+    } catch (...) {
+        t_last_error = "unknown error";
+        return PRGPU_ECUDA;
+    }
+}
+
+void check_device(int device) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        prgpu::fail(PRGPU_ECUDA, "no CUDA device available (libprgpu has no CPU fallback)");
+    if (device < 0 || device >= count)
+        prgpu::fail(PRGPU_EINVAL, "device index out of range: " + std::to_string(device));
+}
+
+template <typename Make>
+int make_graph(int device, prgpu_graph** out, Make&& make) {
+    return guarded([&] {
+        if (!out) prgpu::fail(PRGPU_EINVAL, "null output pointer");
+        *out = nullptr;
+        check_device(device);
+        prgpu::DeviceGuard dg(device);
+        prgpu::Stream st;
+        std::unique_ptr<prgpu_graph> g = make((cudaStream_t)st);
+        PRGPU_CUDA(cudaStreamSynchronize(st));
+        *out = g.release();
+    });
+}
+} // namespace
+
+extern "C" {
+
+int prgpu_graph_build(uint32_t n, const uint32_t* pairs, uint64_t m, int device, prgpu_graph** out) {
+    if (m && !pairs) { t_last_error = "null edge_pairs"; return PRGPU_EINVAL; }
+    return make_graph(device, out, [&](cudaStream_t st) {
+        return prgpu::graph_build_host(n, pairs, m, device, st);
+    });
+}
+
+int prgpu_graph_build_device(uint32_t n, const uint32_t* d_pairs, uint64_t m, int device,
+                             prgpu_graph** out) {
+    if (m && !d_pairs) { t_last_error = "null edge_pairs"; return PRGPU_EINVAL; }
+    return make_graph(device, out, [&](cudaStream_t st) {
+        return prgpu::graph_build_device(n, d_pairs, m, device, st);
+    });
+}
+
+int prgpu_graph_from_csr(uint32_t n, const uint64_t* off, const uint32_t* nbr, const uint32_t* deg,
+                         int device, prgpu_graph** out) {
+    if (!off || !deg || (n && off[n] && !nbr)) { t_last_error = "null CSR array"; return PRGPU_EINVAL; }
+    return make_graph(device, out, [&](cudaStream_t st) {
+        return prgpu::graph_from_csr(n, off, nbr, deg, device, st);
+    });
+}
+
+int prgpu_graph_generate_rmat(uint32_t scale, uint32_t ef, double a, double b, double c,
+                              uint64_t seed, int device, prgpu_graph** out) {
+    return make_graph(device, out, [&](cudaStream_t st) {
+        return prgpu::graph_generate_rmat(scale, ef, a, b, c, seed, device, st);
+    });
+}
+
+int prgpu_graph_generate_grid(uint32_t side, double p, double lr, uint64_t seed, int device,
+                              prgpu_graph** out) {
+    return make_graph(device, out, [&](cudaStream_t st) {
+        return prgpu::graph_generate_grid(side, p, lr, seed, device, st);
+    });
+}
+
+int prgpu_graph_get_info(const prgpu_graph* g, prgpu_graph_info* info) {
+    return guarded([&] {
+        if (!g || !info) prgpu::fail(PRGPU_EINVAL, "null argument");
+        info->vertex_count = g->n;
+        info->edge_count = g->e;
+        info->dangling_count = g->ndangling;
+        info->max_in_degree = g->max_in_degree;
+        info->hub_rows = g->hub_end;
+        info->warp_rows = g->warp_end - g->hub_end;
+        info->thread_rows = g->nonempty_end - g->warp_end;
+        info->empty_rows = g->n - g->nonempty_end;
+        info->device = g->device;
+    });
+}
+
+int prgpu_graph_download(const prgpu_graph* g, uint64_t* off, uint32_t* nbr, uint32_t* deg,
+                         uint32_t* dang) {
+    return guarded([&] {
+        if (!g) prgpu::fail(PRGPU_EINVAL, "null graph");
+        prgpu::DeviceGuard dg(g->device);
+        prgpu::Stream st;
+        prgpu::graph_download(g, off, nbr, deg, dang, st);
+    });
+}
+
+void prgpu_graph_free(prgpu_graph* g) {
+    if (!g) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(g->device);
+    delete g;
+    cudaSetDevice(prev);
+}
+
+int prgpu_pagerank(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
+    return guarded([&] {
+        if (!out) prgpu::fail(PRGPU_EINVAL, "null result");
+        if (g) check_device(g->device);
+        prgpu::SessionPtr s(prgpu::session_create(g, p, true), prgpu::session_destroy);
+        prgpu::session_run(s.get());
+        prgpu::session_results(s.get(), out);
+    });
+}
+
+int prgpu_pagerank_observed(prgpu_graph* g, const prgpu_params* p, prgpu_result* out,
+                            prgpu_observer_fn fn, void* user) {
+    return guarded([&] {
+        if (!out) prgpu::fail(PRGPU_EINVAL, "null result");
+        if (g) check_device(g->device);
+        prgpu::SessionPtr s(prgpu::session_create(g, p, false), prgpu::session_destroy);
+        prgpu::session_observed(s.get(), out, fn, user);
+    });
+}
+
+int prgpu_session_create(prgpu_graph* g, const prgpu_params* p, prgpu_session** out) {
+    return guarded([&] {
+        if (!out) prgpu::fail(PRGPU_EINVAL, "null output pointer");
+        *out = nullptr;
+        if (g) check_device(g->device);
+        *out = prgpu::session_create(g, p, true);
+    });
+}
+
+int prgpu_session_run(prgpu_session* s, double* loop_ms) {
+    return guarded([&] {
+        if (!s) prgpu::fail(PRGPU_EINVAL, "null session");
+        const double ms = prgpu::session_run(s);
+        if (loop_ms) *loop_ms = ms;
+    });
+}
+
+int prgpu_session_results(prgpu_session* s, prgpu_result* out) {
+    return guarded([&] {
+        if (!s || !out) prgpu::fail(PRGPU_EINVAL, "null argument");
+        prgpu::session_results(s, out);
+    });
+}
+
+int prgpu_session_time_pull(prgpu_session* s, int launches, double* ms) {
+    return guarded([&] {
+        if (!s || !ms || launches < 1) prgpu::fail(PRGPU_EINVAL, "bad argument");
+        *ms = prgpu::session_time_pull(s, launches);
+    });
+}
+
+void prgpu_session_free(prgpu_session* s) { prgpu::session_destroy(s); }
+
+int prgpu_error_norm(int norm, const double* r, const double* s, uint64_t n, int device,
+                     double* out) {
+    return guarded([&] {
+        if (!out || (n && (!r || !s))) prgpu::fail(PRGPU_EINVAL, "null argument");
+        check_device(device);
+        *out = prgpu::error_norm_device(norm, r, s, n, device);
+    });
+}
+
+const char* prgpu_last_error(void) { return t_last_error.c_str(); }
+const char* prgpu_version(void) { return "prgpu 0.1.0 (sm_100a)"; }
+uint64_t prgpu_kernel_launch_count(void) { return prgpu::g_launches.load(); }
+
+} // extern "C"

@@ -1,0 +1,113 @@
+// common.cuh — shared internals of libprgpu.so (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/prgpu.h"
+
+namespace prgpu {
+
+// Errors thrown inside the library and turned into status codes at the C ABI.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
+    if (e == cudaSuccess) return;
+    const int code = (e == cudaErrorMemoryAllocation) ? PRGPU_ENOMEM : PRGPU_ECUDA;
+    fail(code, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                   std::to_string(line) + ")");
+}
+
+#define PRGPU_CUDA(call) ::prgpu::check_cuda((call), #call, __FILE__, __LINE__)
+#define PRGPU_LAUNCHED(name)                                                          \
+    do {                                                                              \
+        ::prgpu::g_launches.fetch_add(1, std::memory_order_relaxed);                  \
+        ::prgpu::check_cuda(cudaGetLastError(), name, __FILE__, __LINE__);            \
+    } while (0)
+
+extern std::atomic<uint64_t> g_launches;
+
+// RAII device buffer.
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { reset(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevBuf() { reset(); }
+    void alloc(size_t count) {
+        reset();
+        n = count;
+        if (count) PRGPU_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    T* release() { T* q = p; p = nullptr; n = 0; return q; }
+};
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        PRGPU_CUDA(cudaGetDevice(&prev));
+        if (dev != prev) PRGPU_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+struct Stream {
+    cudaStream_t s = nullptr;
+    Stream() { PRGPU_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+    ~Stream() { if (s) cudaStreamDestroy(s); }
+    Stream(const Stream&) = delete;
+    Stream& operator=(const Stream&) = delete;
+    operator cudaStream_t() const { return s; }
+};
+
+// Pull-kernel degree bins (rows sorted by in-degree descending).
+constexpr uint32_t kHubMinDegree = 4096; // > : block per vertex
+constexpr uint32_t kWarpMinDegree = 32;  // > : warp per vertex; else lane group
+
+inline uint32_t bits_for(uint64_t n) { // ceil(log2(n)), >= 1
+    uint32_t b = 1;
+    while ((1ull << b) < n) ++b;
+    return b;
+}
+
+} // namespace prgpu
+
+// The device graph: engine layout (relabelled) + the permutation back to the
+// caller's ids.  Immutable after construction.
+struct prgpu_graph {
+    int device = 0;
+    uint32_t n = 0;
+    uint64_t e = 0;
+    uint32_t ndangling = 0;
+    uint32_t max_in_degree = 0;
+    uint32_t lg = 1; // bits per vertex id in packed edge keys
+    // engine CSR, vertices relabelled by in-degree descending (ties: old id)
+    prgpu::DevBuf<uint64_t> row_off;    // [n+1]
+    prgpu::DevBuf<uint32_t> col;        // [e + 16] (padding for 128-bit loads)
+    prgpu::DevBuf<uint32_t> deg;        // [n] out-degree, engine ids
+    prgpu::DevBuf<uint32_t> new_of_old; // [n]
+    prgpu::DevBuf<uint32_t> old_of_new; // [n]
+    uint32_t hub_end = 0, warp_end = 0, nonempty_end = 0;
+};

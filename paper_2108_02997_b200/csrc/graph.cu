@@ -1,0 +1,577 @@
+// graph.cu — K0: device in-CSR (transpose) construction, relabelling, the
+// synthetic benchmark generators, and the reference-layout download.
+//
+// Replaces build_csr (graph.hpp:204-234): sort edges by (target, source)
+// (:209-212), drop exact duplicates (:213), count in/out degrees (:220-223),
+// scan (:224), fill in-neighbours (:226-228), dangling list (:230-231).
+// Here the sort is a CUB radix sort of the packed key target<<lg | source
+// (same total order), the counts are integer atomics (order-free, so the
+// arrays are bit-identical to the reference's), and the scan is a device scan.
+//
+// The engine then relabels vertices by in-degree descending (ties: original
+// id ascending) so the degree bins of the pull kernel are contiguous row
+// ranges and the hottest rows/sources are packed at the front.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+namespace prgpu {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(uint64_t n, int threads = kThreads) {
+    uint64_t b = (n + threads - 1) / threads;
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(b, 148ull * 64));
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+
+inline uint64_t mix64_host(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+
+inline uint64_t stream_key(uint64_t seed, uint64_t stream) {
+    return mix64_host(seed * 0x9E3779B97F4A7C15ull + stream);
+}
+
+inline uint64_t prob_threshold(double p) {
+    if (!(p > 0.0)) return 0;
+    const double x = p * 18446744073709551616.0;
+    if (x >= 18446744073709551616.0) return UINT64_MAX;
+    return (uint64_t)x;
+}
+
+constexpr uint64_t kSentinel = ~0ull;
+
+// ---- packing -----------------------------------------------------------------
+__global__ void pairs_to_keys(const uint32_t* __restrict__ pairs, uint64_t m, uint32_t n,
+                              uint32_t lg, uint64_t* __restrict__ keys, int* bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint2 p = reinterpret_cast<const uint2*>(pairs)[i];
+        if (p.x >= n || p.y >= n) *bad = 1;
+        keys[i] = ((uint64_t)p.y << lg) | p.x;
+    }
+}
+
+// ---- synthetic generators (spec: DESIGN.md; host twin: oracle/oracle.c) -------
+struct PermKeys {
+    uint64_t k[3];
+    uint64_t mask;
+    uint32_t hs;
+};
+
+__device__ __forceinline__ uint32_t perm_apply(uint32_t x32, const PermKeys& pk) {
+    uint64_t x = x32;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        x = (x * (pk.k[r] | 1ull)) & pk.mask;
+        x = (x + (pk.k[r] >> 40)) & pk.mask;
+        x ^= x >> pk.hs;
+    }
+    return (uint32_t)x;
+}
+
+__global__ void rmat_keys(uint64_t m, uint32_t scale, uint64_t kd, uint64_t ta, uint64_t tab,
+                          uint64_t tabc, PermKeys pk, uint64_t* __restrict__ keys) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t src = 0, dst = 0;
+        for (uint32_t l = 0; l < scale; ++l) {
+            const uint64_t x = mix64(kd ^ ((i << 6) | l));
+            const uint32_t bit = 1u << (scale - 1 - l);
+            if (x < ta) {
+            } else if (x < tab) {
+                dst |= bit;
+            } else if (x < tabc) {
+                src |= bit;
+            } else {
+                src |= bit;
+                dst |= bit;
+            }
+        }
+        keys[i] = (src == dst) ? kSentinel
+                               : (((uint64_t)perm_apply(dst, pk) << scale) | perm_apply(src, pk));
+    }
+}
+
+__global__ void grid_keys(uint32_t side, uint64_t uh, uint64_t tp, uint64_t kg, uint64_t L,
+                          uint64_t kl, uint64_t n, uint32_t lg, uint64_t* __restrict__ keys) {
+    const uint64_t total = 2 * uh; // candidates
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total + L;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        if (t < total) {
+            uint64_t a, b;
+            if (t < uh) {
+                const uint64_t r = t / (side - 1), c = t % (side - 1);
+                a = r * side + c;
+                b = a + 1;
+            } else {
+                const uint64_t j = t - uh;
+                const uint64_t r = j / side, c = j % side;
+                a = r * side + c;
+                b = a + side;
+            }
+            const bool keep = mix64(kg ^ t) < tp;
+            keys[2 * t] = keep ? ((b << lg) | a) : kSentinel;     // a -> b
+            keys[2 * t + 1] = keep ? ((a << lg) | b) : kSentinel; // b -> a
+        } else {
+            const uint64_t j = t - total;
+            const uint64_t s = __umul64hi(mix64(kl ^ (2 * j)), n);
+            const uint64_t d = __umul64hi(mix64(kl ^ (2 * j + 1)), n);
+            keys[2 * total + j] = (s == d) ? kSentinel : ((d << lg) | s);
+        }
+    }
+}
+
+// ---- CSR assembly ---------------------------------------------------------------
+__global__ void count_degrees(const uint64_t* __restrict__ keys, uint64_t u, uint32_t lg,
+                              uint32_t* __restrict__ in_deg, uint32_t* __restrict__ out_deg) {
+    const uint64_t mask = (1ull << lg) - 1;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < u;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        atomicAdd(&in_deg[k >> lg], 1u);
+        atomicAdd(&out_deg[k & mask], 1u);
+    }
+}
+
+__global__ void iota_u32(uint32_t* __restrict__ v, uint32_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        v[i] = (uint32_t)i;
+}
+
+__global__ void negate_u32(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint32_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = ~in[i];
+}
+
+__global__ void invert_perm(const uint32_t* __restrict__ old_of_new, uint32_t* __restrict__ new_of_old,
+                            uint32_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        new_of_old[old_of_new[i]] = (uint32_t)i;
+}
+
+__global__ void relabel_keys(uint64_t* __restrict__ keys, uint64_t u, uint32_t lg,
+                             const uint32_t* __restrict__ map) {
+    const uint64_t mask = (1ull << lg) - 1;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < u;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        keys[i] = ((uint64_t)map[k >> lg] << lg) | map[k & mask];
+    }
+}
+
+// out[i] = (u64) src[perm[i]]  (perm may be null: identity); out[n] = 0
+__global__ void gather_deg_u64(const uint32_t* __restrict__ src, const uint32_t* __restrict__ perm,
+                               uint64_t* __restrict__ out, uint32_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = (i < n) ? (uint64_t)src[perm ? perm[i] : i] : 0ull;
+}
+
+__global__ void gather_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ perm,
+                           uint32_t* __restrict__ out, uint32_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = src[perm[i]];
+}
+
+__global__ void keys_low(const uint64_t* __restrict__ keys, uint64_t u, uint32_t lg,
+                         uint32_t* __restrict__ col) {
+    const uint64_t mask = (1ull << lg) - 1;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < u;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        col[i] = (uint32_t)(keys[i] & mask);
+}
+
+// bins over rows sorted by in-degree descending: counts of rows above thresholds
+__global__ void bin_counts(const uint64_t* __restrict__ row_off, uint32_t n,
+                           unsigned long long* __restrict__ counts /*4*/) {
+    unsigned long long c0 = 0, c1 = 0, c2 = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t d = row_off[i + 1] - row_off[i];
+        c0 += d > kHubMinDegree;
+        c1 += d > kWarpMinDegree;
+        c2 += d > 0;
+    }
+    atomicAdd(&counts[0], c0);
+    atomicAdd(&counts[1], c1);
+    atomicAdd(&counts[2], c2);
+}
+
+__global__ void count_zero(const uint32_t* __restrict__ v, uint32_t n,
+                           unsigned long long* __restrict__ count) {
+    unsigned long long c = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        c += v[i] == 0;
+    atomicAdd(count, c);
+}
+
+// CSR (reference layout) -> keys, with validation
+__global__ void csr_to_keys(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr,
+                            uint32_t n, uint32_t lg, uint64_t* __restrict__ keys, int* bad) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t lo = off[v], hi = off[v + 1];
+        if (hi < lo) { *bad = 1; continue; }
+        for (uint64_t j = lo; j < hi; ++j) {
+            const uint32_t u = nbr[j];
+            if (u >= n || (j > lo && nbr[j - 1] >= u)) *bad = 1; // ascending, unique
+            keys[j] = ((uint64_t)v << lg) | u;
+        }
+    }
+}
+
+__global__ void compare_u32(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                            uint32_t n, int* bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        if (a[i] != b[i]) *bad = 1;
+}
+
+// engine CSR -> original-id keys (for download)
+__global__ void engine_to_orig_keys(const uint64_t* __restrict__ row_off,
+                                    const uint32_t* __restrict__ col,
+                                    const uint32_t* __restrict__ old_of_new, uint32_t n,
+                                    uint32_t lg, uint64_t* __restrict__ keys) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
+         r += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t dst = old_of_new[r];
+        for (uint64_t j = row_off[r]; j < row_off[r + 1]; ++j)
+            keys[j] = (dst << lg) | old_of_new[col[j]];
+    }
+}
+
+__global__ void in_deg_orig(const uint64_t* __restrict__ row_off,
+                            const uint32_t* __restrict__ new_of_old, uint32_t n,
+                            uint64_t* __restrict__ out) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        if (v == n) { out[v] = 0; continue; }
+        const uint32_t r = new_of_old[v];
+        out[v] = row_off[r + 1] - row_off[r];
+    }
+}
+
+struct IsZero {
+    const uint32_t* deg;
+    __device__ bool operator()(uint32_t v) const { return deg[v] == 0; }
+};
+
+// ---- host helpers -----------------------------------------------------------------
+void sort_keys(DevBuf<uint64_t>& keys, DevBuf<uint64_t>& alt, uint64_t m, int end_bit,
+               cudaStream_t st) {
+    if (m < 2) return;
+    cub::DoubleBuffer<uint64_t> db(keys.p, alt.p);
+    size_t tmp = 0;
+    PRGPU_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, m, 0, end_bit, st));
+    DevBuf<char> t(tmp);
+    PRGPU_CUDA(cub::DeviceRadixSort::SortKeys(t.p, tmp, db, m, 0, end_bit, st));
+    g_launches.fetch_add(1);
+    if (db.Current() != keys.p) std::swap(keys, alt);
+}
+
+uint64_t unique_keys(DevBuf<uint64_t>& keys, DevBuf<uint64_t>& alt, uint64_t m, cudaStream_t st) {
+    if (m == 0) return 0;
+    DevBuf<long long> nsel(1);
+    size_t tmp = 0;
+    PRGPU_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, keys.p, alt.p, nsel.p, (int64_t)m, st));
+    DevBuf<char> t(tmp);
+    PRGPU_CUDA(cub::DeviceSelect::Unique(t.p, tmp, keys.p, alt.p, nsel.p, (int64_t)m, st));
+    g_launches.fetch_add(1);
+    long long u = 0;
+    PRGPU_CUDA(cudaMemcpyAsync(&u, nsel.p, sizeof(u), cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    std::swap(keys, alt);
+    return (uint64_t)u;
+}
+
+void exclusive_scan_u64(uint64_t* data, uint64_t count, cudaStream_t st) {
+    size_t tmp = 0;
+    PRGPU_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, data, data, (int64_t)count, st));
+    DevBuf<char> t(tmp);
+    PRGPU_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, data, data, (int64_t)count, st));
+    g_launches.fetch_add(1);
+}
+
+int read_flag(const DevBuf<int>& f, cudaStream_t st) {
+    int v = 0;
+    PRGPU_CUDA(cudaMemcpyAsync(&v, f.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    return v;
+}
+
+// Sorted unique original-id keys -> engine graph.  Consumes `keys`.
+std::unique_ptr<prgpu_graph> assemble(DevBuf<uint64_t>&& keys_in, uint64_t u, uint32_t n,
+                                      uint32_t lg, int device, cudaStream_t st,
+                                      const uint32_t* expect_out_deg /* device, optional */) {
+    DevBuf<uint64_t> keys(std::move(keys_in));
+    auto g = std::make_unique<prgpu_graph>();
+    g->device = device;
+    g->n = n;
+    g->e = u;
+    g->lg = lg;
+
+    DevBuf<uint32_t> in_deg(n), out_deg(n);
+    PRGPU_CUDA(cudaMemsetAsync(in_deg.p, 0, n * sizeof(uint32_t), st));
+    PRGPU_CUDA(cudaMemsetAsync(out_deg.p, 0, n * sizeof(uint32_t), st));
+    if (u) {
+        count_degrees<<<grid_for(u), kThreads, 0, st>>>(keys.p, u, lg, in_deg.p, out_deg.p);
+        PRGPU_LAUNCHED("count_degrees");
+    }
+    if (expect_out_deg) {
+        DevBuf<int> bad(1);
+        PRGPU_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+        compare_u32<<<grid_for(n), kThreads, 0, st>>>(out_deg.p, expect_out_deg, n, bad.p);
+        PRGPU_LAUNCHED("compare_u32");
+        if (read_flag(bad, st))
+            fail(PRGPU_EINVAL, "graph_from_csr: out_degree does not match in_neighbors");
+    }
+
+    // relabel: stable sort of vertices by ~in_degree (= in-degree descending)
+    {
+        DevBuf<uint32_t> kin(n), kout(n), vin(n);
+        g->old_of_new.alloc(n);
+        negate_u32<<<grid_for(n), kThreads, 0, st>>>(in_deg.p, kin.p, n);
+        PRGPU_LAUNCHED("negate_u32");
+        iota_u32<<<grid_for(n), kThreads, 0, st>>>(vin.p, n);
+        PRGPU_LAUNCHED("iota_u32");
+        size_t tmp = 0;
+        PRGPU_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin.p, kout.p, vin.p,
+                                                   g->old_of_new.p, (int64_t)n, 0, 32, st));
+        DevBuf<char> t(tmp);
+        PRGPU_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, kin.p, kout.p, vin.p,
+                                                   g->old_of_new.p, (int64_t)n, 0, 32, st));
+        g_launches.fetch_add(1);
+        g->new_of_old.alloc(n);
+        invert_perm<<<grid_for(n), kThreads, 0, st>>>(g->old_of_new.p, g->new_of_old.p, n);
+        PRGPU_LAUNCHED("invert_perm");
+    }
+
+    // engine edges: relabel both endpoints, sort (rows ascending, sources ascending)
+    if (u) {
+        relabel_keys<<<grid_for(u), kThreads, 0, st>>>(keys.p, u, lg, g->new_of_old.p);
+        PRGPU_LAUNCHED("relabel_keys");
+        DevBuf<uint64_t> alt(u);
+        sort_keys(keys, alt, u, 2 * (int)lg, st);
+    }
+    g->row_off.alloc((size_t)n + 1);
+    gather_deg_u64<<<grid_for((uint64_t)n + 1), kThreads, 0, st>>>(in_deg.p, g->old_of_new.p,
+                                                                    g->row_off.p, n);
+    PRGPU_LAUNCHED("gather_deg_u64");
+    exclusive_scan_u64(g->row_off.p, (uint64_t)n + 1, st);
+    g->col.alloc(u + 16);
+    PRGPU_CUDA(cudaMemsetAsync(g->col.p, 0, (u + 16) * sizeof(uint32_t), st));
+    if (u) {
+        keys_low<<<grid_for(u), kThreads, 0, st>>>(keys.p, u, lg, g->col.p);
+        PRGPU_LAUNCHED("keys_low");
+    }
+    keys.reset();
+    g->deg.alloc(n);
+    gather_u32<<<grid_for(n), kThreads, 0, st>>>(out_deg.p, g->old_of_new.p, g->deg.p, n);
+    PRGPU_LAUNCHED("gather_u32");
+
+    DevBuf<unsigned long long> counts(4);
+    PRGPU_CUDA(cudaMemsetAsync(counts.p, 0, 4 * sizeof(unsigned long long), st));
+    bin_counts<<<grid_for(n), kThreads, 0, st>>>(g->row_off.p, n, counts.p);
+    PRGPU_LAUNCHED("bin_counts");
+    count_zero<<<grid_for(n), kThreads, 0, st>>>(out_deg.p, n, counts.p + 3);
+    PRGPU_LAUNCHED("count_zero");
+    unsigned long long c[4];
+    uint64_t first_two[2];
+    PRGPU_CUDA(cudaMemcpyAsync(c, counts.p, sizeof(c), cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaMemcpyAsync(first_two, g->row_off.p, sizeof(first_two),
+                               cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    g->hub_end = (uint32_t)c[0];
+    g->warp_end = (uint32_t)c[1];
+    g->nonempty_end = (uint32_t)c[2];
+    g->ndangling = (uint32_t)c[3];
+    g->max_in_degree = (uint32_t)(first_two[1] - first_two[0]);
+    return g;
+}
+
+} // namespace
+
+std::unique_ptr<prgpu_graph> graph_build_device(uint32_t n, const uint32_t* d_pairs, uint64_t m,
+                                                int device, cudaStream_t st) {
+    if (n == 0) fail(PRGPU_EINVAL, "build_csr: vertex_count must be >= 1");
+    const uint32_t lg = bits_for(n);
+    DevBuf<uint64_t> keys(std::max<uint64_t>(m, 1));
+    if (m) {
+        DevBuf<int> bad(1);
+        PRGPU_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+        pairs_to_keys<<<grid_for(m), kThreads, 0, st>>>(d_pairs, m, n, lg, keys.p, bad.p);
+        PRGPU_LAUNCHED("pairs_to_keys");
+        if (read_flag(bad, st)) fail(PRGPU_EINVAL, "build_csr: edge endpoint >= vertex_count");
+        DevBuf<uint64_t> alt(m);
+        sort_keys(keys, alt, m, 2 * (int)lg, st);
+        m = unique_keys(keys, alt, m, st);
+    }
+    return assemble(std::move(keys), m, n, lg, device, st, nullptr);
+}
+
+std::unique_ptr<prgpu_graph> graph_build_host(uint32_t n, const uint32_t* pairs, uint64_t m,
+                                              int device, cudaStream_t st) {
+    DevBuf<uint32_t> d(std::max<uint64_t>(2 * m, 2));
+    if (m)
+        PRGPU_CUDA(cudaMemcpyAsync(d.p, pairs, 2 * m * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    return graph_build_device(n, d.p, m, device, st);
+}
+
+std::unique_ptr<prgpu_graph> graph_from_csr(uint32_t n, const uint64_t* off, const uint32_t* nbr,
+                                            const uint32_t* out_degree, int device,
+                                            cudaStream_t st) {
+    if (n == 0) fail(PRGPU_EINVAL, "graph_from_csr: vertex_count must be >= 1");
+    if (off[0] != 0) fail(PRGPU_EINVAL, "graph_from_csr: in_offsets[0] != 0");
+    const uint64_t e = off[n];
+    const uint32_t lg = bits_for(n);
+    DevBuf<uint64_t> d_off((size_t)n + 1);
+    DevBuf<uint32_t> d_nbr(std::max<uint64_t>(e, 1)), d_deg(n);
+    PRGPU_CUDA(cudaMemcpyAsync(d_off.p, off, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, st));
+    if (e) PRGPU_CUDA(cudaMemcpyAsync(d_nbr.p, nbr, e * 4, cudaMemcpyHostToDevice, st));
+    PRGPU_CUDA(cudaMemcpyAsync(d_deg.p, out_degree, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    DevBuf<uint64_t> keys(std::max<uint64_t>(e, 1));
+    DevBuf<int> bad(1);
+    PRGPU_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    csr_to_keys<<<grid_for(n), kThreads, 0, st>>>(d_off.p, d_nbr.p, n, lg, keys.p, bad.p);
+    PRGPU_LAUNCHED("csr_to_keys");
+    if (read_flag(bad, st))
+        fail(PRGPU_EINVAL, "graph_from_csr: offsets not monotone or neighbours not ascending/unique/in range");
+    d_nbr.reset();
+    d_off.reset();
+    return assemble(std::move(keys), e, n, lg, device, st, d_deg.p);
+}
+
+std::unique_ptr<prgpu_graph> graph_generate_rmat(uint32_t scale, uint32_t ef, double a, double b,
+                                                 double c, uint64_t seed, int device,
+                                                 cudaStream_t st) {
+    if (scale < 1 || scale > 30) fail(PRGPU_EINVAL, "rmat: scale must be in [1, 30]");
+    if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0))
+        fail(PRGPU_EINVAL, "rmat: probabilities must be >= 0 with a+b+c <= 1");
+    const uint32_t n = 1u << scale;
+    const uint64_t m = (uint64_t)ef << scale;
+    PermKeys pk;
+    const uint64_t pkey = stream_key(seed, 2);
+    for (int r = 0; r < 3; ++r) pk.k[r] = mix64_host(pkey + (uint64_t)r);
+    pk.mask = (1ull << scale) - 1;
+    pk.hs = (scale + 1) / 2;
+    DevBuf<uint64_t> keys(std::max<uint64_t>(m, 1));
+    if (m) {
+        rmat_keys<<<grid_for(m), kThreads, 0, st>>>(m, scale, stream_key(seed, 1), prob_threshold(a),
+                                                    prob_threshold(a + b), prob_threshold(a + b + c),
+                                                    pk, keys.p);
+        PRGPU_LAUNCHED("rmat_keys");
+    }
+    uint64_t u = 0;
+    if (m) {
+        DevBuf<uint64_t> alt(m);
+        sort_keys(keys, alt, m, 2 * (int)scale, st);
+        u = unique_keys(keys, alt, m, st);
+        uint64_t last = 0;
+        PRGPU_CUDA(cudaMemcpyAsync(&last, keys.p + (u - 1), 8, cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaStreamSynchronize(st));
+        if (last == kSentinel) --u; // self-loop slots
+    }
+    return assemble(std::move(keys), u, n, scale, device, st, nullptr);
+}
+
+std::unique_ptr<prgpu_graph> graph_generate_grid(uint32_t side, double p, double lr, uint64_t seed,
+                                                 int device, cudaStream_t st) {
+    if (side < 2 || (uint64_t)side * side > 0xFFFFFFFFull)
+        fail(PRGPU_EINVAL, "grid: side must be >= 2 and side^2 < 2^32");
+    const uint64_t n = (uint64_t)side * side;
+    const uint32_t lg = bits_for(n);
+    const uint64_t uh = (uint64_t)side * (side - 1);
+    const uint64_t L = (uint64_t)(lr * (double)n);
+    const uint64_t m = 4 * uh + L;
+    DevBuf<uint64_t> keys(m);
+    grid_keys<<<grid_for(2 * uh + L), kThreads, 0, st>>>(side, uh, prob_threshold(p),
+                                                         stream_key(seed, 3), L, stream_key(seed, 4),
+                                                         n, lg, keys.p);
+    PRGPU_LAUNCHED("grid_keys");
+    DevBuf<uint64_t> alt(m);
+    sort_keys(keys, alt, m, 2 * (int)lg, st);
+    uint64_t u = unique_keys(keys, alt, m, st);
+    alt.reset();
+    uint64_t last = 0;
+    PRGPU_CUDA(cudaMemcpyAsync(&last, keys.p + (u - 1), 8, cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    if (last == kSentinel) --u;
+    return assemble(std::move(keys), u, (uint32_t)n, lg, device, st, nullptr);
+}
+
+void graph_download(const prgpu_graph* g, uint64_t* h_off, uint32_t* h_nbr, uint32_t* h_deg,
+                    uint32_t* h_dang, cudaStream_t st) {
+    const uint32_t n = g->n;
+    const uint64_t e = g->e;
+    if (h_deg || h_dang) {
+        DevBuf<uint32_t> deg(n);
+        gather_u32<<<grid_for(n), kThreads, 0, st>>>(g->deg.p, g->new_of_old.p, deg.p, n);
+        PRGPU_LAUNCHED("gather_u32");
+        if (h_deg)
+            PRGPU_CUDA(cudaMemcpyAsync(h_deg, deg.p, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+        if (h_dang && g->ndangling) {
+            DevBuf<uint32_t> out(g->ndangling);
+            DevBuf<long long> nsel(1);
+            cub::CountingInputIterator<uint32_t> it(0);
+            IsZero pred{deg.p};
+            size_t tmp = 0;
+            PRGPU_CUDA(cub::DeviceSelect::If(nullptr, tmp, it, out.p, nsel.p, (int64_t)n, pred, st));
+            DevBuf<char> t(tmp);
+            PRGPU_CUDA(cub::DeviceSelect::If(t.p, tmp, it, out.p, nsel.p, (int64_t)n, pred, st));
+            g_launches.fetch_add(1);
+            PRGPU_CUDA(cudaMemcpyAsync(h_dang, out.p, (size_t)g->ndangling * 4,
+                                       cudaMemcpyDeviceToHost, st));
+            PRGPU_CUDA(cudaStreamSynchronize(st));
+        }
+        PRGPU_CUDA(cudaStreamSynchronize(st));
+    }
+    if (h_off) {
+        DevBuf<uint64_t> off((size_t)n + 1);
+        in_deg_orig<<<grid_for((uint64_t)n + 1), kThreads, 0, st>>>(g->row_off.p, g->new_of_old.p,
+                                                                    n, off.p);
+        PRGPU_LAUNCHED("in_deg_orig");
+        exclusive_scan_u64(off.p, (uint64_t)n + 1, st);
+        PRGPU_CUDA(cudaMemcpyAsync(h_off, off.p, ((size_t)n + 1) * 8, cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaStreamSynchronize(st));
+    }
+    if (h_nbr && e) {
+        DevBuf<uint64_t> keys(e), alt(e);
+        engine_to_orig_keys<<<grid_for(n), kThreads, 0, st>>>(g->row_off.p, g->col.p,
+                                                              g->old_of_new.p, n, g->lg, keys.p);
+        PRGPU_LAUNCHED("engine_to_orig_keys");
+        sort_keys(keys, alt, e, 2 * (int)g->lg, st);
+        DevBuf<uint32_t> nb(e);
+        keys_low<<<grid_for(e), kThreads, 0, st>>>(keys.p, e, g->lg, nb.p);
+        PRGPU_LAUNCHED("keys_low");
+        PRGPU_CUDA(cudaMemcpyAsync(h_nbr, nb.p, e * 4, cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaStreamSynchronize(st));
+    }
+}
+
+} // namespace prgpu

@@ -1,0 +1,160 @@
+"""CPU: the oracle restatement (oracle/oracle.c) pinned against the reference.
+
+Pins: tests/golden/*.json (written from the reference itself by
+oracle/make_goldens.py) and, where oracle/_ref is built, the reference's own
+build_csr / pagerank / error_norm / generators called side by side.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLD, load_golden
+
+NORMS = ["l1", "l2", "linf"]
+
+
+def test_fixture_csr_and_runs_bit_exact(oracle, small_golden):
+    for name, fx in small_golden["fixtures"].items():
+        pairs = np.array(fx["pairs"], np.uint32)
+        g = oracle.build_csr(fx["n"], pairs)
+        for key in ("in_offsets", "in_neighbors", "out_degree", "dangling"):
+            assert getattr(g, key).tolist() == fx["csr"][key], (name, key)
+        h = oracle.build_csr_handle(fx["n"], pairs)
+        for run in fx["runs"]:
+            got = oracle.pagerank(h, run["alpha"], run["tol"], run["norm"], run["max_iter"],
+                                  trace=True)
+            assert got["iterations"] == run["iterations"], (name, run["alpha"], run["norm"])
+            assert got["converged"] == run["converged"]
+            assert got["ranks"].tolist() == run["ranks"]          # bit-exact
+            assert got["err_trace"].tolist() == run["err_trace"]  # bit-exact
+        oracle.free_csr(h)
+
+
+def test_acceptance_trials_bit_exact(oracle, small_golden):
+    """acceptance.cpp:104-132 trial set: restatement == reference, bit for bit,
+    and the dense oracle agrees (identical iterations, Linf <= 1e-8)."""
+    for t in small_golden["trials"]:
+        pairs = np.array(t["pairs"], np.uint32)
+        h = oracle.build_csr_handle(t["n"], pairs)
+        got = oracle.pagerank(h, t["alpha"], t["tol"], t["norm"], 500, trace=True)
+        oracle.free_csr(h)
+        assert got["iterations"] == t["iterations"]
+        assert got["ranks"].tolist() == t["ranks"]
+        dense = oracle.dense_pagerank(t["n"], pairs, t["alpha"], t["tol"], t["norm"])
+        assert dense["iterations"] == t["dense_iterations"] == t["iterations"]
+        assert np.max(np.abs(dense["ranks"] - np.array(t["ranks"]))) <= 1e-8
+
+
+def test_known_answers(oracle, small_golden):
+    k = small_golden["known"]
+    for a, tol, want in k["estimates"]:
+        assert oracle.estimate_iterations(a, tol) == want
+    for bad in [(1.0, 1e-6), (0.0, 1e-6), (0.85, 1.0), (0.85, 0.0)]:
+        with pytest.raises(ValueError):
+            oracle.estimate_iterations(*bad)
+    n, pairs = oracle.regular_ring(1000, 3)
+    h = oracle.build_csr_handle(n, pairs)
+    for norm, tol, it in k["ring_1000_3"]:
+        assert oracle.pagerank(h, 0.85, tol, norm)["iterations"] == it == 1
+    oracle.free_csr(h)
+    # star closed form (test_pagerank.cpp:34-38,69-87)
+    h = oracle.build_csr_handle(3, np.array([1, 0, 2, 0], np.uint32))
+    r = oracle.pagerank(h, 0.85, 1e-10, "l1")
+    c = 1.0 / (3.0 + 2 * 0.85)
+    assert np.allclose(r["ranks"], [(1 + 2 * 0.85) * c, c, c], rtol=1e-6)
+    oracle.free_csr(h)
+
+
+def test_scale_free_damping_and_sensitivity(oracle, small_golden):
+    sf = small_golden["known"]["scale_free_10k"]
+    rng = oracle.mt19937(2021)
+    n, pairs = oracle.scale_free_web(rng, 10000, 4, 0.08)
+    assert n == sf["n"] and pairs.size // 2 == sf["m"]
+    h = oracle.build_csr_handle(n, pairs)
+    for a, it in sf["damping"].items():
+        assert oracle.pagerank(h, float(a), 1e-6, "l1")["iterations"] == it
+    up = sf["damping"]["0.95"] / sf["damping"]["0.85"]
+    down = sf["damping"]["0.75"] / sf["damping"]["0.85"]
+    assert 2.0 <= up <= 4.0 and 0.4 <= down <= 0.8  # acceptance.cpp:314-329
+    for tr in sf["sensitivity_alpha095"]["traces"]:
+        got = oracle.pagerank(h, 0.95, 1e-300, tr["norm"], 500, trace=True)
+        assert got["err_trace"].tolist() == tr["err_trace"]
+    r = oracle.pagerank(h, 0.85, 1e-6, "l1")
+    assert r["ranks"].tolist() == sf["ranks_085"]
+    oracle.free_csr(h)
+
+
+def test_norm_hand_values(oracle):
+    # test_norms.cpp:17-24
+    r, s = np.array([0.3, 0.7]), np.array([0.5, 0.5])
+    assert abs(oracle.error_norm("l1", r, s) - 0.4) < 1e-12
+    assert abs(oracle.error_norm("linf", r, s) - 0.2) < 1e-12
+    assert abs(oracle.error_norm("l2", r, s) - np.sqrt(0.08)) < 1e-12
+    for k in NORMS:
+        assert oracle.error_norm(k, r, r) == 0.0
+
+
+def test_c1_golden(oracle):
+    gold = load_golden("c1_rmat16.json")
+    arr = np.load(os.path.join(GOLD, "c1_rmat16.npz"))
+    n, pairs = oracle.rmat(16, 16, 0.57, 0.19, 0.19, gold["seed"])
+    assert oracle.hash64(pairs) == gold["graph"]["h_pairs"]
+    g = oracle.build_csr(n, pairs)
+    assert oracle.hash64(g.in_offsets) == gold["graph"]["h_offsets"]
+    assert oracle.hash64(g.in_neighbors) == gold["graph"]["h_neighbors"]
+    assert oracle.hash64(g.out_degree) == gold["graph"]["h_degree"]
+    assert oracle.hash64(g.dangling) == gold["graph"]["h_dangling"]
+    h = oracle.build_csr_handle(n, pairs)
+    for norm in NORMS:
+        r = oracle.pagerank(h, 0.85, 1e-6, norm, trace=True)
+        assert r["iterations"] == gold["runs"][norm]["iterations"]
+        assert np.array_equal(r["ranks"], arr[f"ranks_{norm}"])
+        assert np.array_equal(r["err_trace"], arr[f"trace_{norm}"])
+    oracle.free_csr(h)
+
+
+@pytest.mark.parametrize("name,scale_or_side", [("c2_rmat22.json", 22), ("c3_grid4096.json", 4096)])
+def test_large_generator_pins(oracle, name, scale_or_side):
+    """The benchmark generators reproduce the graphs the goldens were made on
+    (hash of the raw edge list; CSR hashes are checked in the GPU tests)."""
+    path = os.path.join(GOLD, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not generated")
+    gold = load_golden(name)
+    if name.startswith("c2"):
+        n, pairs = oracle.rmat(22, 16, 0.57, 0.19, 0.19, gold["seed"])
+    else:
+        n, pairs = oracle.grid(4096, 0.6, 0.01, gold["seed"])
+    assert n == gold["graph"]["n"]
+    assert pairs.size // 2 == gold["graph"]["raw_edges"]
+    assert oracle.hash64(pairs) == gold["graph"]["h_pairs"]
+
+
+def test_restatement_matches_reference_live(oracle, ref):
+    """Side by side with the reference's own code on fresh random inputs."""
+    o_rng, r_rng = oracle.mt19937(77), ref.rng(77)
+    for trial in range(30):
+        n = 2 + trial
+        a = oracle.random_digraph(o_rng, n, 0.2, trial % 2 == 0)
+        b = ref.random_digraph(r_rng, n, 0.2, trial % 2 == 0)
+        assert a[0] == b[0] and np.array_equal(a[1], b[1])
+    ref.rng_free(r_rng)
+    n, pairs = oracle.rmat(12, 16, 0.57, 0.19, 0.19, 5)
+    go, gr = oracle.build_csr(n, pairs), ref.build_csr(n, pairs)
+    for key in ("in_offsets", "in_neighbors", "out_degree", "dangling"):
+        assert np.array_equal(getattr(go, key), getattr(gr, key))
+    ho, hr = oracle.build_csr_handle(n, pairs), ref.build_csr_handle(n, pairs)
+    for norm in NORMS:
+        for alpha in (0.0, 0.6, 1.0):
+            x = oracle.pagerank(ho, alpha, 1e-9, norm, trace=True)
+            y = ref.pagerank(hr, alpha, 1e-9, norm, trace=True)
+            assert x["iterations"] == y["iterations"]
+            assert np.array_equal(x["ranks"], y["ranks"])
+            assert np.array_equal(x["err_trace"], y["err_trace"])
+    rs = np.random.default_rng(3).random((2, 100))
+    for norm in NORMS:
+        assert oracle.error_norm(norm, rs[0], rs[1]) == ref.error_norm(norm, rs[0], rs[1])
+    oracle.free_csr(ho)
+    ref.free_csr(hr)

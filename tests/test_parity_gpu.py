@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's goldens
+and the oracle restatement on the same seeded inputs.
+
+Bars (BASELINE.json north_star): CSR arrays bit-identical to build_csr;
+iteration counts exactly equal (or +-1 only where the reference's final delta
+is within 1e-3*tau of tau); ranks within Linf 1e-10 of the reference's.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLD, load_golden
+
+pytestmark = pytest.mark.gpu
+
+RANK_TOL = 1e-10  # Linf, fp64 (north_star)
+NORMS = ["l1", "l2", "linf"]
+
+
+def nk(prl, name):
+    return {"l1": prl.NormKind.L1, "l2": prl.NormKind.L2, "linf": prl.NormKind.LInf}[name]
+
+
+def iterations_match(got, want, trace, tol):
+    """Exact, or +-1 where the reference's err at the crossing is within 1e-3*tau of tau."""
+    if got == want:
+        return True
+    if abs(got - want) != 1:
+        return False
+    t = min(got, want)
+    cand = [trace[i] for i in (t - 1, t) if 0 <= i < len(trace)]
+    return any(abs(e - tol) <= 1e-3 * tol for e in cand)
+
+
+def edge_list(prl, n, pairs):
+    return prl.EdgeList(n, np.asarray(pairs, np.uint32).reshape(-1, 2))
+
+
+# ---------------------------------------------------------------------------
+def test_fixtures_csr_and_runs(prl, small_golden):
+    for name, fx in small_golden["fixtures"].items():
+        g = prl.build_csr(edge_list(prl, fx["n"], fx["pairs"]))
+        assert g.in_offsets.tolist() == fx["csr"]["in_offsets"], name
+        assert g.in_neighbors.tolist() == fx["csr"]["in_neighbors"], name
+        assert g.out_degree.tolist() == fx["csr"]["out_degree"], name
+        assert g.dangling.tolist() == fx["csr"]["dangling"], name
+        for run in fx["runs"]:
+            cfg = prl.PageRankConfig(run["alpha"], run["tol"], nk(prl, run["norm"]), run["max_iter"])
+            r = prl.pagerank(g, cfg)
+            assert iterations_match(r.iterations, run["iterations"], run["err_trace"], run["tol"]), \
+                (name, run["alpha"], run["norm"], r.iterations, run["iterations"])
+            assert r.converged == run["converged"]
+            assert np.max(np.abs(r.ranks - np.array(run["ranks"]))) <= RANK_TOL
+
+
+def test_acceptance_trials(prl, small_golden):
+    """acceptance.cpp:104-132: 220 random digraphs (seed 4242, half with forced
+    dangling vertices) against the reference's results and the dense oracle."""
+    for i, t in enumerate(small_golden["trials"]):
+        g = prl.build_csr(edge_list(prl, t["n"], t["pairs"]))
+        cfg = prl.PageRankConfig(t["alpha"], t["tol"], nk(prl, t["norm"]), 500)
+        r = prl.pagerank(g, cfg)
+        assert iterations_match(r.iterations, t["iterations"], t["err_trace"], t["tol"]), i
+        assert np.max(np.abs(r.ranks - np.array(t["ranks"]))) <= RANK_TOL, i
+        assert np.max(np.abs(r.ranks - np.array(t["dense_ranks"]))) <= 1e-8, i
+
+
+def test_known_answers(prl):
+    el = lambda n, e: prl.EdgeList(n, np.array(e, np.uint32).reshape(-1, 2))  # noqa: E731
+    two = prl.build_csr(el(2, [[0, 1], [1, 0]]))
+    for a in (0.0, 0.5, 0.85, 1.0):  # test_pagerank.cpp:49-58
+        r = prl.pagerank(two, prl.PageRankConfig(alpha=a))
+        assert r.iterations == 1 and r.converged and np.allclose(r.ranks, 0.5, rtol=1e-12)
+    one = prl.build_csr(prl.EdgeList(1))  # :60-67
+    r = prl.pagerank(one, prl.PageRankConfig(alpha=0.85))
+    assert r.iterations == 1 and r.converged and abs(r.ranks[0] - 1.0) <= 1e-14
+    star = prl.build_csr(el(3, [[1, 0], [2, 0]]))  # :69-87
+    r = prl.pagerank(star, prl.PageRankConfig(0.85, 1e-10))
+    c = 1.0 / (3.0 + 2 * 0.85)
+    assert r.converged and np.allclose(r.ranks, [(1 + 1.7) * c, c, c], rtol=1e-6)
+    for bad in (dict(alpha=1.5), dict(alpha=-0.1), dict(tolerance=0.0), dict(max_iterations=0)):
+        with pytest.raises(ValueError):  # :89-100
+            prl.pagerank(two, prl.PageRankConfig(**bad))
+    with pytest.raises(ValueError):
+        prl.build_csr(prl.EdgeList(0))
+    # iteration cap honesty (:228-237)
+    web = prl.build_csr(el(6, [[0, 1], [0, 2], [1, 2], [2, 0], [3, 2], [4, 0], [4, 3], [2, 4], [1, 5]]))
+    r = prl.pagerank(web, prl.PageRankConfig(1.0, 1e-15, prl.NormKind.L1, 50))
+    assert r.iterations == 50 and not r.converged
+    r = prl.pagerank(web, prl.PageRankConfig(0.85, 1e-12, prl.NormKind.L1, 2))
+    assert r.iterations == 2 and not r.converged
+    # reference error (:239-261)
+    assert prl.reference_error(star, prl.reference_ranks(star)) == 0.0
+    e75 = prl.pagerank(star, prl.PageRankConfig(0.75, 1e-12))
+    c75, c85 = 1 / (3 + 1.5), 1 / (3 + 1.7)
+    expected = abs(2.5 * c75 - 2.7 * c85) + 2 * abs(c75 - c85)
+    assert math.isclose(prl.reference_error(star, e75.ranks), expected, rel_tol=1e-4)
+
+
+def test_ring_single_iteration(prl, oracle):
+    """acceptance.cpp:248-259: k-regular ring, 1 iteration for every tau and norm."""
+    n, pairs = oracle.regular_ring(100000, 3)
+    g = prl.build_csr(edge_list(prl, n, pairs))
+    assert g.dangling.size == 0
+    for norm in prl.all_norms:
+        for tol in prl.default_tolerance_grid():
+            r = prl.pagerank(g, prl.PageRankConfig(0.85, tol, norm))
+            assert r.iterations == 1 and r.converged
+
+
+def test_observer_rank_conservation_and_floor(prl, oracle):
+    """test_pagerank.cpp:118-146, acceptance.cpp:134-161: sum = 1 +- 1e-9 and the
+    teleport floor on every iteration, seen through the observer."""
+    rng = oracle.mt19937(11)
+    for trial in range(8):
+        n, pairs = oracle.random_digraph(rng, 2 + trial * 5, 0.2, True)
+        g = prl.build_csr(edge_list(prl, n, pairs))
+        seen = []
+
+        def obs(it, ranks, err):
+            seen.append(it)
+            assert abs(float(np.sum(ranks.astype(np.longdouble))) - 1.0) <= 1e-9
+            assert np.all(ranks >= (1 - 0.85) / n * (1 - 1e-12))
+
+        r = prl.pagerank(g, prl.PageRankConfig(0.85, 1e-9), obs)
+        assert seen == list(range(1, r.iterations + 1))
+
+
+def test_norm_and_alpha_ordering(prl, oracle):
+    rng = oracle.mt19937(17)
+    for trial in range(6):
+        n, pairs = oracle.random_digraph(rng, 3 + 7 * trial, 0.2, True)
+        g = prl.build_csr(edge_list(prl, n, pairs))
+        for a in (0.7, 0.85, 0.95):
+            its = [prl.pagerank(g, prl.PageRankConfig(a, 1e-6, nm)).iterations for nm in prl.all_norms]
+            assert its[2] <= its[1] <= its[0]
+        prev = 0
+        for a in prl.default_damping_grid():
+            it = prl.pagerank(g, prl.PageRankConfig(a, 1e-6)).iterations
+            assert it >= prev
+            prev = it
+
+
+def test_error_norm_device(prl):
+    r, s = [0.3, 0.7], [0.5, 0.5]
+    assert math.isclose(prl.error_norm(prl.NormKind.L1, r, s), 0.4, rel_tol=1e-12)
+    assert math.isclose(prl.error_norm(prl.NormKind.LInf, r, s), 0.2, rel_tol=1e-12)
+    assert math.isclose(prl.error_norm(prl.NormKind.L2, r, s), math.sqrt(0.08), rel_tol=1e-12)
+    with pytest.raises(ValueError):
+        prl.error_norm(prl.NormKind.L1, [0.5, 0.5], [1.0])
+    with pytest.raises(ValueError):
+        prl.error_norm(prl.NormKind.L2, [], [])
+
+
+def test_from_csr_roundtrip_and_validation(prl, oracle):
+    n, pairs = oracle.rmat(12, 16, 0.57, 0.19, 0.19, 9)
+    want = oracle.build_csr(n, pairs)
+    g = prl.csr_from_arrays(n, want.in_offsets, want.in_neighbors, want.out_degree)
+    assert np.array_equal(g.in_offsets, want.in_offsets)
+    assert np.array_equal(g.in_neighbors, want.in_neighbors)
+    assert np.array_equal(g.dangling, want.dangling)
+    bad = want.in_neighbors.copy()
+    bad[0], bad[1] = bad[1], bad[0]
+    if want.in_offsets[1] >= 2:
+        with pytest.raises(ValueError):
+            prl.csr_from_arrays(n, want.in_offsets, bad, want.out_degree)
+    with pytest.raises(ValueError):
+        prl.build_csr(prl.EdgeList(3, np.array([[0, 5]], np.uint32)))
+
+
+# ---------------------------------------------------------------------------
+# Benchmark configs (BASELINE.json) — device generators, then parity
+# ---------------------------------------------------------------------------
+def graph_hashes(oracle, g):
+    return dict(h_offsets=oracle.hash64(g.in_offsets), h_neighbors=oracle.hash64(g.in_neighbors),
+                h_degree=oracle.hash64(g.out_degree), h_dangling=oracle.hash64(g.dangling))
+
+
+def test_c1_rmat16(prl, oracle):
+    gold = load_golden("c1_rmat16.json")
+    arr = np.load(os.path.join(GOLD, "c1_rmat16.npz"))
+    g = prl.generate_rmat(16, 16, 0.57, 0.19, 0.19, gold["seed"])
+    assert g.vertex_count == gold["graph"]["n"] and g.edge_count() == gold["graph"]["e"]
+    for k, v in graph_hashes(oracle, g).items():
+        assert v == gold["graph"][k], k
+    # host-generated pairs through build_csr agree too
+    n, pairs = oracle.rmat(16, 16, 0.57, 0.19, 0.19, gold["seed"])
+    g2 = prl.build_csr(edge_list(prl, n, pairs))
+    assert graph_hashes(oracle, g2) == graph_hashes(oracle, g)
+    for norm in NORMS:
+        r = prl.pagerank(g, prl.PageRankConfig(0.85, 1e-6, nk(prl, norm)))
+        tr = arr[f"trace_{norm}"]
+        assert iterations_match(r.iterations, gold["runs"][norm]["iterations"], tr, 1e-6), norm
+        assert np.max(np.abs(r.ranks - arr[f"ranks_{norm}"])) <= RANK_TOL
+
+
+def test_c1_determinism_and_batched_lanes(prl):
+    g = prl.generate_rmat(16, 16, 0.57, 0.19, 0.19, 2108)
+    a = prl.pagerank(g, prl.PageRankConfig(0.85, 1e-8))
+    b = prl.pagerank(g, prl.PageRankConfig(0.85, 1e-8))
+    assert np.array_equal(a.ranks, b.ranks) and a.iterations == b.iterations
+    alphas = [0.5, 0.6, 0.75, 0.85, 0.95]
+    br = prl.pagerank_batched(g, alphas, 1e-8)
+    for k, al in enumerate(alphas):
+        one = prl.pagerank(g, prl.PageRankConfig(al, 1e-8))
+        assert br.results[k].iterations == one.iterations
+        assert np.max(np.abs(br.results[k].ranks - one.ranks)) <= 1e-13
+
+
+def test_c2_rmat22_damping_sweep(prl, oracle):
+    gold = load_golden("c2_rmat22.json")
+    arr = np.load(os.path.join(GOLD, "c2_rmat22.npz"))
+    g = prl.generate_rmat(22, 16, 0.57, 0.19, 0.19, gold["seed"])
+    assert g.edge_count() == gold["graph"]["e"]
+    for k, v in graph_hashes(oracle, g).items():
+        assert v == gold["graph"][k], k
+    alphas = [ln["alpha"] for ln in gold["lanes"]]
+    ref = prl.reference_ranks(g)
+    br = prl.pagerank_batched(g, alphas, 1e-6, prl.NormKind.L1, 500, ref_ranks=ref)
+    idx = arr["sample_idx"]
+    for k, ln in enumerate(gold["lanes"]):
+        r = br.results[k]
+        assert iterations_match(r.iterations, ln["iterations"], arr[f"lane{k}_trace"], 1e-6), k
+        assert r.converged == ln["converged"]
+        assert np.max(np.abs(r.ranks[idx] - arr[f"lane{k}_sample"])) <= RANK_TOL
+        assert np.max(np.abs(r.ranks[arr[f"lane{k}_top_idx"]] - arr[f"lane{k}_top"])) <= RANK_TOL
+        assert abs(float(np.sum(r.ranks.astype(np.longdouble))) - float(arr[f"lane{k}_total"])) <= 1e-9
+        err = float(br.trace[r.iterations - 1, k, 3])
+        assert math.isclose(err, ln["err_vs_ref"], rel_tol=1e-6, abs_tol=1e-12), k
+
+
+def test_c3_grid_tolerance_norm_sweep(prl, oracle):
+    path = os.path.join(GOLD, "c3_grid4096.json")
+    if not os.path.exists(path):
+        pytest.skip("c3 golden not generated")
+    gold = load_golden("c3_grid4096.json")
+    arr = np.load(os.path.join(GOLD, "c3_grid4096.npz"))
+    g = prl.generate_grid(4096, 0.6, 0.01, gold["seed"])
+    assert g.edge_count() == gold["graph"]["e"]
+    for k, v in graph_hashes(oracle, g).items():
+        assert v == gold["graph"][k], k
+    taus = [10.0 ** -k for k in range(1, 11)]
+    plan = prl.SweepPlan(graphs=["grid4096"], alphas=[0.85], tolerances=taus,
+                         norms=list(prl.all_norms), repeats=1)
+    recs = prl.run_sweep(plan, graphs_override={"grid4096": g})
+    assert len(recs) == 30
+    want = {(c["norm"], c["tol"]): c for c in gold["cells"]}
+    for rec in recs:
+        c = want[(prl.norm_name(rec.norm), rec.tolerance)]
+        tr = arr[f"trace_{prl.norm_name(rec.norm)}"]
+        assert iterations_match(rec.iterations, c["iterations"], tr, rec.tolerance), c
+        assert rec.converged == c["converged"]
+        assert math.isclose(rec.err_vs_ref, c["err_vs_ref"], rel_tol=1e-6, abs_tol=1e-13), c
+    # final ranks of the tightest cell per norm
+    idx = arr["sample_idx"]
+    for norm in NORMS:
+        r = prl.pagerank(g, prl.PageRankConfig(0.85, 1e-10, nk(prl, norm)))
+        assert r.iterations == gold["runs"][norm]["iterations"]
+        assert np.max(np.abs(r.ranks[idx] - arr[f"{norm}_final_sample"])) <= RANK_TOL
