@@ -40,6 +40,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 SEED = 2108
 ALPHAS = [0.50, 0.55, 0.60, 0.65, 0.70, 0.75, 0.80, 0.85, 0.90, 0.95, 1.00]
@@ -48,6 +49,8 @@ CONFIGS = {
     "c2": dict(workload="C2 damping sweep: RMAT-22 ef16 a/b/c=.57/.19/.19 seed 2108, "
                         "K=11 alphas .50..1.00 batched, tau 1e-6, L1, max 500 it, fp64",
                kind="rmat", scale=22, alphas=ALPHAS, tol=1e-6, norm=0),
+    "c2k1": dict(workload="C2 graph, single lane alpha .85 tau 1e-6 L1", kind="rmat", scale=22,
+                 alphas=[0.85], tol=1e-6, norm=0),
     "c1": dict(workload="C1: RMAT-16 alpha .85 tau 1e-6 L1", kind="rmat", scale=16,
                alphas=[0.85], tol=1e-6, norm=0),
     "c3": dict(workload="C3: grid 4096^2 p .6 +1% long-range, alpha .85, all norms to tau 1e-10",

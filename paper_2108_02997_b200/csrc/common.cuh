@@ -105,8 +105,11 @@ struct prgpu_graph {
     uint32_t lg = 1; // bits per vertex id in packed edge keys
     // engine CSR, vertices relabelled by in-degree descending (ties: old id)
     prgpu::DevBuf<uint64_t> row_off;    // [n+1]
-    prgpu::DevBuf<uint32_t> col;        // [e + 16] (padding for 128-bit loads)
+    prgpu::DevBuf<uint32_t> col;        // [e + 16] source ids (padding for 128-bit loads)
     prgpu::DevBuf<uint32_t> deg;        // [n] out-degree, engine ids
+    prgpu::DevBuf<uint2> rowinfo;       // [n] {out-degree, source id or ~0u if dangling}
+    prgpu::DevBuf<uint32_t> row_of_src; // [nsrc] engine row of each source id
+    uint32_t nsrc = 0;                  // vertices with out-degree > 0
     prgpu::DevBuf<uint32_t> new_of_old; // [n]
     prgpu::DevBuf<uint32_t> old_of_new; // [n]
     uint32_t hub_end = 0, warp_end = 0, nonempty_end = 0;

@@ -160,10 +160,11 @@ __global__ void iota_u32(uint32_t* __restrict__ v, uint32_t n) {
         v[i] = (uint32_t)i;
 }
 
-__global__ void negate_u32(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint32_t n) {
+__global__ void degree_keys(const uint32_t* __restrict__ in_deg, const uint32_t* __restrict__ out_deg,
+                            uint64_t* __restrict__ out, uint32_t n) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
-        out[i] = ~in[i];
+        out[i] = ((uint64_t)(~in_deg[i]) << 32) | (uint32_t)(~out_deg[i]);
 }
 
 __global__ void invert_perm(const uint32_t* __restrict__ old_of_new, uint32_t* __restrict__ new_of_old,
@@ -256,13 +257,14 @@ __global__ void compare_u32(const uint32_t* __restrict__ a, const uint32_t* __re
 // engine CSR -> original-id keys (for download)
 __global__ void engine_to_orig_keys(const uint64_t* __restrict__ row_off,
                                     const uint32_t* __restrict__ col,
+                                    const uint32_t* __restrict__ row_of_src,
                                     const uint32_t* __restrict__ old_of_new, uint32_t n,
                                     uint32_t lg, uint64_t* __restrict__ keys) {
     for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
          r += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t dst = old_of_new[r];
         for (uint64_t j = row_off[r]; j < row_off[r + 1]; ++j)
-            keys[j] = (dst << lg) | old_of_new[col[j]];
+            keys[j] = (dst << lg) | old_of_new[row_of_src[col[j]]];
     }
 }
 
@@ -275,6 +277,31 @@ __global__ void in_deg_orig(const uint64_t* __restrict__ row_off,
         const uint32_t r = new_of_old[v];
         out[v] = row_off[r + 1] - row_off[r];
     }
+}
+
+__global__ void src_flags(const uint32_t* __restrict__ deg, uint32_t n, uint64_t* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = (i < n && deg[i] > 0) ? 1ull : 0ull;
+}
+
+// rowinfo[i] = {deg, src id}; row_of_src[src] = i
+__global__ void src_maps(const uint32_t* __restrict__ deg, const uint64_t* __restrict__ excl,
+                         uint32_t n, uint2* __restrict__ rowinfo, uint32_t* __restrict__ row_of_src) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t d = deg[i];
+        const uint32_t s = (uint32_t)excl[i];
+        rowinfo[i] = make_uint2(d, d ? s : 0xFFFFFFFFu);
+        if (d) row_of_src[s] = (uint32_t)i;
+    }
+}
+
+// col: engine row ids -> source ids (every in-neighbour has out-degree >= 1)
+__global__ void col_to_src(uint32_t* __restrict__ col, uint64_t e, const uint2* __restrict__ rowinfo) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
+         j += (uint64_t)gridDim.x * blockDim.x)
+        col[j] = rowinfo[col[j]].y;
 }
 
 struct IsZero {
@@ -352,20 +379,23 @@ std::unique_ptr<prgpu_graph> assemble(DevBuf<uint64_t>&& keys_in, uint64_t u, ui
             fail(PRGPU_EINVAL, "graph_from_csr: out_degree does not match in_neighbors");
     }
 
-    // relabel: stable sort of vertices by ~in_degree (= in-degree descending)
+    // relabel: stable sort of vertices by (in-degree desc, out-degree desc, id):
+    // degree bins become contiguous row ranges, and within each in-degree class
+    // the most-gathered sources (high out-degree) are packed together.
     {
-        DevBuf<uint32_t> kin(n), kout(n), vin(n);
+        DevBuf<uint64_t> kin(n), kout(n);
+        DevBuf<uint32_t> vin(n);
         g->old_of_new.alloc(n);
-        negate_u32<<<grid_for(n), kThreads, 0, st>>>(in_deg.p, kin.p, n);
-        PRGPU_LAUNCHED("negate_u32");
+        degree_keys<<<grid_for(n), kThreads, 0, st>>>(in_deg.p, out_deg.p, kin.p, n);
+        PRGPU_LAUNCHED("degree_keys");
         iota_u32<<<grid_for(n), kThreads, 0, st>>>(vin.p, n);
         PRGPU_LAUNCHED("iota_u32");
         size_t tmp = 0;
         PRGPU_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin.p, kout.p, vin.p,
-                                                   g->old_of_new.p, (int64_t)n, 0, 32, st));
+                                                   g->old_of_new.p, (int64_t)n, 0, 64, st));
         DevBuf<char> t(tmp);
         PRGPU_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, kin.p, kout.p, vin.p,
-                                                   g->old_of_new.p, (int64_t)n, 0, 32, st));
+                                                   g->old_of_new.p, (int64_t)n, 0, 64, st));
         g_launches.fetch_add(1);
         g->new_of_old.alloc(n);
         invert_perm<<<grid_for(n), kThreads, 0, st>>>(g->old_of_new.p, g->new_of_old.p, n);
@@ -394,6 +424,27 @@ std::unique_ptr<prgpu_graph> assemble(DevBuf<uint64_t>&& keys_in, uint64_t u, ui
     g->deg.alloc(n);
     gather_u32<<<grid_for(n), kThreads, 0, st>>>(out_deg.p, g->old_of_new.p, g->deg.p, n);
     PRGPU_LAUNCHED("gather_u32");
+
+    // compact source ids: contributions are stored for out-degree > 0 only
+    {
+        DevBuf<uint64_t> flags((size_t)n + 1);
+        src_flags<<<grid_for((uint64_t)n + 1), kThreads, 0, st>>>(g->deg.p, n, flags.p);
+        PRGPU_LAUNCHED("src_flags");
+        exclusive_scan_u64(flags.p, (uint64_t)n + 1, st);
+        uint64_t nsrc = 0;
+        PRGPU_CUDA(cudaMemcpyAsync(&nsrc, flags.p + n, 8, cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaStreamSynchronize(st));
+        g->nsrc = (uint32_t)nsrc;
+        g->rowinfo.alloc(n);
+        g->row_of_src.alloc(std::max<uint64_t>(nsrc, 1));
+        src_maps<<<grid_for(n), kThreads, 0, st>>>(g->deg.p, flags.p, n, g->rowinfo.p,
+                                                   g->row_of_src.p);
+        PRGPU_LAUNCHED("src_maps");
+        if (u) {
+            col_to_src<<<grid_for(u), kThreads, 0, st>>>(g->col.p, u, g->rowinfo.p);
+            PRGPU_LAUNCHED("col_to_src");
+        }
+    }
 
     DevBuf<unsigned long long> counts(4);
     PRGPU_CUDA(cudaMemsetAsync(counts.p, 0, 4 * sizeof(unsigned long long), st));
@@ -563,7 +614,8 @@ void graph_download(const prgpu_graph* g, uint64_t* h_off, uint32_t* h_nbr, uint
     if (h_nbr && e) {
         DevBuf<uint64_t> keys(e), alt(e);
         engine_to_orig_keys<<<grid_for(n), kThreads, 0, st>>>(g->row_off.p, g->col.p,
-                                                              g->old_of_new.p, n, g->lg, keys.p);
+                                                              g->row_of_src.p, g->old_of_new.p, n,
+                                                              g->lg, keys.p);
         PRGPU_LAUNCHED("engine_to_orig_keys");
         sort_keys(keys, alt, e, 2 * (int)g->lg, st);
         DevBuf<uint32_t> nb(e);

@@ -1,0 +1,659 @@
+// pull.cuh — the per-iteration pull kernel (pagerank.hpp:84-99) for sm_100a.
+//
+// One launch = one iteration of the reference's do/while loop for K rank
+// vectors ("lanes", one alpha each):
+//
+//   acc_k[v]  = sum_{u in in(v)} contrib_k[u]                  pagerank.hpp:89-91
+//   next_k[v] = c0_k + alpha_k * acc_k[v]                                   :92
+//   fused epilogue: |delta|, delta^2, max|delta| partials (norms.hpp:56-75),
+//   the next dangling sum (:85-86), contrib'_k[src(v)] = next_k[v] / d[v]
+//   (the per-edge division of :91 done once per vertex: the same IEEE value).
+//   The last CTA to finish reduces the CTA partials in a fixed order, decides
+//   convergence per lane (:95-99), computes the next teleport c0 (:87) and
+//   sets the CUDA-graph WHILE condition: no per-iteration host sync.
+//
+// Work decomposition.  Rows are sorted by (in-degree desc, out-degree desc),
+// so the degree bins are contiguous row ranges and every warp task costs about
+// the same:
+//   chunk task  (hub rows, in-degree > WIN): one warp pulls a 2*WIN-edge chunk
+//               of a long row with 128-bit colidx loads; the warp finishing the
+//               row's last chunk sums the chunk partials in chunk order and
+//               runs the epilogue (hub rows are split across warps and SMs).
+//   packed task (in-degree 1..WIN): a warp takes a run of consecutive rows
+//               holding < 2*WIN edges.  K = 1: every gather of the run is in
+//               flight at once (128-bit colidx loads), staged in shared memory,
+//               then each row is reduced in ascending source order.  K > 1: one
+//               lane group per row, accumulating in registers.
+//   empty task  (in-degree 0): such a row's rank is exactly c0 every
+//               iteration, so it is never stored: its |delta| terms are added
+//               analytically by the finalizer (n_empty * |c0_t - c0_{t-1}|,
+//               n_isolated * c0 for the dangling sum) and the task only writes
+//               the row's next contribution c0/d when it has out-edges.
+// Warps take tasks round-robin (task t -> warp t mod #warps): a static
+// assignment, so every partial sum has a fixed order and runs are
+// bit-reproducible (sweep.hpp:176-179, acceptance.cpp:331-366).  No
+// floating-point atomics anywhere.
+//
+// K lanes share every edge visit: a lane group of LG threads owns an edge (or
+// a row), thread j of the group carrying W of the lanes, so the source's K
+// contributions ([src][KS] rows) are fetched together.
+//
+// Contribution layout (HBM): the hottest sources (src < hot_src, the most
+// gathered ones, packed at the front by the relabelling) keep both parities
+// of their contribution row adjacent, [src][parity][KS], so the hot region of
+// BOTH ping-pong buffers is one contiguous range that an L2 persisting window
+// (or evict_last hints) keeps resident across iterations; colder sources are
+// stored per parity after it.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace prgpu {
+
+constexpr int kNT = 256; // threads per CTA
+constexpr int kWarps = kNT / 32;
+constexpr int kNQ = 5; // partials: L1, L2^2, Linf, dangling sum, L1-vs-ref
+
+struct LaneState {
+    double alpha;
+    double tol;
+    double c0;         // teleport for the next iteration
+    double c0_used;    // teleport of the last completed iteration (= rank of empty rows)
+    double prev_empty; // rank of empty rows before the current iteration
+    double final_err;
+    uint32_t stop_mask;
+    int report_norm;
+    int active;
+    int iterations;
+    int converged;
+    int pad;
+};
+
+struct GlobalState {
+    int iter;
+    int any_active;
+    unsigned int counter;
+    int max_iter;
+};
+
+struct Params {
+    uint32_t n, K;
+    const uint64_t* __restrict__ row_off;
+    const uint32_t* __restrict__ col;  // source ids
+    const uint2* __restrict__ rowinfo; // {out-degree, source id}
+    double* rank[2];                   // [K][n] (rows < empty_begin only)
+    double* cbase;                     // contributions, see caddr()
+    uint64_t cold_off[2];              // first cold row of each parity (in rows of KS)
+    const double* ref;                 // [n] engine ids, or null
+    double* partials;                  // [kNQ*KP][G]
+    double* trace;                     // [max_iter][K][4]
+    LaneState* lanes;                  // [K]
+    GlobalState* gs;
+    // tasks
+    const uint32_t* chunk_row;   // [n_chunk]
+    const uint32_t* chunk_first; // [n_long + 1]
+    const uint32_t* packed_r0;   // [n_packed + 1]
+    double* chunk_acc;           // [n_chunk][KP]
+    unsigned int* row_cnt;       // [n_long]
+    uint32_t n_chunk, n_packed, n_empty_tasks;
+    uint32_t empty_begin;        // first row with in-degree 0
+    uint32_t iso_begin;          // first row with in- and out-degree 0
+    uint32_t G;
+    uint32_t hot_src;            // sources [0, hot_src) in the L2-resident region
+    uint32_t l2mode;             // 0 evict hints, 1 persisting window, 2 no hints
+    uint32_t skip_mask;          // profiling only (PRGPU_SKIP): 1 chunk, 2 packed, 4 empty tasks
+    int use_cond;
+    cudaGraphConditionalHandle cond;
+};
+
+// ---- L2 residency control -------------------------------------------------------
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// streams touched once per iteration (colidx, row offsets, row info)
+__device__ __forceinline__ uint64_t stream_policy(const Params& P) {
+    return P.l2mode == 2 ? policy_evict_normal() : policy_evict_first();
+}
+// contribution of source `src`: hot ones evict_last under the hint mode
+__device__ __forceinline__ uint64_t contrib_policy(const Params& P, uint32_t src) {
+    if (P.l2mode == 0) return src < P.hot_src ? policy_evict_last() : policy_evict_first();
+    return policy_evict_normal();
+}
+
+template <int KS>
+__device__ __forceinline__ double* caddr(const Params& P, int par, uint32_t src) {
+    return src < P.hot_src ? P.cbase + ((size_t)2 * src + par) * KS
+                           : P.cbase + (P.cold_off[par] + (src - P.hot_src)) * KS;
+}
+
+__device__ __forceinline__ uint4 ld_stream_u4(const uint32_t* p, uint64_t pol) {
+    uint4 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+        : "l"(p), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ uint64_t ld_stream_u64(const uint64_t* p, uint64_t pol) {
+    uint64_t r;
+    asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ uint2 ld_stream_u2(const uint2* p, uint64_t pol) {
+    uint2 r;
+    asm("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+        : "=r"(r.x), "=r"(r.y)
+        : "l"(p), "l"(pol));
+    return r;
+}
+
+template <int W>
+__device__ __forceinline__ void load_w(const double* __restrict__ p, double (&v)[W], uint64_t pol) {
+    if constexpr (W % 2 == 0) {
+#pragma unroll
+        for (int w = 0; w < W; w += 2)
+            asm("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                : "=d"(v[w]), "=d"(v[w + 1])
+                : "l"(p + w), "l"(pol));
+    } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+            asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v[w]) : "l"(p + w), "l"(pol));
+    }
+}
+
+template <int W>
+__device__ __forceinline__ void store_w(double* p, const double (&v)[W]) {
+    if constexpr (W % 2 == 0) {
+#pragma unroll
+        for (int w = 0; w < W; w += 2) *reinterpret_cast<double2*>(p + w) = make_double2(v[w], v[w + 1]);
+    } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w) p[w] = v[w];
+    }
+}
+
+template <int W>
+__device__ __forceinline__ void store_w_pol(double* p, const double (&v)[W], uint64_t pol) {
+    if constexpr (W % 2 == 0) {
+#pragma unroll
+        for (int w = 0; w < W; w += 2)
+            asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p + w),
+                         "d"(v[w]), "d"(v[w + 1]), "l"(pol)
+                         : "memory");
+    } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+            asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p + w), "d"(v[w]), "l"(pol)
+                         : "memory");
+    }
+}
+
+// Partial quantities a kernel instance accumulates (bitmask): L1 = 1, L2 = 2,
+// Linf = 4, dangling = 8 (always), L1-vs-ref = 16.  Trimming them frees
+// registers for the wide-lane (K > 1) instances; a norm that is not computed
+// reads NaN in the trace.
+constexpr int kQmAll = 31;
+constexpr int kQmL1 = 1 | 8;
+
+template <int LG, int W, int WIN, int QJ_ = 0, int KS_ = 0>
+struct PullCfg {
+    static constexpr int KP = LG * W;
+    // contribution row stride in doubles (K rounded up to a sector multiple when
+    // the lane group is wider than K: lanes slice*W >= KS idle on loads/stores)
+    static constexpr int KS = KS_ ? KS_ : KP;
+    static constexpr int ES = 32 / LG;   // edge slots (or lane groups) per warp
+    static constexpr int EMAX = 2 * WIN; // edges per packed task / chunk
+    static constexpr int QJ = QJ_ ? QJ_ : ((4 * W <= 4) ? 4 : (4 * W <= 8 ? 2 : 1)); // quads per slot per round
+    static constexpr int ER = 8 * ES;    // rows per empty task
+    // K = 1 stages every gathered value of a run in shared memory; wider lanes
+    // accumulate in registers (staging would double the bytes moved per edge)
+    static constexpr bool STAGED = (KP == 1);
+    static constexpr int SMEM_WARP = STAGED ? EMAX * KP : 0; // doubles per warp
+};
+
+template <int LG, int W, int WIN, int QJ_ = 0, int QM = kQmAll, int KS_ = 0>
+struct Warp {
+    using C = PullCfg<LG, W, WIN, QJ_, KS_>;
+    static constexpr int KP = C::KP, ES = C::ES, KS = C::KS;
+    const Params& P;
+    const int lane, slot, slice, par;
+    const double* __restrict__ rp;
+    double* __restrict__ rn;
+    const double* s_alpha;
+    const double* s_c0;
+    const int* s_active;
+    double part[kNQ][W];
+
+    __device__ Warp(const Params& p, int parity, int ln, const double* a, const double* c0,
+                    const int* act)
+        : P(p), lane(ln), slot(ln / LG), slice(ln % LG), par(parity), rp(p.rank[parity]),
+          rn(p.rank[parity ^ 1]), s_alpha(a), s_c0(c0), s_active(act) {
+#pragma unroll
+        for (int q = 0; q < kNQ; ++q)
+#pragma unroll
+            for (int w = 0; w < W; ++w) part[q][w] = 0.0;
+    }
+
+    __device__ __forceinline__ bool lane_ok(int sl) const { return KS == KP || sl * W < KS; }
+
+    // this thread's slice holds a lane that is still iterating: frozen lanes
+    // are not gathered (lanes are ordered slowest-converging first, so the
+    // live ones share the leading sectors of each contribution row)
+    __device__ __forceinline__ bool slice_live() const {
+        if (!lane_ok(slice)) return false;
+        bool live = false;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const int k = slice * W + w;
+            live |= (k < KP) && s_active[k];
+        }
+        return live;
+    }
+
+    __device__ __forceinline__ void write_contrib(uint32_t src, int sl, const double (&cv)[W]) {
+        store_w_pol<W>(caddr<KS>(P, par ^ 1, src) + sl * W, cv, contrib_policy(P, src));
+    }
+
+    // fused epilogue for row v, lanes [sl*W, sl*W + W)
+    __device__ __forceinline__ void epilogue(uint32_t v, int sl, const double (&acc)[W]) {
+        const uint2 ri = ld_stream_u2(P.rowinfo + v, stream_policy(P));
+        const uint32_t d = ri.x;
+        const size_t n = P.n;
+        double cv[W];
+        bool any = false;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const int k = sl * W + w;
+            cv[w] = 0.0;
+            if (k < (int)P.K && s_active[k]) {
+                any = true;
+                // next[v] = teleport + alpha*acc, two roundings (pagerank.hpp:92)
+                const double r = __dadd_rn(s_c0[k], __dmul_rn(s_alpha[k], acc[w]));
+                const double o = __ldcs(rp + (size_t)k * n + v);
+                const double df = __dsub_rn(r, o);
+                const double ad = fabs(df);
+                if constexpr ((QM & 1) != 0) part[0][w] += ad;
+                if constexpr ((QM & 2) != 0) part[1][w] += df * df;
+                if constexpr ((QM & 4) != 0) part[2][w] = fmax(part[2][w], ad);
+                if (d == 0) part[3][w] += r;
+                if constexpr ((QM & 16) != 0)
+                    if (P.ref) part[4][w] += fabs(__dsub_rn(r, __ldg(P.ref + v)));
+                __stcs(rn + (size_t)k * n + v, r);
+                if (d) cv[w] = __ddiv_rn(r, (double)d); // prev[u]/out_degree[u] (:91)
+            }
+        }
+        if (d && any && lane_ok(sl)) write_contrib(ri.y, sl, cv);
+    }
+
+    // Accumulate edges [lo, hi) into acc with 128-bit colidx loads; slot s
+    // takes quads s, s+ES, ... (fixed order: quad-major, then position).
+    __device__ __forceinline__ void accumulate(uint64_t lo, uint64_t hi, double (&acc)[W]) const {
+        const uint64_t sp = stream_policy(P);
+        const uint32_t* __restrict__ cb = P.col + (lo & ~3ull);
+        const uint32_t off0 = (uint32_t)(lo & 3ull);
+        const uint32_t ne = (uint32_t)(hi - lo) + off0; // <= 2*WIN + 3
+        const bool ok = slice_live();
+        // two quads (8 gathers) in flight per thread; an edge outside [lo, hi)
+        // or an idle lane adds +0.0, which leaves the (non-negative) sum exact
+        for (uint32_t q = 4u * slot; q < ne; q += 8u * ES) {
+            const uint32_t q2 = q + 4u * ES;
+            const uint4 a = ld_stream_u4(cb + q, sp);
+            const uint4 b = (q2 < ne) ? ld_stream_u4(cb + q2, sp) : make_uint4(0, 0, 0, 0);
+            const uint32_t us[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            double v[8][W];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t pos = (j < 4 ? q : q2) + (j & 3);
+#pragma unroll
+                for (int w = 0; w < W; ++w) v[j][w] = 0.0;
+                if (ok && pos >= off0 && pos < ne)
+                    load_w<W>(caddr<KS>(P, par, us[j]) + slice * W, v[j], contrib_policy(P, us[j]));
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+#pragma unroll
+                for (int w = 0; w < W; ++w) acc[w] += v[j][w];
+        }
+    }
+
+    __device__ __forceinline__ void reduce_slots(double (&acc)[W]) const {
+#pragma unroll
+        for (int off = LG; off < 32; off <<= 1)
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[w] += __shfl_xor_sync(0xffffffffu, acc[w], off);
+    }
+
+    // ---- chunk of a long (hub) row ------------------------------------------------
+    __device__ void chunk_task(uint32_t t) {
+        const uint64_t sp = stream_policy(P);
+        const uint32_t row = P.chunk_row[t];
+        const uint32_t first = P.chunk_first[row];
+        const uint32_t nch = P.chunk_first[row + 1] - first;
+        const uint64_t rlo = ld_stream_u64(P.row_off + row, sp), rhi = ld_stream_u64(P.row_off + row + 1, sp);
+        const uint64_t lo = rlo + (uint64_t)(t - first) * C::EMAX;
+        const uint64_t hi = min(lo + C::EMAX, rhi);
+        double acc[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc[w] = 0.0;
+        accumulate(lo, hi, acc);
+        reduce_slots(acc);
+        if (lane < LG) store_w<W>(P.chunk_acc + (size_t)t * KP + slice * W, acc);
+        __threadfence();
+        __syncwarp();
+        unsigned last = 0;
+        if (lane == 0) last = (atomicAdd(P.row_cnt + row, 1u) == nch - 1);
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (!last) return;
+        __threadfence();
+        // the row's chunk partials, in chunk order per slot, then slot tree
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc[w] = 0.0;
+        for (uint32_t c = slot; c < nch; c += ES) {
+            const double* p = P.chunk_acc + (size_t)(first + c) * KP + slice * W;
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[w] += __ldcg(p + w);
+        }
+        reduce_slots(acc);
+        if (lane < LG) epilogue(row, slice, acc);
+        if (lane == 0) P.row_cnt[row] = 0;
+    }
+
+    // ---- packed run of rows, K = 1: all gathers in flight, staged in smem ----------------
+    __device__ void packed_task(uint32_t t, double* __restrict__ sv) {
+        const uint64_t sp = stream_policy(P);
+        const uint32_t r0 = P.packed_r0[t], r1 = P.packed_r0[t + 1];
+        const int R = (int)(r1 - r0); // <= 32
+        if (R <= 0) return;
+        const uint64_t e0 = ld_stream_u64(P.row_off + r0, sp);
+        const uint64_t e1 = ld_stream_u64(P.row_off + r1, sp);
+        // row bounds relative to e0 (a run holds < 2*WIN edges: 32-bit is enough)
+        const uint32_t mylo = (lane < R) ? (uint32_t)(ld_stream_u64(P.row_off + r0 + lane, sp) - e0) : 0;
+        const uint32_t myhi = (lane < R) ? (uint32_t)(ld_stream_u64(P.row_off + r0 + lane + 1, sp) - e0) : 0;
+        // cb is the 16-byte aligned colidx base; valid positions [off0, ne).
+        const uint32_t* __restrict__ cb = P.col + (e0 & ~3ull);
+        const uint32_t off0 = (uint32_t)(e0 & 3ull);
+        const uint32_t ne = (uint32_t)(e1 - e0) + off0;
+        for (uint32_t qb = 4u * slot; qb < ne; qb += 4u * ES * C::QJ) {
+            uint32_t us[C::QJ][4];
+#pragma unroll
+            for (int j = 0; j < C::QJ; ++j) {
+                const uint32_t q = qb + 4u * ES * j;
+                const uint4 c4 = (q < ne) ? ld_stream_u4(cb + q, sp) : make_uint4(0, 0, 0, 0);
+                us[j][0] = c4.x; us[j][1] = c4.y; us[j][2] = c4.z; us[j][3] = c4.w;
+            }
+            double v[C::QJ][4][W];
+#pragma unroll
+            for (int j = 0; j < C::QJ; ++j)
+#pragma unroll
+                for (int tq = 0; tq < 4; ++tq) {
+                    const uint32_t e = qb + 4u * ES * j + tq;
+                    if (e >= off0 && e < ne)
+                        load_w<W>(caddr<KS>(P, par, us[j][tq]) + slice * W, v[j][tq],
+                                  contrib_policy(P, us[j][tq]));
+                }
+#pragma unroll
+            for (int j = 0; j < C::QJ; ++j)
+#pragma unroll
+                for (int tq = 0; tq < 4; ++tq) {
+                    const uint32_t e = qb + 4u * ES * j + tq;
+                    if (e >= off0 && e < ne) store_w<W>(sv + (e - off0) * KP + slice * W, v[j][tq]);
+                }
+        }
+        __syncwarp();
+        // per-row reduction in ascending source order, gs lanes per (row, slice)
+        const int np2 = R <= 1 ? 1 : (R <= 2 ? 2 : (R <= 4 ? 4 : (R <= 8 ? 8 : (R <= 16 ? 16 : 32))));
+        const int rows_per_round = 32 / LG;
+        const int gs = (np2 <= rows_per_round) ? rows_per_round / np2 : 1;
+        const int rounds = (np2 <= rows_per_round) ? 1 : (R + rows_per_round - 1) / rows_per_round;
+        const int sub = (lane / LG) % gs;
+        for (int rd = 0; rd < rounds; ++rd) {
+            const int i = rd * rows_per_round + (lane / LG) / gs;
+            const int src = i < R ? i : 0;
+            const uint32_t lo = __shfl_sync(0xffffffffu, mylo, src);
+            const uint32_t hi = __shfl_sync(0xffffffffu, myhi, src);
+            double acc[W];
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[w] = 0.0;
+            if (i < R) {
+                for (uint32_t j = lo + sub; j < hi; j += gs) {
+                    const double* p = sv + j * KP + slice * W;
+#pragma unroll
+                    for (int w = 0; w < W; ++w) acc[w] += p[w];
+                }
+            }
+            for (int off = LG; off < LG * gs; off <<= 1)
+#pragma unroll
+                for (int w = 0; w < W; ++w) acc[w] += __shfl_xor_sync(0xffffffffu, acc[w], off);
+            if (i < R && sub == 0) epilogue(r0 + i, slice, acc);
+        }
+        __syncwarp();
+    }
+
+    // ---- packed run, K > 1: one lane group per row, register accumulation ------------
+    // Group g takes rows g, g+ES, ... of the run; each row is summed in
+    // ascending source order with 128-bit colidx loads, two quads in flight.
+    __device__ void packed_direct(uint32_t t) {
+        const uint64_t sp = stream_policy(P);
+        const uint32_t r0 = P.packed_r0[t], r1 = P.packed_r0[t + 1];
+        const uint32_t R = r1 - r0;
+        for (uint32_t i = slot; i < R; i += ES) {
+            const uint32_t v = r0 + i;
+            double acc[W];
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[w] = 0.0;
+            // accumulate() with a single slot of this group: quads 0, 1, 2, ...
+            const uint64_t lo = ld_stream_u64(P.row_off + v, sp), hi = ld_stream_u64(P.row_off + v + 1, sp);
+            const uint32_t* __restrict__ cb = P.col + (lo & ~3ull);
+            const uint32_t off0 = (uint32_t)(lo & 3ull);
+            const uint32_t ne = (uint32_t)(hi - lo) + off0;
+            const bool ok = slice_live();
+            for (uint32_t q = 0; q < ne; q += 8) {
+                const uint4 a = ld_stream_u4(cb + q, sp);
+                const uint4 b = (q + 4 < ne) ? ld_stream_u4(cb + q + 4, sp) : make_uint4(0, 0, 0, 0);
+                const uint32_t us[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                double vals[8][W];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) vals[j][w] = 0.0;
+                    if (ok && q + j >= off0 && q + j < ne)
+                        load_w<W>(caddr<KS>(P, par, us[j]) + slice * W, vals[j], contrib_policy(P, us[j]));
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int w = 0; w < W; ++w) acc[w] += vals[j][w];
+            }
+            epilogue(v, slice, acc);
+        }
+    }
+
+    // ---- rows with no in-edges: rank = c0; write c0/d for rows with out-edges,
+    //      and (sweep mode) the L1 distance to the reference -------------------------
+    __device__ void empty_task(uint32_t t) {
+        const uint64_t sp = stream_policy(P);
+        const uint32_t base = P.empty_begin + t * C::ER;
+#pragma unroll 2
+        for (int rd = 0; rd < 8; ++rd) {
+            const uint32_t v = base + rd * ES + slot;
+            if (v >= P.n) break;
+            const uint2 ri = ld_stream_u2(P.rowinfo + v, sp);
+            double cv[W];
+            bool any = false;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const int k = slice * W + w;
+                cv[w] = 0.0;
+                if (k < (int)P.K && s_active[k]) {
+                    any = true;
+                    const double r = s_c0[k];
+                    if constexpr ((QM & 16) != 0)
+                        if (P.ref) part[4][w] += fabs(__dsub_rn(r, __ldg(P.ref + v)));
+                    if (ri.x) cv[w] = __ddiv_rn(r, (double)ri.x);
+                }
+            }
+            if (ri.x && any && lane_ok(slice)) write_contrib(ri.y, slice, cv);
+        }
+    }
+};
+
+template <int LG, int W, int WIN, int QJ_, int MINB, int QM = kQmAll, int KS_ = 0>
+__global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
+    using C = PullCfg<LG, W, WIN, QJ_, KS_>;
+    constexpr int KP = C::KP;
+    __shared__ double s_alpha[KP], s_c0[KP];
+    __shared__ int s_active[KP];
+    __shared__ int s_iter, s_flag;
+    extern __shared__ __align__(16) double s_dyn[]; // [kWarps][SMEM_WARP] gathered values
+    __shared__ double s_red[kWarps][kNQ * KP];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        s_iter = P.gs->iter;
+        s_flag = P.gs->any_active;
+    }
+    if (tid < KP) {
+        const bool real = tid < (int)P.K;
+        s_alpha[tid] = real ? P.lanes[tid].alpha : 0.0;
+        s_c0[tid] = real ? P.lanes[tid].c0 : 0.0;
+        s_active[tid] = real ? P.lanes[tid].active : 0;
+    }
+    __syncthreads();
+    if (!s_flag) return; // speculative launch after convergence (host-loop mode)
+
+    Warp<LG, W, WIN, QJ_, QM, KS_> w(P, s_iter & 1, lane, s_alpha, s_c0, s_active);
+    double* sv = s_dyn + (size_t)warp * C::SMEM_WARP;
+    const uint32_t TW = P.G * kWarps;
+    const uint32_t T1 = P.n_chunk, T2 = T1 + P.n_packed, T3 = T2 + P.n_empty_tasks;
+    for (uint32_t t = blockIdx.x * kWarps + warp; t < T3; t += TW) {
+        if (t < T1) {
+            if (!(P.skip_mask & 1)) w.chunk_task(t);
+        } else if (t < T2) {
+            if (!(P.skip_mask & 2)) {
+                if constexpr (C::STAGED) w.packed_task(t - T1, sv);
+                else w.packed_direct(t - T1);
+            }
+        } else if (!(P.skip_mask & 4)) {
+            w.empty_task(t - T2);
+        }
+    }
+
+    // ---- CTA partials, fixed order ------------------------------------------------
+#pragma unroll
+    for (int q = 0; q < kNQ; ++q)
+#pragma unroll
+        for (int wv = 0; wv < W; ++wv) {
+            double v = w.part[q][wv];
+#pragma unroll
+            for (int off = LG; off < 32; off <<= 1) {
+                const double o = __shfl_xor_sync(0xffffffffu, v, off);
+                v = (q == 2) ? fmax(v, o) : v + o;
+            }
+            if (lane < LG) s_red[warp][q * KP + w.slice * W + wv] = v;
+        }
+    __syncthreads();
+    for (int t = tid; t < kNQ * KP; t += kNT) {
+        const int q = t / KP;
+        double v = 0.0;
+#pragma unroll
+        for (int wp = 0; wp < kWarps; ++wp) v = (q == 2) ? fmax(v, s_red[wp][t]) : v + s_red[wp][t];
+        P.partials[(size_t)t * P.G + blockIdx.x] = v;
+    }
+
+    // ---- last CTA: reduce partials, convergence, next teleport --------------------------
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_flag = (atomicAdd(&P.gs->counter, 1u) == P.G - 1);
+    __syncthreads();
+    if (!s_flag) return;
+    __threadfence();
+
+    __shared__ double s_tot[kNQ * KP];
+    for (int t = warp; t < kNQ * KP; t += kWarps) {
+        const int q = t / KP;
+        double v = 0.0;
+        for (uint32_t b = lane; b < P.G; b += 32) {
+            const double x = __ldcg(P.partials + (size_t)t * P.G + b);
+            v = (q == 2) ? fmax(v, x) : v + x;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double o = __shfl_xor_sync(0xffffffffu, v, off);
+            v = (q == 2) ? fmax(v, o) : v + o;
+        }
+        if (lane == 0) s_tot[t] = v;
+    }
+    __syncthreads();
+    const int iter = s_iter; // iterations completed before this launch
+    if (tid < (int)P.K && s_active[tid]) {
+        const int k = tid;
+        LaneState& L = P.lanes[k];
+        // rows with no in-edges all moved from prev_empty to c0 (exactly); add
+        // their terms once instead of per row
+        const double c0 = s_c0[k];
+        const double de = __dsub_rn(c0, L.prev_empty);
+        const double ade = fabs(de);
+        const double n_empty = (double)(P.n - P.empty_begin), n_iso = (double)(P.n - P.iso_begin);
+        double l1s = s_tot[0 * KP + k], l2s = s_tot[1 * KP + k], linf = s_tot[2 * KP + k];
+        double dang = s_tot[3 * KP + k];
+        if (P.n > P.empty_begin) {
+            l1s = __dadd_rn(l1s, __dmul_rn(n_empty, ade));
+            l2s = __dadd_rn(l2s, __dmul_rn(n_empty, __dmul_rn(de, de)));
+            linf = fmax(linf, ade);
+            dang = __dadd_rn(dang, __dmul_rn(n_iso, c0));
+        }
+        const double l2 = sqrt(l2s);
+        double* tr = P.trace + ((size_t)iter * P.K + k) * 4;
+        tr[0] = (QM & 1) ? l1s : NAN;
+        tr[1] = (QM & 2) ? l2 : NAN;
+        tr[2] = (QM & 4) ? linf : NAN;
+        tr[3] = (QM & 16) ? s_tot[4 * KP + k] : NAN;
+        const double errs[3] = {l1s, l2, linf};
+        const int done = iter + 1;
+        L.iterations = done;
+        L.final_err = errs[L.report_norm];
+        L.c0_used = c0;
+        L.prev_empty = c0;
+        bool stop = true; // every norm in the mask strictly below tau (pagerank.hpp:99)
+        for (int q = 0; q < 3; ++q)
+            if ((L.stop_mask >> q) & 1u) stop = stop && (errs[q] < L.tol);
+        if (stop) {
+            L.converged = 1;
+            L.active = 0;
+        } else if (done >= P.gs->max_iter) {
+            L.active = 0;
+        }
+        // teleport = (1 - alpha)/n + alpha*dangling_sum/n   (pagerank.hpp:87)
+        const double a = L.alpha, nd = (double)P.n;
+        L.c0 = __dadd_rn(__ddiv_rn(__dsub_rn(1.0, a), nd), __ddiv_rn(__dmul_rn(a, dang), nd));
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int any = 0;
+        for (uint32_t k = 0; k < P.K; ++k) any |= P.lanes[k].active;
+        P.gs->iter = iter + 1;
+        P.gs->any_active = any;
+        P.gs->counter = 0;
+        __threadfence();
+        if (P.use_cond) cudaGraphSetConditional(P.cond, any ? 1u : 0u);
+    }
+}
+
+} // namespace prgpu
