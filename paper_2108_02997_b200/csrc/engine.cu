@@ -171,8 +171,11 @@ struct LaneCfg {
     int LG, W, WIN, KS; // KS: contribution row stride (doubles)
     KernelFn fn;
     int KP() const { return LG * W; }
+    int QM = kQmAll;
     size_t smem() const {
-        return KP() == 1 ? (size_t)kWarps * 2 * WIN * sizeof(double) : 0; // PullCfg::STAGED
+        const size_t staged = KP() == 1 ? (size_t)kWarps * 2 * WIN * sizeof(double) : 0; // STAGED
+        const size_t cols = W >= 6 ? (size_t)popc_c(QM) * W * kNT * sizeof(double) : 0;    // Partials
+        return staged + cols;
     }
 };
 
@@ -186,33 +189,35 @@ inline int variant() {
 // otherwise only L1 + dangling (the damping sweep's stopping rule).
 template <int LG, int W, int WIN, int MINB, int KS = LG * W>
 LaneCfg wide_cfg(bool all_q) {
-    return all_q ? LaneCfg{LG, W, WIN, KS, pull_kernel<LG, W, WIN, 0, MINB, kQmAll, KS>}
-                 : LaneCfg{LG, W, WIN, KS, pull_kernel<LG, W, WIN, 0, MINB, kQmL1, KS>};
+    return all_q ? LaneCfg{LG, W, WIN, KS, pull_kernel<LG, W, WIN, 0, MINB, kQmAll, KS>, kQmAll}
+                 : LaneCfg{LG, W, WIN, KS, pull_kernel<LG, W, WIN, 0, MINB, kQmL1, KS>, kQmL1};
 }
 
 inline LaneCfg lane_cfg(int K, bool all_q) {
+    // Defaults measured on B200 (scripts/gpu_variants*.sh);
+    // PRGPU_VARIANT selects the alternatives that lost.
     const int var = variant();
     if (K == 1) {
         switch (var) {
-        case 1: return {1, 1, 256, 1, pull_kernel<1, 1, 256, 2, 4>};
+        case 1: return {1, 1, 256, 1, pull_kernel<1, 1, 256, 4, 2>};
         case 2: return {1, 1, 256, 1, pull_kernel<1, 1, 256, 4, 3>};
         case 3: return {1, 1, 128, 1, pull_kernel<1, 1, 128, 2, 4>};
-        default: return {1, 1, 256, 1, pull_kernel<1, 1, 256, 4, 2>};
+        default: return {1, 1, 256, 1, pull_kernel<1, 1, 256, 2, 4>};
         }
     }
-    // wide lanes: one double per thread (W = 1), LG = next power of two >= K,
-    // contribution rows padded to a whole number of 32-byte sectors
-    if (K == 2) return wide_cfg<2, 1, 64, 4>(all_q);
-    if (K <= 4) return wide_cfg<4, 1, 64, 4>(all_q);
-    if (K <= 8) return wide_cfg<8, 1, 64, 4>(all_q);
+    // wide lanes: two doubles per thread (one 16-byte load per edge),
+    // LG = KS/2 threads per edge, rows padded to whole 32-byte sectors
+    if (K == 2) return wide_cfg<1, 2, 64, 4>(all_q);
+    if (K <= 4) return wide_cfg<2, 2, 64, 4>(all_q);
+    if (K <= 8) return wide_cfg<4, 2, 64, 4>(all_q);
     if (K <= 12) {
         if (var == 1) return wide_cfg<4, 3, 64, 3>(all_q);
-        if (var == 2) return wide_cfg<16, 1, 64, 6, 12>(all_q);
-        if (var == 3) return wide_cfg<16, 1, 32, 4, 12>(all_q);
-        if (var == 4) return wide_cfg<8, 2, 64, 4, 12>(all_q);
-        return wide_cfg<16, 1, 64, 4, 12>(all_q);
+        if (var == 2) return wide_cfg<16, 1, 64, 4, 12>(all_q);
+        if (var == 5) return wide_cfg<1, 12, 64, 3>(all_q);
+        if (var == 6) return wide_cfg<2, 6, 64, 3>(all_q);
+        return wide_cfg<8, 2, 64, 4, 12>(all_q);
     }
-    return wide_cfg<16, 1, 64, 4>(all_q);
+    return wide_cfg<8, 2, 64, 4>(all_q);
 }
 
 void launch_init(const LaneCfg& c, const Params& P, uint32_t ndangling, cudaStream_t st) {
@@ -516,6 +521,9 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     PRGPU_CUDA(cudaEventCreate(&s->e0));
     PRGPU_CUDA(cudaEventCreate(&s->e1));
 
+    // PRGPU_NO_GRAPH=1: host-driven speculative launches instead of the graph
+    // (ncu cannot profile kernel nodes under a conditional node)
+    if (const char* ng = std::getenv("PRGPU_NO_GRAPH")) build_graph = build_graph && std::atoi(ng) == 0;
     if (build_graph) {
         // graph: WHILE(cond) { pull_kernel } — cond defaults to 1 at every launch
         PRGPU_CUDA(cudaGraphCreate(&s->graph, 0));

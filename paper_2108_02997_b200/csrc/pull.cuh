@@ -212,6 +212,44 @@ __device__ __forceinline__ void store_w_pol(double* p, const double (&v)[W], uin
 constexpr int kQmAll = 31;
 constexpr int kQmL1 = 1 | 8;
 
+constexpr int popc_c(int x) { return x ? (x & 1) + popc_c(x >> 1) : 0; }
+
+// Per-thread partial sums.  Narrow lanes keep them in registers; a thread that
+// carries many lanes (W >= 6) keeps them in its own shared-memory column
+// (thread-strided, conflict-free) so the gather path keeps its registers.
+template <int W, int QM, bool SMEMP>
+struct Partials {
+    static constexpr int NQU = popc_c(QM);
+    static constexpr int qidx(int q) { return popc_c(QM & ((1 << q) - 1)); }
+    double reg[SMEMP ? 1 : kNQ][SMEMP ? 1 : W];
+    double* sp;
+    __device__ void init(double* smem_cols, int tid) {
+        if constexpr (SMEMP) {
+            sp = smem_cols + tid;
+#pragma unroll
+            for (int i = 0; i < NQU * W; ++i) sp[i * kNT] = 0.0;
+        } else {
+#pragma unroll
+            for (int q = 0; q < kNQ; ++q)
+#pragma unroll
+                for (int w = 0; w < W; ++w) reg[q][w] = 0.0;
+        }
+    }
+    __device__ __forceinline__ double& at(int q, int w) {
+        if constexpr (SMEMP) return sp[(qidx(q) * W + w) * kNT];
+        else return reg[q][w];
+    }
+    __device__ __forceinline__ void add(int q, int w, double x) {
+        if ((QM >> q) & 1) at(q, w) += x;
+    }
+    __device__ __forceinline__ void max(int q, int w, double x) {
+        if ((QM >> q) & 1) at(q, w) = fmax(at(q, w), x);
+    }
+    __device__ __forceinline__ double get(int q, int w) {
+        return ((QM >> q) & 1) ? at(q, w) : 0.0;
+    }
+};
+
 template <int LG, int W, int WIN, int QJ_ = 0, int KS_ = 0>
 struct PullCfg {
     static constexpr int KP = LG * W;
@@ -239,16 +277,14 @@ struct Warp {
     const double* s_alpha;
     const double* s_c0;
     const int* s_active;
-    double part[kNQ][W];
+    static constexpr bool SMEMP = (W >= 6);
+    Partials<W, QM, SMEMP> part;
 
     __device__ Warp(const Params& p, int parity, int ln, const double* a, const double* c0,
-                    const int* act)
+                    const int* act, double* smem_cols, int tid)
         : P(p), lane(ln), slot(ln / LG), slice(ln % LG), par(parity), rp(p.rank[parity]),
           rn(p.rank[parity ^ 1]), s_alpha(a), s_c0(c0), s_active(act) {
-#pragma unroll
-        for (int q = 0; q < kNQ; ++q)
-#pragma unroll
-            for (int w = 0; w < W; ++w) part[q][w] = 0.0;
+        part.init(smem_cols, tid);
     }
 
     __device__ __forceinline__ bool lane_ok(int sl) const { return KS == KP || sl * W < KS; }
@@ -289,12 +325,12 @@ struct Warp {
                 const double o = __ldcs(rp + (size_t)k * n + v);
                 const double df = __dsub_rn(r, o);
                 const double ad = fabs(df);
-                if constexpr ((QM & 1) != 0) part[0][w] += ad;
-                if constexpr ((QM & 2) != 0) part[1][w] += df * df;
-                if constexpr ((QM & 4) != 0) part[2][w] = fmax(part[2][w], ad);
-                if (d == 0) part[3][w] += r;
+                part.add(0, w, ad);
+                part.add(1, w, df * df);
+                part.max(2, w, ad);
+                if (d == 0) part.add(3, w, r);
                 if constexpr ((QM & 16) != 0)
-                    if (P.ref) part[4][w] += fabs(__dsub_rn(r, __ldg(P.ref + v)));
+                    if (P.ref) part.add(4, w, fabs(__dsub_rn(r, __ldg(P.ref + v))));
                 __stcs(rn + (size_t)k * n + v, r);
                 if (d) cv[w] = __ddiv_rn(r, (double)d); // prev[u]/out_degree[u] (:91)
             }
@@ -310,26 +346,33 @@ struct Warp {
         const uint32_t off0 = (uint32_t)(lo & 3ull);
         const uint32_t ne = (uint32_t)(hi - lo) + off0; // <= 2*WIN + 3
         const bool ok = slice_live();
-        // two quads (8 gathers) in flight per thread; an edge outside [lo, hi)
-        // or an idle lane adds +0.0, which leaves the (non-negative) sum exact
+        // two quads (8 edges) per step; an edge outside [lo, hi) or an idle lane
+        // adds +0.0, which leaves the (non-negative) sum exact.  Narrow lanes
+        // issue all 8 gathers before the adds; wide lanes (W >= 6) consume
+        // each edge's row as it arrives (register budget).
+        constexpr int EF = (W >= 6) ? 1 : 8; // gathers held in flight per thread
         for (uint32_t q = 4u * slot; q < ne; q += 8u * ES) {
             const uint32_t q2 = q + 4u * ES;
             const uint4 a = ld_stream_u4(cb + q, sp);
             const uint4 b = (q2 < ne) ? ld_stream_u4(cb + q2, sp) : make_uint4(0, 0, 0, 0);
             const uint32_t us[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-            double v[8][W];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const uint32_t pos = (j < 4 ? q : q2) + (j & 3);
+            for (int j0 = 0; j0 < 8; j0 += EF) {
+                double v[EF][W];
 #pragma unroll
-                for (int w = 0; w < W; ++w) v[j][w] = 0.0;
-                if (ok && pos >= off0 && pos < ne)
-                    load_w<W>(caddr<KS>(P, par, us[j]) + slice * W, v[j], contrib_policy(P, us[j]));
+                for (int j = 0; j < EF; ++j) {
+                    const uint32_t pos = ((j0 + j) < 4 ? q : q2) + ((j0 + j) & 3);
+#pragma unroll
+                    for (int w = 0; w < W; ++w) v[j][w] = 0.0;
+                    if (ok && pos >= off0 && pos < ne)
+                        load_w<W>(caddr<KS>(P, par, us[j0 + j]) + slice * W, v[j],
+                                  contrib_policy(P, us[j0 + j]));
+                }
+#pragma unroll
+                for (int j = 0; j < EF; ++j)
+#pragma unroll
+                    for (int w = 0; w < W; ++w) acc[w] += v[j][w];
             }
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-#pragma unroll
-                for (int w = 0; w < W; ++w) acc[w] += v[j][w];
         }
     }
 
@@ -468,18 +511,23 @@ struct Warp {
                 const uint4 a = ld_stream_u4(cb + q, sp);
                 const uint4 b = (q + 4 < ne) ? ld_stream_u4(cb + q + 4, sp) : make_uint4(0, 0, 0, 0);
                 const uint32_t us[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-                double vals[8][W];
+                constexpr int EF = (W >= 6) ? 1 : 8; // see accumulate()
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
+                for (int j0 = 0; j0 < 8; j0 += EF) {
+                    double vals[EF][W];
 #pragma unroll
-                    for (int w = 0; w < W; ++w) vals[j][w] = 0.0;
-                    if (ok && q + j >= off0 && q + j < ne)
-                        load_w<W>(caddr<KS>(P, par, us[j]) + slice * W, vals[j], contrib_policy(P, us[j]));
+                    for (int j = 0; j < EF; ++j) {
+#pragma unroll
+                        for (int w = 0; w < W; ++w) vals[j][w] = 0.0;
+                        if (ok && q + j0 + j >= off0 && q + j0 + j < ne)
+                            load_w<W>(caddr<KS>(P, par, us[j0 + j]) + slice * W, vals[j],
+                                      contrib_policy(P, us[j0 + j]));
+                    }
+#pragma unroll
+                    for (int j = 0; j < EF; ++j)
+#pragma unroll
+                        for (int w = 0; w < W; ++w) acc[w] += vals[j][w];
                 }
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-#pragma unroll
-                    for (int w = 0; w < W; ++w) acc[w] += vals[j][w];
             }
             epilogue(v, slice, acc);
         }
@@ -505,7 +553,7 @@ struct Warp {
                     any = true;
                     const double r = s_c0[k];
                     if constexpr ((QM & 16) != 0)
-                        if (P.ref) part[4][w] += fabs(__dsub_rn(r, __ldg(P.ref + v)));
+                        if (P.ref) part.add(4, w, fabs(__dsub_rn(r, __ldg(P.ref + v))));
                     if (ri.x) cv[w] = __ddiv_rn(r, (double)ri.x);
                 }
             }
@@ -538,7 +586,10 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     __syncthreads();
     if (!s_flag) return; // speculative launch after convergence (host-loop mode)
 
-    Warp<LG, W, WIN, QJ_, QM, KS_> w(P, s_iter & 1, lane, s_alpha, s_c0, s_active);
+    // dynamic smem: [kWarps][SMEM_WARP] staged gathers, then the per-thread
+    // partial columns when W >= 6
+    Warp<LG, W, WIN, QJ_, QM, KS_> w(P, s_iter & 1, lane, s_alpha, s_c0, s_active,
+                                     s_dyn + (size_t)kWarps * C::SMEM_WARP, tid);
     double* sv = s_dyn + (size_t)warp * C::SMEM_WARP;
     const uint32_t TW = P.G * kWarps;
     const uint32_t T1 = P.n_chunk, T2 = T1 + P.n_packed, T3 = T2 + P.n_empty_tasks;
@@ -560,7 +611,7 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     for (int q = 0; q < kNQ; ++q)
 #pragma unroll
         for (int wv = 0; wv < W; ++wv) {
-            double v = w.part[q][wv];
+            double v = w.part.get(q, wv);
 #pragma unroll
             for (int off = LG; off < 32; off <<= 1) {
                 const double o = __shfl_xor_sync(0xffffffffu, v, off);
