@@ -51,6 +51,12 @@ CONFIGS = {
                kind="rmat", scale=22, alphas=ALPHAS, tol=1e-6, norm=0),
     "c2k1": dict(workload="C2 graph, single lane alpha .85 tau 1e-6 L1", kind="rmat", scale=22,
                  alphas=[0.85], tol=1e-6, norm=0),
+    "c2s20": dict(workload="RMAT-20 damping sweep (probe)", kind="rmat", scale=20, alphas=ALPHAS,
+                  tol=1e-6, norm=0),
+    "c2s18": dict(workload="RMAT-18 damping sweep (probe)", kind="rmat", scale=18, alphas=ALPHAS,
+                  tol=1e-6, norm=0),
+    "c2s24": dict(workload="RMAT-24 damping sweep (probe)", kind="rmat", scale=24, alphas=ALPHAS,
+                  tol=1e-6, norm=0),
     "c1": dict(workload="C1: RMAT-16 alpha .85 tau 1e-6 L1", kind="rmat", scale=16,
                alphas=[0.85], tol=1e-6, norm=0),
     "c3": dict(workload="C3: grid 4096^2 p .6 +1% long-range, alpha .85, all norms to tau 1e-10",

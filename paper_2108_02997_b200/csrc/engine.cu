@@ -464,44 +464,16 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     P.use_cond = 0;
     P.skip_mask = 0;
     if (const char* sk = std::getenv("PRGPU_SKIP")) P.skip_mask = (uint32_t)std::atoi(sk);
-    // L2 residency of the hot contribution region (see pull.cuh): 0 = evict
-    // hints, 1 = hardware persisting window, 2 = none.  PRGPU_L2MODE / _HOT_FRAC
-    // override (tuning).  Sizes come from the device, not hard-coded.
+    // streams (colidx, offsets, row info) are loaded evict_first (l2mode 0);
+    // PRGPU_L2MODE=2 turns the hints off (tuning).  Contributions: two
+    // ping-pong buffers [parity][src][KS].
     P.l2mode = 0;
     if (const char* m = std::getenv("PRGPU_L2MODE")) P.l2mode = (uint32_t)std::atoi(m);
-    size_t window_bytes = 0;
-    {
-        int l2 = 0, max_persist = 0, max_window = 0;
-        PRGPU_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device));
-        PRGPU_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, g->device));
-        PRGPU_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, g->device));
-        double frac = 0.5;
-        if (const char* f = std::getenv("PRGPU_HOT_FRAC")) frac = std::atof(f);
-        const double per_src = 2.0 * KS * sizeof(double);
-        double budget = frac * l2;
-        if (P.l2mode == 1) budget = std::min<double>(std::min(max_persist, max_window), budget * 2.0);
-        P.hot_src = (uint32_t)std::min<double>((double)g->nsrc, std::max(0.0, budget / per_src));
-        window_bytes = (size_t)P.hot_src * 2 * KS * sizeof(double);
-        if (P.l2mode == 1 && window_bytes)
-            PRGPU_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize,
-                                          std::min<size_t>(window_bytes, (size_t)max_persist)));
-    }
-    // contributions: [hot src][parity][KS], then cold parity 0, cold parity 1
+    P.hot_src = 0;
     P.cbase = s->contrib.p;
-    P.cold_off[0] = 2ull * P.hot_src;
-    P.cold_off[1] = 2ull * P.hot_src + (nsrc - std::min<size_t>(P.hot_src, nsrc));
+    P.cold_off[0] = 0;
+    P.cold_off[1] = nsrc;
     build_tasks(s.get());
-    cudaAccessPolicyWindow win{};
-    if (P.l2mode == 1 && window_bytes) {
-        win.base_ptr = P.cbase;
-        win.num_bytes = window_bytes;
-        win.hitRatio = 1.0f;
-        win.hitProp = cudaAccessPropertyPersisting;
-        win.missProp = cudaAccessPropertyStreaming;
-        cudaStreamAttrValue sa{};
-        sa.accessPolicyWindow = win;
-        PRGPU_CUDA(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &sa));
-    }
 
     // persistent grid: resident CTAs, but at least ~4 tasks per warp
     const size_t smem = s->cfg.smem();
@@ -549,11 +521,6 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         kp.kernelParams = args;
         cudaGraphNode_t knode;
         PRGPU_CUDA(cudaGraphAddKernelNode(&knode, body, nullptr, 0, &kp));
-        if (P.l2mode == 1 && window_bytes) {
-            cudaKernelNodeAttrValue kv{};
-            kv.accessPolicyWindow = win;
-            PRGPU_CUDA(cudaGraphKernelNodeSetAttribute(knode, cudaKernelNodeAttributeAccessPolicyWindow, &kv));
-        }
         PRGPU_CUDA(cudaGraphInstantiate(&s->exec, s->graph, 0));
         s->use_graph = true;
     }

@@ -84,8 +84,8 @@ struct Params {
     const uint32_t* __restrict__ col;  // source ids
     const uint2* __restrict__ rowinfo; // {out-degree, source id}
     double* rank[2];                   // [K][n] (rows < empty_begin only)
-    double* cbase;                     // contributions, see caddr()
-    uint64_t cold_off[2];              // first cold row of each parity (in rows of KS)
+    double* cbase;                     // contributions [parity][src][KS], see caddr()
+    uint64_t cold_off[2];              // first row of each parity buffer (in rows of KS)
     const double* ref;                 // [n] engine ids, or null
     double* partials;                  // [kNQ*KP][G]
     double* trace;                     // [max_iter][K][4]
@@ -137,8 +137,7 @@ __device__ __forceinline__ uint64_t contrib_policy(const Params& P, uint32_t src
 
 template <int KS>
 __device__ __forceinline__ double* caddr(const Params& P, int par, uint32_t src) {
-    return src < P.hot_src ? P.cbase + ((size_t)2 * src + par) * KS
-                           : P.cbase + (P.cold_off[par] + (src - P.hot_src)) * KS;
+    return P.cbase + (P.cold_off[par] + src) * KS;
 }
 
 __device__ __forceinline__ uint4 ld_stream_u4(const uint32_t* p, uint64_t pol) {
@@ -163,18 +162,20 @@ __device__ __forceinline__ uint2 ld_stream_u2(const uint2* p, uint64_t pol) {
     return r;
 }
 
+// gathers: plain read-only loads (measured: L2 residency hints on the
+// contributions did not pay, and the policy/address arithmetic per edge did)
 template <int W>
-__device__ __forceinline__ void load_w(const double* __restrict__ p, double (&v)[W], uint64_t pol) {
+__device__ __forceinline__ void load_w(const double* __restrict__ p, double (&v)[W]) {
     if constexpr (W % 2 == 0) {
 #pragma unroll
-        for (int w = 0; w < W; w += 2)
-            asm("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-                : "=d"(v[w]), "=d"(v[w + 1])
-                : "l"(p + w), "l"(pol));
+        for (int w = 0; w < W; w += 2) {
+            const double2 x = __ldg(reinterpret_cast<const double2*>(p + w));
+            v[w] = x.x;
+            v[w + 1] = x.y;
+        }
     } else {
 #pragma unroll
-        for (int w = 0; w < W; ++w)
-            asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v[w]) : "l"(p + w), "l"(pol));
+        for (int w = 0; w < W; ++w) v[w] = __ldg(p + w);
     }
 }
 
@@ -304,7 +305,7 @@ struct Warp {
     }
 
     __device__ __forceinline__ void write_contrib(uint32_t src, int sl, const double (&cv)[W]) {
-        store_w_pol<W>(caddr<KS>(P, par ^ 1, src) + sl * W, cv, contrib_policy(P, src));
+        store_w<W>(caddr<KS>(P, par ^ 1, src) + sl * W, cv);
     }
 
     // fused epilogue for row v, lanes [sl*W, sl*W + W)
@@ -365,8 +366,7 @@ struct Warp {
 #pragma unroll
                     for (int w = 0; w < W; ++w) v[j][w] = 0.0;
                     if (ok && pos >= off0 && pos < ne)
-                        load_w<W>(caddr<KS>(P, par, us[j0 + j]) + slice * W, v[j],
-                                  contrib_policy(P, us[j0 + j]));
+                        load_w<W>(caddr<KS>(P, par, us[j0 + j]) + slice * W, v[j]);
                 }
 #pragma unroll
                 for (int j = 0; j < EF; ++j)
@@ -448,8 +448,7 @@ struct Warp {
                 for (int tq = 0; tq < 4; ++tq) {
                     const uint32_t e = qb + 4u * ES * j + tq;
                     if (e >= off0 && e < ne)
-                        load_w<W>(caddr<KS>(P, par, us[j][tq]) + slice * W, v[j][tq],
-                                  contrib_policy(P, us[j][tq]));
+                        load_w<W>(caddr<KS>(P, par, us[j][tq]) + slice * W, v[j][tq]);
                 }
 #pragma unroll
             for (int j = 0; j < C::QJ; ++j)
@@ -520,8 +519,7 @@ struct Warp {
 #pragma unroll
                         for (int w = 0; w < W; ++w) vals[j][w] = 0.0;
                         if (ok && q + j0 + j >= off0 && q + j0 + j < ne)
-                            load_w<W>(caddr<KS>(P, par, us[j0 + j]) + slice * W, vals[j],
-                                      contrib_policy(P, us[j0 + j]));
+                            load_w<W>(caddr<KS>(P, par, us[j0 + j]) + slice * W, vals[j]);
                     }
 #pragma unroll
                     for (int j = 0; j < EF; ++j)
