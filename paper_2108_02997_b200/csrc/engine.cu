@@ -201,23 +201,21 @@ inline LaneCfg lane_cfg(int K, bool all_q) {
         switch (var) {
         case 1: return {1, 1, 256, 1, pull_kernel<1, 1, 256, 4, 2>};
         case 2: return {1, 1, 256, 1, pull_kernel<1, 1, 256, 4, 3>};
-        case 3: return {1, 1, 128, 1, pull_kernel<1, 1, 128, 2, 4>};
-        default: return {1, 1, 256, 1, pull_kernel<1, 1, 256, 2, 4>};
+        case 3: return {1, 1, 256, 1, pull_kernel<1, 1, 256, 2, 4>};
+        default: return {1, 1, 256, 1, pull_kernel<1, 1, 256, 2, 3>};
         }
     }
     // wide lanes: two doubles per thread (one 16-byte load per edge),
     // LG = KS/2 threads per edge, rows padded to whole 32-byte sectors
     if (K == 2) return wide_cfg<1, 2, 64, 4>(all_q);
-    if (K <= 4) return wide_cfg<2, 2, 64, 4>(all_q);
-    if (K <= 8) return wide_cfg<4, 2, 64, 4>(all_q);
+    if (K <= 4) return wide_cfg<2, 2, 128, 4>(all_q);
+    if (K <= 8) return wide_cfg<4, 2, 128, 4>(all_q);
     if (K <= 12) {
-        if (var == 1) return wide_cfg<4, 3, 64, 3>(all_q);
-        if (var == 2) return wide_cfg<16, 1, 64, 4, 12>(all_q);
-        if (var == 5) return wide_cfg<1, 12, 64, 3>(all_q);
-        if (var == 6) return wide_cfg<2, 6, 64, 3>(all_q);
-        return wide_cfg<8, 2, 64, 4, 12>(all_q);
+        if (var == 1) return wide_cfg<8, 2, 64, 4, 12>(all_q);
+        if (var == 2) return wide_cfg<8, 2, 256, 4, 12>(all_q);
+        return wide_cfg<8, 2, 128, 4, 12>(all_q);
     }
-    return wide_cfg<8, 2, 64, 4>(all_q);
+    return wide_cfg<8, 2, 128, 4>(all_q);
 }
 
 void launch_init(const LaneCfg& c, const Params& P, uint32_t ndangling, cudaStream_t st) {
@@ -314,7 +312,13 @@ uint32_t count_isolated(const prgpu_graph* g, cudaStream_t st) {
 void build_tasks(prgpu_session* s) {
     const prgpu_graph* g = s->g;
     cudaStream_t st = s->stream;
-    const uint32_t win = (uint32_t)s->cfg.WIN, emax = 2 * win;
+    // hub rows (in-degree > WIN) are cut into chunk tasks of `emax` edges:
+    // large enough to amortise a task's fixed cost (row lookup, the fence and
+    // counter that hand the row to its last chunk), small enough to balance
+    const uint32_t win = (uint32_t)s->cfg.WIN;
+    uint32_t emax = std::max<uint32_t>(2 * win, s->KP == 1 ? 4096 : 2048); // measured
+    if (const char* c = std::getenv("PRGPU_CHUNK")) emax = std::max(2 * win, (uint32_t)std::atoi(c));
+    s->P.chunk = emax;
     const uint32_t n = g->n;
     // long rows: a prefix, since rows are sorted by in-degree descending
     DevBuf<unsigned int> cnt(1);

@@ -98,6 +98,7 @@ struct Params {
     double* chunk_acc;           // [n_chunk][KP]
     unsigned int* row_cnt;       // [n_long]
     uint32_t n_chunk, n_packed, n_empty_tasks;
+    uint32_t chunk;              // edges per chunk task
     uint32_t empty_begin;        // first row with in-degree 0
     uint32_t iso_begin;          // first row with in- and out-degree 0
     uint32_t G;
@@ -263,8 +264,8 @@ struct PullCfg {
     static constexpr int ER = 8 * ES;    // rows per empty task
     // K = 1 stages every gathered value of a run in shared memory; wider lanes
     // accumulate in registers (staging would double the bytes moved per edge)
-    static constexpr bool STAGED = (KP == 1);
-    static constexpr int SMEM_WARP = STAGED ? EMAX * KP : 0; // doubles per warp
+    static constexpr bool STAGED = (KP == 1); // measured: staging wide lanes lost
+    static constexpr int SMEM_WARP = STAGED ? EMAX * KS : 0; // doubles per warp
 };
 
 template <int LG, int W, int WIN, int QJ_ = 0, int QM = kQmAll, int KS_ = 0>
@@ -274,6 +275,7 @@ struct Warp {
     const Params& P;
     const int lane, slot, slice, par;
     const double* __restrict__ rp;
+    const double* __restrict__ cpl; // contributions read by this thread: buffer par, + slice*W
     double* __restrict__ rn;
     const double* s_alpha;
     const double* s_c0;
@@ -284,7 +286,8 @@ struct Warp {
     __device__ Warp(const Params& p, int parity, int ln, const double* a, const double* c0,
                     const int* act, double* smem_cols, int tid)
         : P(p), lane(ln), slot(ln / LG), slice(ln % LG), par(parity), rp(p.rank[parity]),
-          rn(p.rank[parity ^ 1]), s_alpha(a), s_c0(c0), s_active(act) {
+          rn(p.rank[parity ^ 1]), cpl(p.cbase + p.cold_off[parity] * KS + (ln % LG) * W), s_alpha(a),
+          s_c0(c0), s_active(act) {
         part.init(smem_cols, tid);
     }
 
@@ -352,10 +355,17 @@ struct Warp {
         // issue all 8 gathers before the adds; wide lanes (W >= 6) consume
         // each edge's row as it arrives (register budget).
         constexpr int EF = (W >= 6) ? 1 : 8; // gathers held in flight per thread
-        for (uint32_t q = 4u * slot; q < ne; q += 8u * ES) {
+        // software pipeline: the next step's colidx quads are loaded before
+        // this step's gathers are consumed, so each step costs one round trip
+        uint32_t q = 4u * slot;
+        uint4 na = (q < ne) ? ld_stream_u4(cb + q, sp) : make_uint4(0, 0, 0, 0);
+        uint4 nb = (q + 4u * ES < ne) ? ld_stream_u4(cb + q + 4u * ES, sp) : make_uint4(0, 0, 0, 0);
+        for (; q < ne; q += 8u * ES) {
             const uint32_t q2 = q + 4u * ES;
-            const uint4 a = ld_stream_u4(cb + q, sp);
-            const uint4 b = (q2 < ne) ? ld_stream_u4(cb + q2, sp) : make_uint4(0, 0, 0, 0);
+            const uint4 a = na, b = nb;
+            const uint32_t qn = q + 8u * ES;
+            if (qn < ne) na = ld_stream_u4(cb + qn, sp);
+            if (qn + 4u * ES < ne) nb = ld_stream_u4(cb + qn + 4u * ES, sp);
             const uint32_t us[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
             for (int j0 = 0; j0 < 8; j0 += EF) {
@@ -366,7 +376,7 @@ struct Warp {
 #pragma unroll
                     for (int w = 0; w < W; ++w) v[j][w] = 0.0;
                     if (ok && pos >= off0 && pos < ne)
-                        load_w<W>(caddr<KS>(P, par, us[j0 + j]) + slice * W, v[j]);
+                        load_w<W>(cpl + (size_t)us[j0 + j] * KS, v[j]);
                 }
 #pragma unroll
                 for (int j = 0; j < EF; ++j)
@@ -390,13 +400,17 @@ struct Warp {
         const uint32_t first = P.chunk_first[row];
         const uint32_t nch = P.chunk_first[row + 1] - first;
         const uint64_t rlo = ld_stream_u64(P.row_off + row, sp), rhi = ld_stream_u64(P.row_off + row + 1, sp);
-        const uint64_t lo = rlo + (uint64_t)(t - first) * C::EMAX;
-        const uint64_t hi = min(lo + C::EMAX, rhi);
+        const uint64_t lo = rlo + (uint64_t)(t - first) * P.chunk;
+        const uint64_t hi = min(lo + P.chunk, rhi);
         double acc[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) acc[w] = 0.0;
         accumulate(lo, hi, acc);
         reduce_slots(acc);
+        if (nch == 1) { // the whole row was this chunk: no hand-off needed
+            if (lane < LG) epilogue(row, slice, acc);
+            return;
+        }
         if (lane < LG) store_w<W>(P.chunk_acc + (size_t)t * KP + slice * W, acc);
         __threadfence();
         __syncwarp();
@@ -433,6 +447,7 @@ struct Warp {
         const uint32_t* __restrict__ cb = P.col + (e0 & ~3ull);
         const uint32_t off0 = (uint32_t)(e0 & 3ull);
         const uint32_t ne = (uint32_t)(e1 - e0) + off0;
+        const bool live = slice_live();
         for (uint32_t qb = 4u * slot; qb < ne; qb += 4u * ES * C::QJ) {
             uint32_t us[C::QJ][4];
 #pragma unroll
@@ -447,15 +462,15 @@ struct Warp {
 #pragma unroll
                 for (int tq = 0; tq < 4; ++tq) {
                     const uint32_t e = qb + 4u * ES * j + tq;
-                    if (e >= off0 && e < ne)
-                        load_w<W>(caddr<KS>(P, par, us[j][tq]) + slice * W, v[j][tq]);
+                    if (live && e >= off0 && e < ne)
+                        load_w<W>(cpl + (size_t)us[j][tq] * KS, v[j][tq]);
                 }
 #pragma unroll
             for (int j = 0; j < C::QJ; ++j)
 #pragma unroll
                 for (int tq = 0; tq < 4; ++tq) {
                     const uint32_t e = qb + 4u * ES * j + tq;
-                    if (e >= off0 && e < ne) store_w<W>(sv + (e - off0) * KP + slice * W, v[j][tq]);
+                    if (live && e >= off0 && e < ne) store_w<W>(sv + (e - off0) * KS + slice * W, v[j][tq]);
                 }
         }
         __syncwarp();
@@ -475,7 +490,7 @@ struct Warp {
             for (int w = 0; w < W; ++w) acc[w] = 0.0;
             if (i < R) {
                 for (uint32_t j = lo + sub; j < hi; j += gs) {
-                    const double* p = sv + j * KP + slice * W;
+                    const double* p = sv + j * KS + slice * W;
 #pragma unroll
                     for (int w = 0; w < W; ++w) acc[w] += p[w];
                 }
@@ -519,7 +534,7 @@ struct Warp {
 #pragma unroll
                         for (int w = 0; w < W; ++w) vals[j][w] = 0.0;
                         if (ok && q + j0 + j >= off0 && q + j0 + j < ne)
-                            load_w<W>(caddr<KS>(P, par, us[j0 + j]) + slice * W, vals[j]);
+                            load_w<W>(cpl + (size_t)us[j0 + j] * KS, vals[j]);
                     }
 #pragma unroll
                     for (int j = 0; j < EF; ++j)
