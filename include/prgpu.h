@@ -139,6 +139,54 @@ PRGPU_API int prgpu_session_results(prgpu_session* s, prgpu_result* out);
 PRGPU_API int prgpu_session_time_pull(prgpu_session* s, int launches, double* ms_per_launch);
 PRGPU_API void prgpu_session_free(prgpu_session* s);
 
+/* ---- multi-GPU: 1D partition -----------------------------
+ * One process per GPU.  Each rank owns a contiguous, cost-balanced range of
+ * engine rows (hub rows are never split across ranks) and therefore a
+ * contiguous range of source ids.  Per iteration:
+ *   prgpu_part_step      local pull over the rank's rows; its new
+ *                        contributions land in contrib[parity_out] rows
+ *                        [src_begin, src_end) and its partial sums in
+ *                        rank_partials[rank]
+ *   (caller)             all-gather: every rank's contribution rows and
+ *                        partial vector into every rank's buffers (NCCL)
+ *   prgpu_part_finalize  reduce the partial vectors in rank order (identical
+ *                        on every rank), decide convergence, next teleport
+ * Buffers may be supplied by the caller (e.g. torch tensors used by NCCL). */
+typedef struct {
+    uint32_t row_begin, row_end;   /* engine rows owned */
+    uint64_t src_begin, src_end;   /* source ids owned (contiguous) */
+    uint32_t task_begin, task_end; /* warp tasks run by the rank */
+} prgpu_partition;
+
+typedef struct {
+    double* contrib[2];         /* device: contribution buffers, parity 0/1 */
+    uint32_t stride;            /* doubles per source row (K padded to 32 B) */
+    uint64_t nsrc;              /* source rows per buffer */
+    double* rank_partials;      /* device: [nranks][partials_per_rank] */
+    uint32_t partials_per_rank;
+} prgpu_exchange;
+
+/* Sizes of the buffers a partition session needs (doubles). */
+PRGPU_API int prgpu_part_buffer_sizes(prgpu_graph* g, const prgpu_params* p, int nranks,
+                                      uint64_t* contrib_doubles, uint64_t* partial_doubles);
+/* ext_contrib (optional, device, contrib_doubles) and ext_rank_partials
+ * (optional, device, partial_doubles) let the caller own the exchanged memory. */
+PRGPU_API int prgpu_part_create(prgpu_graph* g, const prgpu_params* p, int rank, int nranks,
+                                double* ext_contrib, double* ext_rank_partials, prgpu_session** out);
+PRGPU_API int prgpu_part_plan(prgpu_session* s, prgpu_partition* parts /* [nranks] */);
+PRGPU_API int prgpu_part_exchange(prgpu_session* s, prgpu_exchange* ex);
+/* Work is enqueued on `stream` (a cudaStream_t; NULL = the session's own). */
+PRGPU_API int prgpu_part_set_stream(prgpu_session* s, void* stream);
+PRGPU_API int prgpu_part_init(prgpu_session* s);
+PRGPU_API int prgpu_part_step(prgpu_session* s, int* parity_out);
+PRGPU_API int prgpu_part_finalize(prgpu_session* s);
+/* Synchronises the stream; any lane still iterating? */
+PRGPU_API int prgpu_part_active(prgpu_session* s, int* any_active);
+/* Final ranks of caller lane `lane` for this rank's engine rows [row_begin, row_end). */
+PRGPU_API int prgpu_part_local_ranks(prgpu_session* s, int lane, double* out);
+/* Engine row -> caller vertex id, [n]. */
+PRGPU_API int prgpu_graph_permutation(const prgpu_graph* g, uint32_t* old_of_new);
+
 /* ---- norms (replaces error_norm, norms.hpp:48-78) ----------------------- */
 PRGPU_API int prgpu_error_norm(int norm, const double* r, const double* s, uint64_t n, int device,
                      double* out);

@@ -22,8 +22,21 @@ EXPORTS = [
     "prgpu_graph_download", "prgpu_graph_free", "prgpu_pagerank", "prgpu_pagerank_observed",
     "prgpu_session_create", "prgpu_session_run", "prgpu_session_results",
     "prgpu_session_time_pull", "prgpu_session_free", "prgpu_error_norm", "prgpu_last_error",
-    "prgpu_version", "prgpu_kernel_launch_count",
+    "prgpu_version", "prgpu_kernel_launch_count", "prgpu_part_buffer_sizes", "prgpu_part_create",
+    "prgpu_part_plan", "prgpu_part_exchange", "prgpu_part_set_stream", "prgpu_part_init",
+    "prgpu_part_step", "prgpu_part_finalize", "prgpu_part_active", "prgpu_part_local_ranks",
+    "prgpu_graph_permutation",
 ]
+
+
+class Partition(C.Structure):
+    _fields_ = [("row_begin", C.c_uint32), ("row_end", C.c_uint32), ("src_begin", C.c_uint64),
+                ("src_end", C.c_uint64), ("task_begin", C.c_uint32), ("task_end", C.c_uint32)]
+
+
+class Exchange(C.Structure):
+    _fields_ = [("contrib", C.c_void_p * 2), ("stride", C.c_uint32), ("nsrc", C.c_uint64),
+                ("rank_partials", C.c_void_p), ("partials_per_rank", C.c_uint32)]
 
 
 class GraphInfo(C.Structure):
@@ -87,6 +100,17 @@ def lib():
             "prgpu_last_error": ([], C.c_char_p),
             "prgpu_version": ([], C.c_char_p),
             "prgpu_kernel_launch_count": ([], u64),
+            "prgpu_part_buffer_sizes": ([vp, C.POINTER(Params), i32, C.POINTER(u64), C.POINTER(u64)], i32),
+            "prgpu_part_create": ([vp, C.POINTER(Params), i32, i32, vp, vp, pp], i32),
+            "prgpu_part_plan": ([vp, C.POINTER(Partition)], i32),
+            "prgpu_part_exchange": ([vp, C.POINTER(Exchange)], i32),
+            "prgpu_part_set_stream": ([vp, vp], i32),
+            "prgpu_part_init": ([vp], i32),
+            "prgpu_part_step": ([vp, C.POINTER(i32)], i32),
+            "prgpu_part_finalize": ([vp], i32),
+            "prgpu_part_active": ([vp, C.POINTER(i32)], i32),
+            "prgpu_part_local_ranks": ([vp, i32, vp], i32),
+            "prgpu_graph_permutation": ([vp, vp], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

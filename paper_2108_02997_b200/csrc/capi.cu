@@ -19,7 +19,17 @@ std::unique_ptr<prgpu_graph> graph_generate_rmat(uint32_t, uint32_t, double, dou
 std::unique_ptr<prgpu_graph> graph_generate_grid(uint32_t, double, double, uint64_t, int,
                                                  cudaStream_t);
 void graph_download(const prgpu_graph*, uint64_t*, uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
-prgpu_session* session_create(prgpu_graph*, const prgpu_params*, bool);
+prgpu_session* session_create(prgpu_graph*, const prgpu_params*, bool, int, int, double*, double*);
+void part_sizes(prgpu_graph*, const prgpu_params*, int, uint64_t*, uint64_t*);
+void part_exchange(prgpu_session*, prgpu_exchange*);
+int part_step(prgpu_session*);
+void part_finalize(prgpu_session*);
+void part_local_ranks(prgpu_session*, int, double*);
+void session_init(prgpu_session*);
+int read_any_active(prgpu_session*);
+void part_plan_copy(prgpu_session*, prgpu_partition*);
+void part_set_stream(prgpu_session*, void*);
+void graph_permutation(const prgpu_graph*, uint32_t*);
 void session_destroy(prgpu_session*);
 using SessionPtr = std::unique_ptr<prgpu_session, void (*)(prgpu_session*)>;
 double session_run(prgpu_session*);
@@ -153,7 +163,7 @@ int prgpu_pagerank(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
     return guarded([&] {
         if (!out) prgpu::fail(PRGPU_EINVAL, "null result");
         if (g) check_device(g->device);
-        prgpu::SessionPtr s(prgpu::session_create(g, p, true), prgpu::session_destroy);
+        prgpu::SessionPtr s(prgpu::session_create(g, p, true, 0, 0, nullptr, nullptr), prgpu::session_destroy);
         prgpu::session_run(s.get());
         prgpu::session_results(s.get(), out);
     });
@@ -164,7 +174,7 @@ int prgpu_pagerank_observed(prgpu_graph* g, const prgpu_params* p, prgpu_result*
     return guarded([&] {
         if (!out) prgpu::fail(PRGPU_EINVAL, "null result");
         if (g) check_device(g->device);
-        prgpu::SessionPtr s(prgpu::session_create(g, p, false), prgpu::session_destroy);
+        prgpu::SessionPtr s(prgpu::session_create(g, p, false, 0, 0, nullptr, nullptr), prgpu::session_destroy);
         prgpu::session_observed(s.get(), out, fn, user);
     });
 }
@@ -174,7 +184,7 @@ int prgpu_session_create(prgpu_graph* g, const prgpu_params* p, prgpu_session** 
         if (!out) prgpu::fail(PRGPU_EINVAL, "null output pointer");
         *out = nullptr;
         if (g) check_device(g->device);
-        *out = prgpu::session_create(g, p, true);
+        *out = prgpu::session_create(g, p, true, 0, 0, nullptr, nullptr);
     });
 }
 
@@ -208,6 +218,89 @@ int prgpu_error_norm(int norm, const double* r, const double* s, uint64_t n, int
         if (!out || (n && (!r || !s))) prgpu::fail(PRGPU_EINVAL, "null argument");
         check_device(device);
         *out = prgpu::error_norm_device(norm, r, s, n, device);
+    });
+}
+
+int prgpu_part_buffer_sizes(prgpu_graph* g, const prgpu_params* p, int nranks, uint64_t* contrib,
+                            uint64_t* partials) {
+    return guarded([&] {
+        if (!contrib || !partials) prgpu::fail(PRGPU_EINVAL, "null argument");
+        prgpu::part_sizes(g, p, nranks, contrib, partials);
+    });
+}
+
+int prgpu_part_create(prgpu_graph* g, const prgpu_params* p, int rank, int nranks, double* ext_contrib,
+                      double* ext_rank_partials, prgpu_session** out) {
+    return guarded([&] {
+        if (!out) prgpu::fail(PRGPU_EINVAL, "null output pointer");
+        *out = nullptr;
+        if (nranks < 1) prgpu::fail(PRGPU_EINVAL, "partition: nranks must be >= 1");
+        if (g) check_device(g->device);
+        *out = prgpu::session_create(g, p, false, rank, nranks, ext_contrib, ext_rank_partials);
+    });
+}
+
+int prgpu_part_plan(prgpu_session* s, prgpu_partition* parts) {
+    return guarded([&] {
+        if (!s || !parts) prgpu::fail(PRGPU_EINVAL, "null argument");
+        prgpu::part_plan_copy(s, parts);
+    });
+}
+
+int prgpu_part_exchange(prgpu_session* s, prgpu_exchange* ex) {
+    return guarded([&] {
+        if (!s || !ex) prgpu::fail(PRGPU_EINVAL, "null argument");
+        prgpu::part_exchange(s, ex);
+    });
+}
+
+int prgpu_part_set_stream(prgpu_session* s, void* stream) {
+    return guarded([&] {
+        if (!s) prgpu::fail(PRGPU_EINVAL, "null session");
+        prgpu::part_set_stream(s, stream);
+    });
+}
+
+int prgpu_part_init(prgpu_session* s) {
+    return guarded([&] {
+        if (!s) prgpu::fail(PRGPU_EINVAL, "null session");
+        prgpu::session_init(s);
+    });
+}
+
+int prgpu_part_step(prgpu_session* s, int* parity_out) {
+    return guarded([&] {
+        if (!s) prgpu::fail(PRGPU_EINVAL, "null session");
+        const int par = prgpu::part_step(s);
+        if (parity_out) *parity_out = par;
+    });
+}
+
+int prgpu_part_finalize(prgpu_session* s) {
+    return guarded([&] {
+        if (!s) prgpu::fail(PRGPU_EINVAL, "null session");
+        prgpu::part_finalize(s);
+    });
+}
+
+int prgpu_part_active(prgpu_session* s, int* any) {
+    return guarded([&] {
+        if (!s || !any) prgpu::fail(PRGPU_EINVAL, "null argument");
+        *any = prgpu::read_any_active(s);
+    });
+}
+
+int prgpu_part_local_ranks(prgpu_session* s, int lane, double* out) {
+    return guarded([&] {
+        if (!s || !out) prgpu::fail(PRGPU_EINVAL, "null argument");
+        prgpu::part_local_ranks(s, lane, out);
+    });
+}
+
+int prgpu_graph_permutation(const prgpu_graph* g, uint32_t* old_of_new) {
+    return guarded([&] {
+        if (!g || !old_of_new) prgpu::fail(PRGPU_EINVAL, "null argument");
+        prgpu::graph_permutation(g, old_of_new);
     });
 }
 

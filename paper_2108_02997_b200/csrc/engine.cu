@@ -169,9 +169,10 @@ using KernelFn = void (*)(const Params);
 
 struct LaneCfg {
     int LG, W, WIN, KS; // KS: contribution row stride (doubles)
-    KernelFn fn;
-    int KP() const { return LG * W; }
+    KernelFn fn;        // pull_kernel instance
     int QM = kQmAll;
+    KernelFn fin = nullptr; // matching part_finalize_kernel (multi-GPU)
+    int KP() const { return LG * W; }
     size_t smem() const {
         const size_t staged = KP() == 1 ? (size_t)kWarps * 2 * WIN * sizeof(double) : 0; // STAGED
         const size_t cols = W >= 6 ? (size_t)popc_c(QM) * W * kNT * sizeof(double) : 0;    // Partials
@@ -187,10 +188,15 @@ inline int variant() {
 
 // `all_q`: the run needs every partial (all norms / the reference trace);
 // otherwise only L1 + dangling (the damping sweep's stopping rule).
+template <int LG, int W, int WIN, int QJ, int MINB, int QM, int KS>
+LaneCfg mk_cfg() {
+    return LaneCfg{LG, W, WIN, KS ? KS : LG * W, pull_kernel<LG, W, WIN, QJ, MINB, QM, KS>, QM,
+                   part_finalize_kernel<LG, W, WIN, QJ, MINB, QM, KS>};
+}
+
 template <int LG, int W, int WIN, int MINB, int KS = LG * W>
 LaneCfg wide_cfg(bool all_q) {
-    return all_q ? LaneCfg{LG, W, WIN, KS, pull_kernel<LG, W, WIN, 0, MINB, kQmAll, KS>, kQmAll}
-                 : LaneCfg{LG, W, WIN, KS, pull_kernel<LG, W, WIN, 0, MINB, kQmL1, KS>, kQmL1};
+    return all_q ? mk_cfg<LG, W, WIN, 0, MINB, kQmAll, KS>() : mk_cfg<LG, W, WIN, 0, MINB, kQmL1, KS>();
 }
 
 inline LaneCfg lane_cfg(int K, bool all_q) {
@@ -199,10 +205,10 @@ inline LaneCfg lane_cfg(int K, bool all_q) {
     const int var = variant();
     if (K == 1) {
         switch (var) {
-        case 1: return {1, 1, 256, 1, pull_kernel<1, 1, 256, 4, 2>};
-        case 2: return {1, 1, 256, 1, pull_kernel<1, 1, 256, 4, 3>};
-        case 3: return {1, 1, 256, 1, pull_kernel<1, 1, 256, 2, 4>};
-        default: return {1, 1, 256, 1, pull_kernel<1, 1, 256, 2, 3>};
+        case 1: return mk_cfg<1, 1, 256, 4, 2, kQmAll, 0>();
+        case 2: return mk_cfg<1, 1, 256, 4, 3, kQmAll, 0>();
+        case 3: return mk_cfg<1, 1, 256, 2, 4, kQmAll, 0>();
+        default: return mk_cfg<1, 1, 256, 2, 3, kQmAll, 0>();
         }
     }
     // wide lanes: two doubles per thread (one 16-byte load per edge),
@@ -257,6 +263,12 @@ struct prgpu_session {
     bool use_graph = false;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     double last_loop_ms = 0;
+    // multi-GPU partition
+    int part_rank = 0, nranks = 1, host_iter = 0;
+    std::vector<prgpu_partition> parts;
+    DevBuf<double> rank_partials;
+    cudaStream_t ext_stream = nullptr;
+    cudaStream_t cur() const { return ext_stream ? ext_stream : (cudaStream_t)stream; }
 
     ~prgpu_session() {
         if (exec) cudaGraphExecDestroy(exec);
@@ -393,9 +405,112 @@ void build_tasks(prgpu_session* s) {
     P.n_packed = (uint32_t)n_packed;
     P.n_empty_tasks = (n_empty_rows + er - 1) / er;
     P.empty_begin = phi;
+    P.task_begin = 0;
+    P.task_end = P.n_chunk + P.n_packed + P.n_empty_tasks;
+    P.part_mode = 0;
+    P.part_rank = 0;
+    P.nranks = 1;
 }
 
-prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_graph) {
+// ---- 1D partition (multi-GPU): contiguous task ranges with equal cost, cut at
+// row boundaries (a hub row's chunks stay on one rank), so each rank owns a
+// contiguous row range and a contiguous source-id range. --------------------------
+__global__ void task_costs_kernel(Params P, uint32_t er, uint64_t* __restrict__ cost) {
+    const uint32_t T1 = P.n_chunk, T2 = T1 + P.n_packed, T3 = T2 + P.n_empty_tasks;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < T3; t += gridDim.x * blockDim.x) {
+        uint64_t c;
+        if (t < T1) {
+            const uint32_t row = P.chunk_row[t];
+            const uint64_t d = P.row_off[row + 1] - P.row_off[row];
+            const uint64_t off = (uint64_t)(t - P.chunk_first[row]) * P.chunk;
+            c = (d - off < P.chunk ? d - off : P.chunk);
+        } else if (t < T2) {
+            const uint32_t r0 = P.packed_r0[t - T1], r1 = P.packed_r0[t - T1 + 1];
+            c = (P.row_off[r1] - P.row_off[r0]) + 2ull * (r1 - r0);
+        } else {
+            c = 2ull * er;
+        }
+        cost[t] = c;
+    }
+}
+
+__device__ uint32_t row_of_task(const Params& P, uint32_t t, uint32_t er) {
+    const uint32_t T1 = P.n_chunk, T2 = T1 + P.n_packed, T3 = T2 + P.n_empty_tasks;
+    if (t >= T3) return P.n;
+    if (t < T1) return P.chunk_row[t];
+    if (t < T2) return P.packed_r0[t - T1];
+    const uint64_t r = (uint64_t)P.empty_begin + (uint64_t)(t - T2) * er;
+    return r < P.n ? (uint32_t)r : P.n;
+}
+
+// bound[b] for b in [0, nranks]: task, row and source boundaries
+__global__ void partition_kernel(Params P, const uint64_t* __restrict__ incl, uint32_t er, uint32_t nranks,
+                                 const uint32_t* __restrict__ row_of_src, uint32_t nsrc,
+                                 uint64_t* __restrict__ bound /* [nranks+1][3] */) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nranks) return;
+    const uint32_t T = P.n_chunk + P.n_packed + P.n_empty_tasks;
+    uint32_t t;
+    if (b == 0) t = 0;
+    else if (b == nranks) t = T;
+    else {
+        const uint64_t total = T ? incl[T - 1] : 0, target = total * b / nranks;
+        uint32_t lo = 0, hi = T; // first task whose exclusive prefix >= target
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) / 2;
+            if ((mid ? incl[mid - 1] : 0) < target) lo = mid + 1; else hi = mid;
+        }
+        t = lo;
+        if (t < P.n_chunk && t != P.chunk_first[P.chunk_row[t]]) t = P.chunk_first[P.chunk_row[t] + 1];
+    }
+    const uint32_t row = row_of_task(P, t, er);
+    uint32_t lo = 0, hi = nsrc; // sources with engine row < row
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (row_of_src[mid] < row) lo = mid + 1; else hi = mid;
+    }
+    bound[3 * b + 0] = t;
+    bound[3 * b + 1] = row;
+    bound[3 * b + 2] = lo;
+}
+
+void plan_partition(prgpu_session* s, int nranks) {
+    const prgpu_graph* g = s->g;
+    cudaStream_t st = s->stream;
+    Params& P = s->P;
+    const uint32_t T = P.n_chunk + P.n_packed + P.n_empty_tasks;
+    const uint32_t er = 8 * (32 / s->cfg.LG);
+    DevBuf<uint64_t> cost(std::max<uint32_t>(T, 1)), bound(3 * ((size_t)nranks + 1));
+    if (T) {
+        task_costs_kernel<<<blocks_for(T), kNT, 0, st>>>(P, er, cost.p);
+        PRGPU_LAUNCHED("task_costs");
+        size_t tmp = 0;
+        PRGPU_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, cost.p, cost.p, (int64_t)T, st));
+        DevBuf<char> t(std::max<size_t>(tmp, 1));
+        PRGPU_CUDA(cub::DeviceScan::InclusiveSum(t.p, tmp, cost.p, cost.p, (int64_t)T, st));
+        g_launches.fetch_add(1);
+    }
+    partition_kernel<<<1, 64, 0, st>>>(P, cost.p, er, (uint32_t)nranks, g->row_of_src.p, g->nsrc, bound.p);
+    PRGPU_LAUNCHED("partition");
+    std::vector<uint64_t> b(3 * ((size_t)nranks + 1));
+    PRGPU_CUDA(cudaMemcpyAsync(b.data(), bound.p, b.size() * 8, cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    for (int r = 1; r <= nranks; ++r) // monotone after the row-boundary adjustment
+        for (int f = 0; f < 3; ++f) b[3 * r + f] = std::max(b[3 * r + f], b[3 * (r - 1) + f]);
+    s->parts.resize(nranks);
+    for (int r = 0; r < nranks; ++r) {
+        prgpu_partition& q = s->parts[r];
+        q.task_begin = (uint32_t)b[3 * r];
+        q.task_end = (uint32_t)b[3 * (r + 1)];
+        q.row_begin = (uint32_t)b[3 * r + 1];
+        q.row_end = (uint32_t)b[3 * (r + 1) + 1];
+        q.src_begin = b[3 * r + 2];
+        q.src_end = b[3 * (r + 1) + 2];
+    }
+}
+
+prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_graph, int rank = 0,
+                              int nranks = 0, double* ext_contrib = nullptr, double* ext_rp = nullptr) {
     validate_params(p);
     if (!g || g->n == 0) fail(PRGPU_EINVAL, "pagerank: graph has no vertices");
     DeviceGuard dg(g->device);
@@ -415,8 +530,12 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
 
     s->rank.alloc(2 * (size_t)K * n);
     const int KS = s->cfg.KS;
-    s->contrib.alloc(2 * nsrc * KS);
-    PRGPU_CUDA(cudaMemsetAsync(s->contrib.p, 0, 2 * nsrc * KS * sizeof(double), st));
+    double* cbase = ext_contrib;
+    if (!cbase) {
+        s->contrib.alloc(2 * nsrc * KS);
+        cbase = s->contrib.p;
+    }
+    PRGPU_CUDA(cudaMemsetAsync(cbase, 0, 2 * nsrc * KS * sizeof(double), st));
     s->trace.alloc((size_t)s->max_iter * K * 4);
     PRGPU_CUDA(cudaMemsetAsync(s->trace.p, 0, (size_t)s->max_iter * K * 4 * sizeof(double), st));
     s->lanes.alloc(K);
@@ -474,10 +593,29 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     P.l2mode = 0;
     if (const char* m = std::getenv("PRGPU_L2MODE")) P.l2mode = (uint32_t)std::atoi(m);
     P.hot_src = 0;
-    P.cbase = s->contrib.p;
+    P.cbase = cbase;
     P.cold_off[0] = 0;
     P.cold_off[1] = nsrc;
     build_tasks(s.get());
+    if (nranks >= 1) { // partition session (nranks == 0: the fused single-GPU run)
+        if (rank < 0 || rank >= nranks) fail(PRGPU_EINVAL, "partition: rank out of range");
+        plan_partition(s.get(), nranks);
+        const prgpu_partition& me = s->parts[rank];
+        s->part_rank = rank;
+        s->nranks = nranks;
+        P.task_begin = me.task_begin;
+        P.task_end = me.task_end;
+        P.part_mode = 1;
+        P.part_rank = (uint32_t)rank;
+        P.nranks = (uint32_t)nranks;
+        double* rp = ext_rp;
+        if (!rp) {
+            s->rank_partials.alloc((size_t)nranks * kNQ * KP);
+            rp = s->rank_partials.p;
+        }
+        P.rank_partials = rp;
+        build_graph = false;
+    }
 
     // persistent grid: resident CTAs, but at least ~4 tasks per warp
     const size_t smem = s->cfg.smem();
@@ -487,7 +625,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     PRGPU_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, g->device));
     PRGPU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)s->cfg.fn, kNT, smem));
     per_sm = std::max(1, per_sm);
-    const uint64_t tasks = (uint64_t)P.n_chunk + P.n_packed + P.n_empty_tasks;
+    const uint64_t tasks = (uint64_t)P.task_end - P.task_begin;
     const uint64_t want = (tasks + kWarps * 4 - 1) / (kWarps * 4);
     const uint32_t G = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)dev_sms * per_sm, want));
     P.G = G;
@@ -532,6 +670,28 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     return s.release();
 }
 
+void part_plan_copy(prgpu_session* s, prgpu_partition* parts) {
+    if (s->parts.empty()) fail(PRGPU_EINVAL, "not a partition session");
+    std::copy(s->parts.begin(), s->parts.end(), parts);
+}
+
+void part_set_stream(prgpu_session* s, void* stream) { s->ext_stream = (cudaStream_t)stream; }
+
+void graph_permutation(const prgpu_graph* g, uint32_t* old_of_new) {
+    DeviceGuard dg(g->device);
+    PRGPU_CUDA(cudaMemcpy(old_of_new, g->old_of_new.p, (size_t)g->n * 4, cudaMemcpyDeviceToHost));
+}
+
+void part_sizes(prgpu_graph* g, const prgpu_params* p, int nranks, uint64_t* contrib, uint64_t* partials) {
+    validate_params(p);
+    if (!g || nranks < 1) fail(PRGPU_EINVAL, "partition: bad graph or nranks");
+    const uint32_t mask = p->stop_mask ? p->stop_mask : (1u << p->norm);
+    const bool l1_only = mask == 1u && p->norm == PRGPU_NORM_L1 && !p->ref_ranks;
+    const LaneCfg c = lane_cfg(p->lanes, !l1_only);
+    *contrib = 2ull * std::max<uint64_t>(g->nsrc, 1) * c.KS;
+    *partials = (uint64_t)nranks * kNQ * c.KP();
+}
+
 void session_destroy(prgpu_session* s) {
     if (!s) return;
     int prev = 0;
@@ -542,25 +702,68 @@ void session_destroy(prgpu_session* s) {
 }
 
 void session_init(prgpu_session* s) {
+    // pageable host sources: the copies are staged before the call returns
     PRGPU_CUDA(cudaMemcpyAsync(s->lanes.p, s->lanes_host.data(), s->K * sizeof(LaneState),
-                               cudaMemcpyHostToDevice, s->stream));
+                               cudaMemcpyHostToDevice, s->cur()));
     GlobalState gsh{0, 1, 0u, s->max_iter};
-    PRGPU_CUDA(cudaMemcpyAsync(s->gs.p, &gsh, sizeof(gsh), cudaMemcpyHostToDevice, s->stream));
-    launch_init(s->cfg, s->P, s->g->ndangling, s->stream);
+    PRGPU_CUDA(cudaMemcpyAsync(s->gs.p, &gsh, sizeof(gsh), cudaMemcpyHostToDevice, s->cur()));
+    launch_init(s->cfg, s->P, s->g->ndangling, s->cur());
+    s->host_iter = 0;
 }
 
 void launch_pull(prgpu_session* s) {
     Params P = s->P;
     P.use_cond = 0;
-    s->cfg.fn<<<P.G, kNT, s->cfg.smem(), s->stream>>>(P);
+    s->cfg.fn<<<P.G, kNT, s->cfg.smem(), s->cur()>>>(P);
     PRGPU_LAUNCHED("pull_kernel");
 }
 
 int read_any_active(prgpu_session* s) {
     GlobalState gsh;
-    PRGPU_CUDA(cudaMemcpyAsync(&gsh, s->gs.p, sizeof(gsh), cudaMemcpyDeviceToHost, s->stream));
-    PRGPU_CUDA(cudaStreamSynchronize(s->stream));
+    PRGPU_CUDA(cudaMemcpyAsync(&gsh, s->gs.p, sizeof(gsh), cudaMemcpyDeviceToHost, s->cur()));
+    PRGPU_CUDA(cudaStreamSynchronize(s->cur()));
     return gsh.any_active;
+}
+
+// ---- partition sessions ----------------------------------------------------------
+void part_exchange(prgpu_session* s, prgpu_exchange* ex) {
+    const int KS = s->cfg.KS;
+    ex->contrib[0] = s->P.cbase + s->P.cold_off[0] * KS;
+    ex->contrib[1] = s->P.cbase + s->P.cold_off[1] * KS;
+    ex->stride = (uint32_t)KS;
+    ex->nsrc = std::max<uint64_t>(s->g->nsrc, 1);
+    ex->rank_partials = s->P.rank_partials;
+    ex->partials_per_rank = (uint32_t)(kNQ * s->KP);
+}
+
+int part_step(prgpu_session* s) {
+    DeviceGuard dg(s->g->device);
+    launch_pull(s);
+    return ++s->host_iter & 1; // the buffer this iteration wrote
+}
+
+void part_finalize(prgpu_session* s) {
+    DeviceGuard dg(s->g->device);
+    s->cfg.fin<<<1, kNT, 0, s->cur()>>>(s->P);
+    PRGPU_LAUNCHED("part_finalize");
+}
+
+void part_local_ranks(prgpu_session* s, int user_lane, double* out) {
+    DeviceGuard dg(s->g->device);
+    int slot = -1;
+    for (int k = 0; k < s->K; ++k)
+        if (s->user_of[k] == user_lane) slot = k;
+    if (slot < 0) fail(PRGPU_EINVAL, "local_ranks: lane out of range");
+    LaneState L;
+    PRGPU_CUDA(cudaMemcpyAsync(&L, s->lanes.p + slot, sizeof(L), cudaMemcpyDeviceToHost, s->cur()));
+    PRGPU_CUDA(cudaStreamSynchronize(s->cur()));
+    const prgpu_partition& me = s->parts[s->part_rank];
+    const uint32_t stored_end = std::min(me.row_end, s->P.empty_begin);
+    if (stored_end > me.row_begin)
+        PRGPU_CUDA(cudaMemcpyAsync(out, s->P.rank[L.iterations & 1] + (size_t)slot * s->g->n + me.row_begin,
+                                   (size_t)(stored_end - me.row_begin) * 8, cudaMemcpyDeviceToHost, s->cur()));
+    PRGPU_CUDA(cudaStreamSynchronize(s->cur()));
+    for (uint32_t r = std::max(me.row_begin, stored_end); r < me.row_end; ++r) out[r - me.row_begin] = L.c0_used;
 }
 
 double session_run(prgpu_session* s) {

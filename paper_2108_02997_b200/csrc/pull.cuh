@@ -105,6 +105,13 @@ struct Params {
     uint32_t hot_src;            // sources [0, hot_src) in the L2-resident region
     uint32_t l2mode;             // 0 evict hints, 1 persisting window, 2 no hints
     uint32_t skip_mask;          // profiling only (PRGPU_SKIP): 1 chunk, 2 packed, 4 empty tasks
+    // multi-GPU partition (1D row ranges): this rank runs tasks [task_begin, task_end)
+    // and leaves its partial vector in rank_partials[part_rank]; a separate
+    // finalize reduces all ranks' vectors in rank order after the exchange
+    uint32_t task_begin, task_end;
+    int part_mode;
+    uint32_t part_rank, nranks;
+    double* rank_partials;       // [nranks][kNQ*KP]
     int use_cond;
     cudaGraphConditionalHandle cond;
 };
@@ -575,6 +582,66 @@ struct Warp {
     }
 };
 
+// Per-lane convergence and the next teleport from the reduced partials
+// (pagerank.hpp:87, :95-99); thread k < K handles lane k, thread 0 the loop flag.
+template <int KP, int QM>
+__device__ void finalize_lanes(const Params& P, const double* s_tot, const double* s_c0,
+                               const int* s_active, int iter) {
+    const int tid = threadIdx.x;
+    if (tid < (int)P.K && s_active[tid]) {
+        const int k = tid;
+        LaneState& L = P.lanes[k];
+        // rows with no in-edges all moved from prev_empty to c0 (exactly); add
+        // their terms once instead of per row
+        const double c0 = s_c0[k];
+        const double de = __dsub_rn(c0, L.prev_empty);
+        const double ade = fabs(de);
+        const double n_empty = (double)(P.n - P.empty_begin), n_iso = (double)(P.n - P.iso_begin);
+        double l1s = s_tot[0 * KP + k], l2s = s_tot[1 * KP + k], linf = s_tot[2 * KP + k];
+        double dang = s_tot[3 * KP + k];
+        if (P.n > P.empty_begin) {
+            l1s = __dadd_rn(l1s, __dmul_rn(n_empty, ade));
+            l2s = __dadd_rn(l2s, __dmul_rn(n_empty, __dmul_rn(de, de)));
+            linf = fmax(linf, ade);
+            dang = __dadd_rn(dang, __dmul_rn(n_iso, c0));
+        }
+        const double l2 = sqrt(l2s);
+        double* tr = P.trace + ((size_t)iter * P.K + k) * 4;
+        tr[0] = (QM & 1) ? l1s : NAN;
+        tr[1] = (QM & 2) ? l2 : NAN;
+        tr[2] = (QM & 4) ? linf : NAN;
+        tr[3] = (QM & 16) ? s_tot[4 * KP + k] : NAN;
+        const double errs[3] = {l1s, l2, linf};
+        const int done = iter + 1;
+        L.iterations = done;
+        L.final_err = errs[L.report_norm];
+        L.c0_used = c0;
+        L.prev_empty = c0;
+        bool stop = true; // every norm in the mask strictly below tau (pagerank.hpp:99)
+        for (int q = 0; q < 3; ++q)
+            if ((L.stop_mask >> q) & 1u) stop = stop && (errs[q] < L.tol);
+        if (stop) {
+            L.converged = 1;
+            L.active = 0;
+        } else if (done >= P.gs->max_iter) {
+            L.active = 0;
+        }
+        // teleport = (1 - alpha)/n + alpha*dangling_sum/n   (pagerank.hpp:87)
+        const double a = L.alpha, nd = (double)P.n;
+        L.c0 = __dadd_rn(__ddiv_rn(__dsub_rn(1.0, a), nd), __ddiv_rn(__dmul_rn(a, dang), nd));
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int any = 0;
+        for (uint32_t k = 0; k < P.K; ++k) any |= P.lanes[k].active;
+        P.gs->iter = iter + 1;
+        P.gs->any_active = any;
+        P.gs->counter = 0;
+        __threadfence();
+        if (P.use_cond) cudaGraphSetConditional(P.cond, any ? 1u : 0u);
+    }
+}
+
 template <int LG, int W, int WIN, int QJ_, int MINB, int QM = kQmAll, int KS_ = 0>
 __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     using C = PullCfg<LG, W, WIN, QJ_, KS_>;
@@ -605,8 +672,8 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
                                      s_dyn + (size_t)kWarps * C::SMEM_WARP, tid);
     double* sv = s_dyn + (size_t)warp * C::SMEM_WARP;
     const uint32_t TW = P.G * kWarps;
-    const uint32_t T1 = P.n_chunk, T2 = T1 + P.n_packed, T3 = T2 + P.n_empty_tasks;
-    for (uint32_t t = blockIdx.x * kWarps + warp; t < T3; t += TW) {
+    const uint32_t T1 = P.n_chunk, T2 = T1 + P.n_packed;
+    for (uint32_t t = P.task_begin + blockIdx.x * kWarps + warp; t < P.task_end; t += TW) {
         if (t < T1) {
             if (!(P.skip_mask & 1)) w.chunk_task(t);
         } else if (t < T2) {
@@ -665,59 +732,41 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
         if (lane == 0) s_tot[t] = v;
     }
     __syncthreads();
-    const int iter = s_iter; // iterations completed before this launch
-    if (tid < (int)P.K && s_active[tid]) {
-        const int k = tid;
-        LaneState& L = P.lanes[k];
-        // rows with no in-edges all moved from prev_empty to c0 (exactly); add
-        // their terms once instead of per row
-        const double c0 = s_c0[k];
-        const double de = __dsub_rn(c0, L.prev_empty);
-        const double ade = fabs(de);
-        const double n_empty = (double)(P.n - P.empty_begin), n_iso = (double)(P.n - P.iso_begin);
-        double l1s = s_tot[0 * KP + k], l2s = s_tot[1 * KP + k], linf = s_tot[2 * KP + k];
-        double dang = s_tot[3 * KP + k];
-        if (P.n > P.empty_begin) {
-            l1s = __dadd_rn(l1s, __dmul_rn(n_empty, ade));
-            l2s = __dadd_rn(l2s, __dmul_rn(n_empty, __dmul_rn(de, de)));
-            linf = fmax(linf, ade);
-            dang = __dadd_rn(dang, __dmul_rn(n_iso, c0));
+    if (P.part_mode) { // multi-GPU: publish this rank's vector; finalize runs after the exchange
+        for (int t = tid; t < kNQ * KP; t += kNT) P.rank_partials[(size_t)P.part_rank * kNQ * KP + t] = s_tot[t];
+        if (tid == 0) P.gs->counter = 0;
+        return;
+    }
+    finalize_lanes<KP, QM>(P, s_tot, s_c0, s_active, s_iter);
+}
+
+// Multi-GPU finalize (one CTA, identical on every rank): the ranks' partial
+// vectors reduced in rank order, then the same lane update as the fused path.
+template <int LG, int W, int WIN, int QJ_, int MINB, int QM = kQmAll, int KS_ = 0>
+__global__ void __launch_bounds__(kNT) part_finalize_kernel(const Params P) {
+    constexpr int KP = PullCfg<LG, W, WIN, QJ_, KS_>::KP;
+    __shared__ double s_c0[KP], s_tot[kNQ * KP];
+    __shared__ int s_active[KP];
+    __shared__ int s_iter;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_iter = P.gs->iter;
+    if (tid < KP) {
+        const bool real = tid < (int)P.K;
+        s_c0[tid] = real ? P.lanes[tid].c0 : 0.0;
+        s_active[tid] = real ? P.lanes[tid].active : 0;
+    }
+    for (int t = tid; t < kNQ * KP; t += kNT) {
+        const int q = t / KP;
+        double v = 0.0;
+        for (uint32_t r = 0; r < P.nranks; ++r) {
+            const double x = P.rank_partials[(size_t)r * kNQ * KP + t];
+            v = (q == 2) ? fmax(v, x) : v + x;
         }
-        const double l2 = sqrt(l2s);
-        double* tr = P.trace + ((size_t)iter * P.K + k) * 4;
-        tr[0] = (QM & 1) ? l1s : NAN;
-        tr[1] = (QM & 2) ? l2 : NAN;
-        tr[2] = (QM & 4) ? linf : NAN;
-        tr[3] = (QM & 16) ? s_tot[4 * KP + k] : NAN;
-        const double errs[3] = {l1s, l2, linf};
-        const int done = iter + 1;
-        L.iterations = done;
-        L.final_err = errs[L.report_norm];
-        L.c0_used = c0;
-        L.prev_empty = c0;
-        bool stop = true; // every norm in the mask strictly below tau (pagerank.hpp:99)
-        for (int q = 0; q < 3; ++q)
-            if ((L.stop_mask >> q) & 1u) stop = stop && (errs[q] < L.tol);
-        if (stop) {
-            L.converged = 1;
-            L.active = 0;
-        } else if (done >= P.gs->max_iter) {
-            L.active = 0;
-        }
-        // teleport = (1 - alpha)/n + alpha*dangling_sum/n   (pagerank.hpp:87)
-        const double a = L.alpha, nd = (double)P.n;
-        L.c0 = __dadd_rn(__ddiv_rn(__dsub_rn(1.0, a), nd), __ddiv_rn(__dmul_rn(a, dang), nd));
+        s_tot[t] = v;
     }
     __syncthreads();
-    if (tid == 0) {
-        int any = 0;
-        for (uint32_t k = 0; k < P.K; ++k) any |= P.lanes[k].active;
-        P.gs->iter = iter + 1;
-        P.gs->any_active = any;
-        P.gs->counter = 0;
-        __threadfence();
-        if (P.use_cond) cudaGraphSetConditional(P.cond, any ? 1u : 0u);
-    }
+    if (!P.gs->any_active) return;
+    finalize_lanes<KP, QM>(P, s_tot, s_c0, s_active, s_iter);
 }
 
 } // namespace prgpu

@@ -1,0 +1,244 @@
+"""Multi-GPU pull PageRank: 1D row partition, one process per GPU.
+
+Each rank owns a contiguous, cost-balanced range of engine rows (a hub row is
+never split across ranks) and so a contiguous range of source ids.  Per
+iteration:
+
+  1. ``prgpu_part_step``     — local pull over the rank's rows (sm_100a kernel)
+  2. exchange                — every rank's new contribution rows and its
+                               partial-sum vector reach every rank
+                               (``torch.distributed`` over NCCL / NVLink)
+  3. ``prgpu_part_finalize`` — the ranks' partial vectors are reduced in rank
+                               order, so c0 and the stop decision are identical
+                               on every rank (and deterministic)
+
+The exchanged buffers are torch tensors handed to the engine, so NCCL moves
+them in place; engine work is enqueued on torch's current stream.
+``emulate`` runs the same protocol with several partitions in one process on
+one GPU (buffer copies instead of NCCL) — that is how the partitioned path is
+checked bit-for-bit against the single-GPU run when only one GPU is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+from .pagerank_lab import CsrGraph, NormKind, _params
+
+
+@dataclass
+class PartResult:
+    iterations: np.ndarray     # [K]
+    ranks: Optional[np.ndarray]  # [K, n] original vertex ids (when gathered)
+    run_iterations: int
+    loop_ms: float
+
+
+class _Part:
+    """One rank's engine session plus its exchange buffers (torch tensors)."""
+
+    def __init__(self, g: CsrGraph, alphas, tolerance, norm, max_iterations, stop_mask, rank,
+                 nranks, device):
+        import torch
+        self.torch = torch
+        self.g = g
+        self.K = len(alphas)
+        self.rank, self.nranks = rank, nranks
+        p, self._keep = _params(list(alphas), tolerance, norm, max_iterations, stop_mask)
+        self._p = p
+        nc, npart = C.c_uint64(), C.c_uint64()
+        check(lib().prgpu_part_buffer_sizes(g.handle, C.byref(p), nranks, C.byref(nc),
+                                            C.byref(npart)), "part sizes")
+        dev = torch.device("cuda", device)
+        self.contrib = torch.empty(nc.value, dtype=torch.float64, device=dev)
+        self.partials = torch.zeros(npart.value, dtype=torch.float64, device=dev)
+        self._s = C.c_void_p()
+        check(lib().prgpu_part_create(g.handle, C.byref(p), rank, nranks, self.contrib.data_ptr(),
+                                      self.partials.data_ptr(), C.byref(self._s)), "part create")
+        parts = (_lib.Partition * nranks)()
+        check(lib().prgpu_part_plan(self._s, parts), "part plan")
+        self.parts = [parts[i] for i in range(nranks)]
+        ex = _lib.Exchange()
+        check(lib().prgpu_part_exchange(self._s, C.byref(ex)), "part exchange")
+        self.stride = ex.stride
+        self.nsrc = ex.nsrc
+        self.ppr = ex.partials_per_rank
+        base = self.contrib.data_ptr()
+        # views of the two parity buffers and of each rank's rows in them
+        self.buf = [self.contrib[(ex.contrib[i] - base) // 8:(ex.contrib[i] - base) // 8 +
+                                 self.nsrc * self.stride] for i in (0, 1)]
+        self.slot = self.partials.view(nranks, self.ppr)
+
+    def chunk(self, parity, r):
+        q = self.parts[r]
+        return self.buf[parity][q.src_begin * self.stride:q.src_end * self.stride]
+
+    def set_stream(self):
+        s = self.torch.cuda.current_stream(self.contrib.device).cuda_stream
+        if not s:
+            raise RuntimeError("run inside `with torch.cuda.stream(...)`: the legacy default "
+                               "stream cannot be shared with the engine")
+        check(lib().prgpu_part_set_stream(self._s, C.c_void_p(s)), "part stream")
+
+    def init(self):
+        check(lib().prgpu_part_init(self._s), "part init")
+
+    def step(self) -> int:
+        par = C.c_int()
+        check(lib().prgpu_part_step(self._s, C.byref(par)), "part step")
+        return par.value
+
+    def finalize(self):
+        check(lib().prgpu_part_finalize(self._s), "part finalize")
+
+    def active(self) -> bool:
+        a = C.c_int()
+        check(lib().prgpu_part_active(self._s, C.byref(a)), "part active")
+        return bool(a.value)
+
+    def local_ranks(self, lane) -> np.ndarray:
+        q = self.parts[self.rank]
+        out = np.zeros(q.row_end - q.row_begin, np.float64)
+        check(lib().prgpu_part_local_ranks(self._s, lane, out.ctypes.data), "local ranks")
+        return out
+
+    def close(self):
+        if self._s:
+            lib().prgpu_session_free(self._s)
+            self._s = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _permutation(g: CsrGraph) -> np.ndarray:
+    perm = np.zeros(g.vertex_count, np.uint32)
+    check(lib().prgpu_graph_permutation(g.handle, perm.ctypes.data), "permutation")
+    return perm
+
+
+def _assemble(g: CsrGraph, chunks_by_rank, K) -> np.ndarray:
+    """Concatenate per-rank engine-row chunks and map back to caller ids."""
+    perm = _permutation(g)
+    out = np.zeros((K, g.vertex_count), np.float64)
+    for k in range(K):
+        eng = np.concatenate([c[k] for c in chunks_by_rank])
+        out[k, perm] = eng
+    return out
+
+
+def emulate(g: CsrGraph, alphas: Sequence[float], nranks: int, tolerance=1e-6,
+            norm: NormKind = NormKind.L1, max_iterations: int = 500, stop_mask: int = 0,
+            want_ranks: bool = True) -> PartResult:
+    """All `nranks` partitions in this process on this GPU; the exchange is a
+    device copy of each rank's rows into every other rank's buffers."""
+    import torch
+    dev = g.device
+    parts = [_Part(g, alphas, tolerance, norm, max_iterations, stop_mask, r, nranks, dev)
+             for r in range(nranks)]
+    stream = torch.cuda.Stream(device=dev)  # a real stream: the legacy default is handle 0
+    with torch.cuda.stream(stream):
+        return _emulate_on(parts, alphas, max_iterations, want_ranks, g)
+
+
+def _emulate_on(parts, alphas, max_iterations, want_ranks, g):
+    import torch
+    for p in parts:
+        p.set_stream()
+        p.init()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    its = 0
+    while its < max_iterations:
+        pars = [p.step() for p in parts]
+        par = pars[0]
+        for dst in parts:
+            for r, src in enumerate(parts):
+                if src is not dst:
+                    dst.chunk(par, r).copy_(src.chunk(par, r))
+                    dst.slot[r].copy_(src.slot[r])
+        for p in parts:
+            p.finalize()
+        its += 1
+        if not parts[0].active():
+            break
+    stop.record()
+    torch.cuda.synchronize()
+    K = len(alphas)
+    res = PartResult(iterations=np.zeros(K, np.int32), ranks=None, run_iterations=its,
+                     loop_ms=start.elapsed_time(stop))
+    if want_ranks:
+        chunks = [[p.local_ranks(k) for k in range(K)] for p in parts]
+        res.ranks = _assemble(g, chunks, K)
+    res.iterations[:] = _lane_iterations(parts[0])
+    for p in parts:
+        p.close()
+    return res
+
+
+def _lane_iterations(part: _Part) -> np.ndarray:
+    """Per-lane iteration counts from the session's result call."""
+    K = part.K
+    its = np.zeros(K, np.int32)
+    r = _lib.Result(None, its.ctypes.data_as(C.POINTER(C.c_int)), None, None, None, 0.0, 0)
+    check(lib().prgpu_session_results(part._s, C.byref(r)), "results")
+    return its
+
+
+def run_distributed(g: CsrGraph, alphas: Sequence[float], tolerance=1e-6,
+                    norm: NormKind = NormKind.L1, max_iterations: int = 500, stop_mask: int = 0,
+                    want_ranks: bool = False) -> PartResult:
+    """One rank of an N-GPU run (torch.distributed initialised with NCCL,
+    one process per GPU).  Contribution rows of rank r travel by a broadcast
+    from r; the partial vectors by an all-gather."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    stream = torch.cuda.Stream(device=g.device)  # engine, copies and NCCL share it
+    with torch.cuda.stream(stream):
+        return _run_distributed_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ranks,
+                                   rank, world)
+
+
+def _run_distributed_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ranks, rank, world):
+    import torch
+    import torch.distributed as dist
+    part = _Part(g, alphas, tolerance, norm, max_iterations, stop_mask, rank, world, g.device)
+    part.set_stream()
+    part.init()
+    mine = torch.empty(part.ppr, dtype=torch.float64, device=part.contrib.device)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    start.record()
+    its = 0
+    while its < max_iterations:
+        par = part.step()
+        if world > 1:
+            for r in range(world):
+                dist.broadcast(part.chunk(par, r), src=r)
+            mine.copy_(part.slot[rank])
+            dist.all_gather_into_tensor(part.partials, mine)
+        part.finalize()
+        its += 1
+        if not part.active():
+            break
+    stop.record()
+    torch.cuda.synchronize()
+    K = len(alphas)
+    res = PartResult(iterations=_lane_iterations(part), ranks=None, run_iterations=its,
+                     loop_ms=start.elapsed_time(stop))
+    if want_ranks:
+        local = [part.local_ranks(k) for k in range(K)]
+        gathered = [None] * world
+        dist.all_gather_object(gathered, local)
+        res.ranks = _assemble(g, gathered, K)
+    part.close()
+    return res
