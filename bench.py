@@ -21,8 +21,9 @@ lanes on one GPU, tau 1e-6, L1, max 500 iterations, fp64.
 
 --impl reference times the reference's own pagerank (oracle/_ref, compiled
 from the reference headers; else the oracle/ C port) on this box's host cores.
-Multi-GPU (torchrun): every rank runs an independent replica of the sweep
-(weak scaling, no data-path collective); rank 0 prints the line.
+Multi-GPU (torchrun): the graph is 1D-partitioned across the ranks (row
+ranges, NCCL exchange of contributions + partial sums every iteration; strong
+scaling); --replicas runs independent copies instead (weak scaling).
 """
 from __future__ import annotations
 
@@ -379,6 +380,60 @@ def run_ours(args, cfg):
     return 0
 
 
+def run_partitioned(args, cfg):
+    """N > 1 (torchrun): the 1D row partition of SURVEY 8e — every rank pulls
+    its cost-balanced row range, contributions and partials are exchanged over
+    NCCL each iteration (strong scaling: the job is the same graph at any N)."""
+    import torch
+    import torch.distributed as tdist
+    import paper_2108_02997_b200 as prl
+    from paper_2108_02997_b200 import distributed
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if cfg["kind"] == "rmat":
+        g = prl.generate_rmat(cfg["scale"], 16, 0.57, 0.19, 0.19, SEED, device=local)
+    else:
+        g = prl.generate_grid(cfg["side"], 0.6, 0.01, SEED, device=local)
+    n, e = g.vertex_count, g.edge_count()
+    run = lambda: distributed.run_distributed(g, cfg["alphas"], cfg["tol"],  # noqa: E731
+                                              prl.NormKind(cfg["norm"]), 500, cfg.get("stop_mask", 0))
+    for _ in range(args.warmup):
+        r = run()
+    iters = r.iterations
+    lane_its = int(np.sum(iters))
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        ms = []
+        for _ in range(args.steps):
+            r = run()
+            ms.append(r.loop_ms)
+        wall = time.perf_counter() - t0
+    t = torch.tensor([float(sum(ms))], device=f"cuda:{local}", dtype=torch.float64)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    value = lane_its * e / (ms_per_step / 1e3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded RMAT/grid generated on the device (DESIGN.md)",
+            "config": {"workload": cfg["workload"], "vertices": n, "edges": e,
+                       "iterations_per_lane": iters.tolist(), "lane_iterations": lane_its,
+                       "parallelism": f"1D row partition x{world}, NCCL exchange per iteration",
+                       "timed_scope": "iteration loop incl. exchange, CUDA events, max over ranks",
+                       "wall_s": wall},
+            "gpu_launches": args.steps * r.run_iterations * 2,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    tdist.barrier()
+    tdist.destroy_process_group()
+    return 0
+
+
 def measure_e2e(args, cfg, g, prl, torch, dev, lane_its):
     """C-ABI call with host buffers: prgpu_graph_from_csr (pinned H2D of the
     reference-layout CSR + device relabel) -> prgpu_pagerank (K lanes, ranks
@@ -431,12 +486,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent replicas (weak scaling) instead of the 1D partition")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference_arm(args, cfg)
+    if (env_rank()[1] > 1 or os.environ.get("PRGPU_BENCH_PARTITION")) and not args.replicas:
+        return run_partitioned(args, cfg)
     return run_ours(args, cfg)
 
 
