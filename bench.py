@@ -455,12 +455,18 @@ def measure_e2e(args, cfg, g, prl, torch, dev, lane_its):
                     its.ctypes.data_as(C.POINTER(C.c_int)),
                     conv.ctypes.data_as(C.POINTER(C.c_uint8)), None, None, 0.0, 0)
 
+    split = []
+
     def step():
         h = C.c_void_p()
+        t0 = time.perf_counter()
         _lib.check(L.prgpu_graph_from_csr(n, off.data_ptr(), nbr.data_ptr(), deg.data_ptr(), dev,
                                           C.byref(h)), "graph_from_csr")
+        t1 = time.perf_counter()
         _lib.check(L.prgpu_pagerank(h, C.byref(p), C.byref(r)), "pagerank")
+        t2 = time.perf_counter()
         L.prgpu_graph_free(h)
+        split.append((t1 - t0, t2 - t1, time.perf_counter() - t2))
 
     for _ in range(max(1, args.warmup // 2)):
         step()
@@ -469,6 +475,10 @@ def measure_e2e(args, cfg, g, prl, torch, dev, lane_its):
     for _ in range(steps):
         step()
     dt = (time.perf_counter() - t0) / steps
+    if os.environ.get("PRGPU_TIMING_LOG"):
+        for a_, b_, c_ in split:
+            print(f"e2e split: from_csr {a_ * 1e3:.1f} ms, pagerank {b_ * 1e3:.1f} ms, free {c_ * 1e3:.1f} ms",
+                  file=sys.stderr)
     h2d = 8 * (n + 1) + 4 * e + 4 * n + 8 * K
     d2h = 8 * K * n + 13 * K
     return {"value": lane_its * e / dt / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": h2d,

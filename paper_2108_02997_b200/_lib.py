@@ -10,7 +10,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libprgpu.so")
+LIB_PATH = os.environ.get("PRGPU_LIB") or os.path.join(HERE, "libprgpu.so")  # override: tuning builds
 
 PRGPU_OK, PRGPU_EINVAL, PRGPU_ECUDA, PRGPU_ENCCL, PRGPU_ENOMEM = 0, 1, 2, 3, 4
 MAX_LANES = 16

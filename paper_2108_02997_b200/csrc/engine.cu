@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <memory>
 #include <vector>
@@ -174,7 +175,8 @@ struct LaneCfg {
     KernelFn fin = nullptr; // matching part_finalize_kernel (multi-GPU)
     int KP() const { return LG * W; }
     size_t smem() const {
-        const size_t staged = KP() == 1 ? (size_t)kWarps * 2 * WIN * sizeof(double) : 0; // STAGED
+        const size_t staged = KP() == 1 ? (size_t)kWarps * 2 * WIN * sizeof(double) // STAGED
+                                        : 0;
         const size_t cols = W >= 6 ? (size_t)popc_c(QM) * W * kNT * sizeof(double) : 0;    // Partials
         return staged + cols;
     }
@@ -218,7 +220,8 @@ inline LaneCfg lane_cfg(int K, bool all_q) {
     if (K <= 8) return wide_cfg<4, 2, 128, 4>(all_q);
     if (K <= 12) {
         if (var == 1) return wide_cfg<8, 2, 64, 4, 12>(all_q);
-        if (var == 2) return wide_cfg<8, 2, 256, 4, 12>(all_q);
+        if (var == 2) return wide_cfg<8, 2, 128, 3, 12>(all_q);
+        if (var == 3) return wide_cfg<8, 2, 64, 3, 12>(all_q);
         return wide_cfg<8, 2, 128, 4, 12>(all_q);
     }
     return wide_cfg<8, 2, 128, 4>(all_q);
@@ -593,6 +596,8 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     P.l2mode = 0;
     if (const char* m = std::getenv("PRGPU_L2MODE")) P.l2mode = (uint32_t)std::atoi(m);
     P.hot_src = 0;
+    if (const char* h = std::getenv("PRGPU_HOT_MB")) // tuning: L2-resident source rows
+        P.hot_src = (uint32_t)std::min<uint64_t>(nsrc, ((uint64_t)std::atoi(h) << 20) / (KS * sizeof(double)));
     P.cbase = cbase;
     P.cold_off[0] = 0;
     P.cold_off[1] = nsrc;
@@ -879,10 +884,12 @@ double session_time_pull(prgpu_session* s, int launches) {
         if (!read_any_active(s)) { ++done; break; }
     }
     double total = 0;
+    const bool log = std::getenv("PRGPU_TIMING_LOG") != nullptr; // per-launch times (tuning)
     for (int i = 0; i < done; ++i) {
         float ms = 0;
         PRGPU_CUDA(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]));
         total += ms;
+        if (log) std::fprintf(stderr, "launch %d: %.4f ms\n", i + 1, ms);
     }
     for (auto& e : ev) cudaEventDestroy(e);
     return done ? total / done : 0.0;

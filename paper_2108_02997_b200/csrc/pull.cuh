@@ -54,6 +54,11 @@ namespace prgpu {
 
 constexpr int kNT = 256; // threads per CTA
 constexpr int kWarps = kNT / 32;
+#ifdef PRGPU_NO_BCAST
+constexpr bool kBcast = false; // tuning builds only
+#else
+constexpr bool kBcast = true;
+#endif
 constexpr int kNQ = 5; // partials: L1, L2^2, Linf, dangling sum, L1-vs-ref
 
 struct LaneState {
@@ -159,6 +164,12 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint32_t* p, uint64_t pol) {
 __device__ __forceinline__ uint64_t ld_stream_u64(const uint64_t* p, uint64_t pol) {
     uint64_t r;
     asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t pol) {
+    uint32_t r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
     return r;
 }
 
@@ -271,7 +282,7 @@ struct PullCfg {
     static constexpr int ER = 8 * ES;    // rows per empty task
     // K = 1 stages every gathered value of a run in shared memory; wider lanes
     // accumulate in registers (staging would double the bytes moved per edge)
-    static constexpr bool STAGED = (KP == 1); // measured: staging wide lanes lost
+    static constexpr bool STAGED = (KP == 1); // measured: staging wide lanes' values lost
     static constexpr int SMEM_WARP = STAGED ? EMAX * KS : 0; // doubles per warp
 };
 
@@ -314,13 +325,31 @@ struct Warp {
         return live;
     }
 
+    // l2mode >= 3 (tuning): hot sources' rows (src < hot_src, next iteration's
+    // most-gathered) written evict_last (3) / evict_normal (4), the rest
+    // evict_first; 5: every row evict_first
     __device__ __forceinline__ void write_contrib(uint32_t src, int sl, const double (&cv)[W]) {
-        store_w<W>(caddr<KS>(P, par ^ 1, src) + sl * W, cv);
+        double* dst = caddr<KS>(P, par ^ 1, src) + sl * W;
+        if (P.l2mode >= 3) {
+            const uint64_t pol = (P.l2mode == 5 || src >= P.hot_src) ? policy_evict_first()
+                                 : P.l2mode == 3                   ? policy_evict_last()
+                                                                   : policy_evict_normal();
+            store_w_pol<W>(dst, cv, pol);
+        } else {
+            store_w<W>(dst, cv);
+        }
     }
 
     // fused epilogue for row v, lanes [sl*W, sl*W + W)
     __device__ __forceinline__ void epilogue(uint32_t v, int sl, const double (&acc)[W]) {
         const uint2 ri = ld_stream_u2(P.rowinfo + v, stream_policy(P));
+        epilogue_with<true>(v, sl, acc, ri, acc);
+    }
+
+    // the epilogue with the row's info and previous ranks already at hand
+    template <bool LOAD_PREV = false>
+    __device__ __forceinline__ void epilogue_with(uint32_t v, int sl, const double (&acc)[W], uint2 ri,
+                                                  const double (&o)[W]) {
         const uint32_t d = ri.x;
         const size_t n = P.n;
         double cv[W];
@@ -333,8 +362,7 @@ struct Warp {
                 any = true;
                 // next[v] = teleport + alpha*acc, two roundings (pagerank.hpp:92)
                 const double r = __dadd_rn(s_c0[k], __dmul_rn(s_alpha[k], acc[w]));
-                const double o = __ldcs(rp + (size_t)k * n + v);
-                const double df = __dsub_rn(r, o);
+                const double df = __dsub_rn(r, LOAD_PREV ? __ldcs(rp + (size_t)k * n + v) : o[w]);
                 const double ad = fabs(df);
                 part.add(0, w, ad);
                 part.add(1, w, df * df);
@@ -393,6 +421,46 @@ struct Warp {
         }
     }
 
+    // Wide lanes (LG > 1): every lane loads distinct colidx (128 edges per
+    // block, coalesced) and each edge's source id is broadcast to its lane
+    // group with one shuffle, so the index work is not repeated LG times.
+    // Slot s sums edges s, s+ES, s+2ES, ... of the block, in order.
+    __device__ __forceinline__ void accumulate_bcast(uint64_t lo, uint64_t hi, double (&acc)[W]) const {
+        const uint64_t sp = stream_policy(P);
+        const uint32_t ne = (uint32_t)(hi - lo);
+        const uint32_t* __restrict__ cb = P.col + lo;
+        const bool ok = slice_live();
+        constexpr int STEPS = 32 / ES; // steps per 32-edge group
+        constexpr int SB = STEPS < 4 ? STEPS : 4; // gathers in flight per sub-batch (registers)
+        for (uint32_t base = 0; base < ne; base += 128) {
+            uint32_t c[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t e = base + lane + 32u * j;
+                c[j] = e < ne ? ld_stream_u32(cb + e, sp) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+#pragma unroll
+                for (int i0 = 0; i0 < STEPS; i0 += SB) {
+                    double v[SB][W];
+#pragma unroll
+                    for (int i = 0; i < SB; ++i) {
+                        const uint32_t src = __shfl_sync(0xffffffffu, c[j], (i0 + i) * ES + slot);
+                        const uint32_t e = base + 32u * j + (i0 + i) * ES + slot;
+#pragma unroll
+                        for (int w = 0; w < W; ++w) v[i][w] = 0.0;
+                        if (ok && e < ne) load_w<W>(cpl + (size_t)src * KS, v[i]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < SB; ++i)
+#pragma unroll
+                        for (int w = 0; w < W; ++w) acc[w] += v[i][w];
+                }
+            }
+        }
+    }
+
     __device__ __forceinline__ void reduce_slots(double (&acc)[W]) const {
 #pragma unroll
         for (int off = LG; off < 32; off <<= 1)
@@ -412,7 +480,8 @@ struct Warp {
         double acc[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) acc[w] = 0.0;
-        accumulate(lo, hi, acc);
+        if constexpr (LG > 1 && kBcast) accumulate_bcast(lo, hi, acc);
+        else accumulate(lo, hi, acc);
         reduce_slots(acc);
         if (nch == 1) { // the whole row was this chunk: no hand-off needed
             if (lane < LG) epilogue(row, slice, acc);
@@ -717,11 +786,23 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     __threadfence();
 
     __shared__ double s_tot[kNQ * KP];
+    for (int t = tid; t < kNQ * KP; t += kNT) s_tot[t] = 0.0;
+    __syncthreads();
+    // only the quantities this instance tracks, only real lanes; each warp
+    // streams one quantity's CTA column with 4 loads in flight per lane
     for (int t = warp; t < kNQ * KP; t += kWarps) {
         const int q = t / KP;
+        if (!((QM >> q) & 1) || (t % KP) >= (int)P.K) continue;
         double v = 0.0;
-        for (uint32_t b = lane; b < P.G; b += 32) {
-            const double x = __ldcg(P.partials + (size_t)t * P.G + b);
+        const double* col = P.partials + (size_t)t * P.G;
+        uint32_t b = lane;
+        for (; b + 96 < P.G; b += 128) {
+            const double x0 = __ldcg(col + b), x1 = __ldcg(col + b + 32), x2 = __ldcg(col + b + 64),
+                         x3 = __ldcg(col + b + 96);
+            v = (q == 2) ? fmax(fmax(fmax(fmax(v, x0), x1), x2), x3) : (((v + x0) + x1) + x2) + x3;
+        }
+        for (; b < P.G; b += 32) {
+            const double x = __ldcg(col + b);
             v = (q == 2) ? fmax(v, x) : v + x;
         }
 #pragma unroll

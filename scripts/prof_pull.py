@@ -20,6 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2", choices=sorted(bench.CONFIGS))
     ap.add_argument("--launches", type=int, default=8)
+    ap.add_argument("--all", action="store_true", help="run to convergence")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     if cfg["kind"] == "rmat":
@@ -28,7 +29,7 @@ def main():
         g = prl.generate_grid(cfg["side"], 0.6, 0.01, bench.SEED)
     s = prl.Session(g, cfg["alphas"], cfg["tol"], prl.NormKind(cfg["norm"]), 500,
                     cfg.get("stop_mask", 0))
-    ms = s.time_pull(args.launches)
+    ms = s.time_pull(500 if args.all else args.launches)
     info = g.info
     print(f"{args.config}: N={g.vertex_count} E={g.edge_count()} hub={info.hub_rows} "
           f"warp={info.warp_rows} thread={info.thread_rows} empty={info.empty_rows} "
