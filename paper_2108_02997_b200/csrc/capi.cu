@@ -3,12 +3,26 @@
 // leaves a thread-local message for prgpu_last_error().
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 
 #include "common.cuh"
 
 namespace prgpu {
 std::atomic<uint64_t> g_launches{0};
+
+void pool_init() {
+    static std::once_flag once[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::call_once(once[dev & 63], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = kPoolKeepBytes;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+}
 
 std::unique_ptr<prgpu_graph> graph_build_device(uint32_t, const uint32_t*, uint64_t, int, cudaStream_t);
 std::unique_ptr<prgpu_graph> graph_build_host(uint32_t, const uint32_t*, uint64_t, int, cudaStream_t);
@@ -79,6 +93,7 @@ int make_graph(int device, prgpu_graph** out, Make&& make) {
         check_device(device);
         prgpu::DeviceGuard dg(device);
         prgpu::Stream st;
+        prgpu::AllocScope scope(st);
         std::unique_ptr<prgpu_graph> g = make((cudaStream_t)st);
         PRGPU_CUDA(cudaStreamSynchronize(st));
         *out = g.release();
@@ -146,6 +161,7 @@ int prgpu_graph_download(const prgpu_graph* g, uint64_t* off, uint32_t* nbr, uin
         if (!g) prgpu::fail(PRGPU_EINVAL, "null graph");
         prgpu::DeviceGuard dg(g->device);
         prgpu::Stream st;
+        prgpu::AllocScope scope(st);
         prgpu::graph_download(g, off, nbr, deg, dang, st);
     });
 }
@@ -155,7 +171,18 @@ void prgpu_graph_free(prgpu_graph* g) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(g->device);
-    delete g;
+    {
+        // no call may still use the graph: its buffers go back to the pool
+        // ordered after everything already queued on the device
+        cudaDeviceSynchronize();
+        cudaStream_t st = nullptr;
+        cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        {
+            prgpu::AllocScope scope(st);
+            delete g;
+        }
+        cudaStreamDestroy(st);
+    }
     cudaSetDevice(prev);
 }
 

@@ -4,9 +4,13 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "../../include/prgpu.h"
 
@@ -36,30 +40,88 @@ inline void check_cuda(cudaError_t e, const char* what, const char* file, int li
 
 extern std::atomic<uint64_t> g_launches;
 
+// Host-side phase timing for tuning (PRGPU_TIMING_LOG=1): syncs the stream at
+// each mark and prints the time since the previous one.  Off by default.
+struct PhaseLog {
+    bool on;
+    cudaStream_t st;
+    std::chrono::steady_clock::time_point t;
+    const char* scope;
+    PhaseLog(const char* sc, cudaStream_t s)
+        : on(std::getenv("PRGPU_TIMING_LOG") != nullptr), st(s), t(std::chrono::steady_clock::now()),
+          scope(sc) {}
+    void mark(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[%s] %-22s %8.3f ms\n", scope, what,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
+// Stream-ordered allocation.  Inside an AllocScope, DevBufs come from the
+// device's default memory pool (cudaMallocAsync on the scope's stream) and are
+// returned to it stream-ordered, so the many temporaries of a graph build and
+// a session cost no cudaMalloc/cudaFree round trips; the pool keeps up to
+// kPoolKeepBytes cached across calls.  Outside a scope: plain cudaMalloc/Free.
+inline thread_local cudaStream_t t_alloc_stream = nullptr;
+constexpr uint64_t kPoolKeepBytes = 8ull << 30;
+void pool_init(); // current device, once
+
+struct AllocScope {
+    cudaStream_t prev;
+    explicit AllocScope(cudaStream_t s) : prev(t_alloc_stream) {
+        pool_init();
+        t_alloc_stream = s;
+    }
+    ~AllocScope() { t_alloc_stream = prev; }
+    AllocScope(const AllocScope&) = delete;
+    AllocScope& operator=(const AllocScope&) = delete;
+};
+
 // RAII device buffer.
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    bool pooled = false;
     DevBuf() = default;
     explicit DevBuf(size_t count) { alloc(count); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), pooled(o.pooled) { o.p = nullptr; o.n = 0; }
     DevBuf& operator=(DevBuf&& o) noexcept {
-        if (this != &o) { reset(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        if (this != &o) {
+            reset();
+            p = o.p; n = o.n; pooled = o.pooled;
+            o.p = nullptr; o.n = 0;
+        }
         return *this;
     }
     ~DevBuf() { reset(); }
     void alloc(size_t count) {
         reset();
         n = count;
-        if (count) PRGPU_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        if (!count) return;
+        if (t_alloc_stream) {
+            PRGPU_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), t_alloc_stream));
+            pooled = true;
+        } else {
+            PRGPU_CUDA(cudaMalloc(&p, count * sizeof(T)));
+            pooled = false;
+        }
     }
     void reset() {
-        if (p) cudaFree(p);
+        if (p) {
+            if (pooled && t_alloc_stream) cudaFreeAsync(p, t_alloc_stream);
+            else cudaFree(p); // also valid for pool memory (synchronous)
+        }
         p = nullptr;
         n = 0;
+    }
+    void swap(DevBuf& o) noexcept {
+        std::swap(p, o.p); std::swap(n, o.n); std::swap(pooled, o.pooled);
     }
     T* release() { T* q = p; p = nullptr; n = 0; return q; }
 };
@@ -80,6 +142,15 @@ struct Stream {
     Stream(const Stream&) = delete;
     Stream& operator=(const Stream&) = delete;
     operator cudaStream_t() const { return s; }
+};
+
+struct Event {
+    cudaEvent_t e = nullptr;
+    Event() { PRGPU_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+    ~Event() { if (e) cudaEventDestroy(e); }
+    Event(const Event&) = delete;
+    Event& operator=(const Event&) = delete;
+    operator cudaEvent_t() const { return e; }
 };
 
 // Pull-kernel degree bins (rows sorted by in-degree descending).

@@ -518,6 +518,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     if (!g || g->n == 0) fail(PRGPU_EINVAL, "pagerank: graph has no vertices");
     DeviceGuard dg(g->device);
     auto s = std::make_unique<prgpu_session>();
+    AllocScope scope(s->stream);
     s->g = g;
     s->K = p->lanes;
     {
@@ -530,6 +531,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     const size_t n = g->n, nsrc = std::max<size_t>(g->nsrc, 1);
     const int K = s->K, KP = s->KP;
     cudaStream_t st = s->stream;
+    PhaseLog ph("session", st);
 
     s->rank.alloc(2 * (size_t)K * n);
     const int KS = s->cfg.KS;
@@ -544,6 +546,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     s->lanes.alloc(K);
     s->gs.alloc(1);
 
+    ph.mark("alloc");
     // device slots hold lanes by alpha descending (slowest-converging first),
     // so the lanes still live late in a sweep share the leading sectors of each
     // contribution row; results are mapped back to the caller's order
@@ -622,6 +625,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         build_graph = false;
     }
 
+    ph.mark("init + tasks");
     // persistent grid: resident CTAs, but at least ~4 tasks per warp
     const size_t smem = s->cfg.smem();
     PRGPU_CUDA(cudaFuncSetAttribute((const void*)s->cfg.fn,
@@ -672,6 +676,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         s->use_graph = true;
     }
     PRGPU_CUDA(cudaStreamSynchronize(st));
+    ph.mark("graph");
     return s.release();
 }
 
@@ -702,7 +707,14 @@ void session_destroy(prgpu_session* s) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(s->g->device);
-    delete s;
+    // buffers return to the pool on the session's own stream (destroyed after
+    // them) once all queued work — ours and a partition caller's — is done
+    cudaStreamSynchronize(s->cur());
+    cudaStreamSynchronize(s->stream);
+    {
+        AllocScope scope(s->stream);
+        delete s;
+    }
     cudaSetDevice(prev);
 }
 
@@ -798,6 +810,8 @@ double session_run(prgpu_session* s) {
 void session_results(prgpu_session* s, prgpu_result* out) {
     DeviceGuard dg(s->g->device);
     cudaStream_t st = s->stream;
+    AllocScope scope(st);
+    PhaseLog ph("results", st);
     std::vector<LaneState> L(s->K);
     PRGPU_CUDA(cudaMemcpyAsync(L.data(), s->lanes.p, s->K * sizeof(LaneState),
                                cudaMemcpyDeviceToHost, st));
@@ -814,6 +828,7 @@ void session_results(prgpu_session* s, prgpu_result* out) {
             PRGPU_CUDA(cudaMemcpyAsync(out->ranks + (size_t)s->user_of[k] * n, tmp.p + (size_t)k * n,
                                        n * 8, cudaMemcpyDeviceToHost, st));
         PRGPU_CUDA(cudaStreamSynchronize(st));
+        ph.mark("ranks d2h");
     }
     if (out->err_trace) {
         std::vector<double> tr((size_t)s->max_iter * K * 4);

@@ -207,6 +207,22 @@ __global__ void keys_low(const uint64_t* __restrict__ keys, uint64_t u, uint32_t
         col[i] = (uint32_t)(keys[i] & mask);
 }
 
+template <typename T>
+__device__ __forceinline__ void block_add(T v, unsigned long long* dst) {
+    __shared__ unsigned long long s_sum[kThreads / 32];
+    unsigned long long x = (unsigned long long)v;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+    if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < kThreads / 32; ++w) t += s_sum[w];
+        if (t) atomicAdd(dst, t);
+    }
+    __syncthreads();
+}
+
 // bins over rows sorted by in-degree descending: counts of rows above thresholds
 __global__ void bin_counts(const uint64_t* __restrict__ row_off, uint32_t n,
                            unsigned long long* __restrict__ counts /*4*/) {
@@ -218,9 +234,9 @@ __global__ void bin_counts(const uint64_t* __restrict__ row_off, uint32_t n,
         c1 += d > kWarpMinDegree;
         c2 += d > 0;
     }
-    atomicAdd(&counts[0], c0);
-    atomicAdd(&counts[1], c1);
-    atomicAdd(&counts[2], c2);
+    block_add(c0, &counts[0]);
+    block_add(c1, &counts[1]);
+    block_add(c2, &counts[2]);
 }
 
 __global__ void count_zero(const uint32_t* __restrict__ v, uint32_t n,
@@ -229,22 +245,87 @@ __global__ void count_zero(const uint32_t* __restrict__ v, uint32_t n,
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
         c += v[i] == 0;
-    atomicAdd(count, c);
+    block_add(c, count);
 }
 
-// CSR (reference layout) -> keys, with validation
-__global__ void csr_to_keys(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr,
-                            uint32_t n, uint32_t lg, uint64_t* __restrict__ keys, int* bad) {
+// ---- edge-parallel CSR passes ------------------------------------------------------
+// Block b covers edges [b*kEdgeChunk, (b+1)*kEdgeChunk); the row of an edge is
+// the last row o with off[o] <= j, found by binary search inside the rows the
+// chunk spans (so hub rows are split across blocks: no per-row stragglers).
+constexpr uint32_t kEdgeChunk = 4096;
+
+__device__ __forceinline__ uint32_t last_row_le(const uint64_t* __restrict__ off, uint32_t lo, uint32_t hi,
+                                                uint64_t j) {
+    while (lo < hi) { // largest o in [lo, hi] with off[o] <= j
+        const uint32_t mid = lo + (hi - lo + 1) / 2;
+        if (off[mid] <= j) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ void chunk_rows(const uint64_t* __restrict__ off, uint32_t n, uint64_t j0,
+                                           uint64_t j1, uint32_t& r0, uint32_t& r1) {
+    __shared__ uint32_t s_r[2];
+    if (threadIdx.x == 0) {
+        s_r[0] = last_row_le(off, 0, n - 1, j0);
+        s_r[1] = last_row_le(off, 0, n - 1, j1 - 1);
+    }
+    __syncthreads();
+    r0 = s_r[0];
+    r1 = s_r[1];
+}
+
+// offsets monotone (off[0] == 0 is checked on the host)
+__global__ void check_offsets(const uint64_t* __restrict__ off, uint32_t n, uint64_t e, int* bad) {
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
-         v += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t lo = off[v], hi = off[v + 1];
-        if (hi < lo) { *bad = 1; continue; }
-        for (uint64_t j = lo; j < hi; ++j) {
-            const uint32_t u = nbr[j];
-            if (u >= n || (j > lo && nbr[j - 1] >= u)) *bad = 1; // ascending, unique
-            keys[j] = ((uint64_t)v << lg) | u;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        if (off[v + 1] < off[v] || off[v + 1] > e) *bad = 1;
+}
+
+// in-neighbours in range, strictly ascending per row; out-degree histogram
+__global__ void check_edges(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr, uint32_t n,
+                            uint64_t e, uint32_t* __restrict__ out_cnt, int* bad) {
+    const uint64_t j0 = (uint64_t)blockIdx.x * kEdgeChunk, j1 = min(j0 + kEdgeChunk, e);
+    uint32_t r0, r1;
+    chunk_rows(off, n, j0, j1, r0, r1);
+    for (uint64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+        const uint32_t u = nbr[j];
+        if (u >= n) { *bad = 1; continue; }
+        atomicAdd(out_cnt + u, 1u);
+        if (j > 0) {
+            const uint32_t o = last_row_le(off, r0, r1, j);
+            if (j > off[o] && nbr[j - 1] >= u) *bad = 1;
         }
     }
+}
+
+// engine CSR fill: edge j of original row o lands at row_off[new(o)] + (j - off[o])
+// as the engine source id of its in-neighbour; rows keep the caller's
+// (ascending original id) neighbour order — the reference's summation order
+__global__ void scatter_edges(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr, uint32_t n,
+                              uint64_t e, const uint32_t* __restrict__ new_of_old,
+                              const uint64_t* __restrict__ row_off, const uint32_t* __restrict__ src_of_old,
+                              uint32_t* __restrict__ col) {
+    const uint64_t j0 = (uint64_t)blockIdx.x * kEdgeChunk, j1 = min(j0 + kEdgeChunk, e);
+    uint32_t r0, r1;
+    chunk_rows(off, n, j0, j1, r0, r1);
+    for (uint64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+        const uint32_t o = last_row_le(off, r0, r1, j);
+        col[row_off[new_of_old[o]] + (j - off[o])] = src_of_old[nbr[j]];
+    }
+}
+
+__global__ void in_deg_from_off(const uint64_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ d) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        d[v] = (uint32_t)(off[v + 1] - off[v]);
+}
+
+__global__ void src_of_old_kernel(const uint2* __restrict__ rowinfo, const uint32_t* __restrict__ new_of_old,
+                                  uint32_t n, uint32_t* __restrict__ out) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        out[v] = rowinfo[new_of_old[v]].y;
 }
 
 __global__ void compare_u32(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
@@ -352,32 +433,24 @@ int read_flag(const DevBuf<int>& f, cudaStream_t st) {
     return v;
 }
 
-// Sorted unique original-id keys -> engine graph.  Consumes `keys`.
-std::unique_ptr<prgpu_graph> assemble(DevBuf<uint64_t>&& keys_in, uint64_t u, uint32_t n,
-                                      uint32_t lg, int device, cudaStream_t st,
-                                      const uint32_t* expect_out_deg /* device, optional */) {
-    DevBuf<uint64_t> keys(std::move(keys_in));
+// Original-label CSR on the device (off[n+1], nbr[e] ascending per row,
+// out-degrees) -> engine graph, in two halves: the vertex side (relabelling,
+// row offsets, source ids) needs only off and the degrees, so graph_from_csr
+// runs it while the neighbour array is still in flight from the host.
+// The inputs are not modified.
+std::unique_ptr<prgpu_graph> assemble_vertices(uint32_t n, const uint64_t* off, uint64_t e,
+                                               const uint32_t* out_deg, uint32_t lg, int device,
+                                               cudaStream_t st) {
+    PhaseLog ph("assemble", st);
     auto g = std::make_unique<prgpu_graph>();
     g->device = device;
     g->n = n;
-    g->e = u;
+    g->e = e;
     g->lg = lg;
 
-    DevBuf<uint32_t> in_deg(n), out_deg(n);
-    PRGPU_CUDA(cudaMemsetAsync(in_deg.p, 0, n * sizeof(uint32_t), st));
-    PRGPU_CUDA(cudaMemsetAsync(out_deg.p, 0, n * sizeof(uint32_t), st));
-    if (u) {
-        count_degrees<<<grid_for(u), kThreads, 0, st>>>(keys.p, u, lg, in_deg.p, out_deg.p);
-        PRGPU_LAUNCHED("count_degrees");
-    }
-    if (expect_out_deg) {
-        DevBuf<int> bad(1);
-        PRGPU_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
-        compare_u32<<<grid_for(n), kThreads, 0, st>>>(out_deg.p, expect_out_deg, n, bad.p);
-        PRGPU_LAUNCHED("compare_u32");
-        if (read_flag(bad, st))
-            fail(PRGPU_EINVAL, "graph_from_csr: out_degree does not match in_neighbors");
-    }
+    DevBuf<uint32_t> in_deg(n);
+    in_deg_from_off<<<grid_for(n), kThreads, 0, st>>>(off, n, in_deg.p);
+    PRGPU_LAUNCHED("in_deg_from_off");
 
     // relabel: stable sort of vertices by (in-degree desc, out-degree desc, id):
     // degree bins become contiguous row ranges, and within each in-degree class
@@ -386,7 +459,7 @@ std::unique_ptr<prgpu_graph> assemble(DevBuf<uint64_t>&& keys_in, uint64_t u, ui
         DevBuf<uint64_t> kin(n), kout(n);
         DevBuf<uint32_t> vin(n);
         g->old_of_new.alloc(n);
-        degree_keys<<<grid_for(n), kThreads, 0, st>>>(in_deg.p, out_deg.p, kin.p, n);
+        degree_keys<<<grid_for(n), kThreads, 0, st>>>(in_deg.p, out_deg, kin.p, n);
         PRGPU_LAUNCHED("degree_keys");
         iota_u32<<<grid_for(n), kThreads, 0, st>>>(vin.p, n);
         PRGPU_LAUNCHED("iota_u32");
@@ -401,28 +474,15 @@ std::unique_ptr<prgpu_graph> assemble(DevBuf<uint64_t>&& keys_in, uint64_t u, ui
         invert_perm<<<grid_for(n), kThreads, 0, st>>>(g->old_of_new.p, g->new_of_old.p, n);
         PRGPU_LAUNCHED("invert_perm");
     }
+    ph.mark("relabel sort");
 
-    // engine edges: relabel both endpoints, sort (rows ascending, sources ascending)
-    if (u) {
-        relabel_keys<<<grid_for(u), kThreads, 0, st>>>(keys.p, u, lg, g->new_of_old.p);
-        PRGPU_LAUNCHED("relabel_keys");
-        DevBuf<uint64_t> alt(u);
-        sort_keys(keys, alt, u, 2 * (int)lg, st);
-    }
     g->row_off.alloc((size_t)n + 1);
     gather_deg_u64<<<grid_for((uint64_t)n + 1), kThreads, 0, st>>>(in_deg.p, g->old_of_new.p,
                                                                     g->row_off.p, n);
     PRGPU_LAUNCHED("gather_deg_u64");
     exclusive_scan_u64(g->row_off.p, (uint64_t)n + 1, st);
-    g->col.alloc(u + 16);
-    PRGPU_CUDA(cudaMemsetAsync(g->col.p, 0, (u + 16) * sizeof(uint32_t), st));
-    if (u) {
-        keys_low<<<grid_for(u), kThreads, 0, st>>>(keys.p, u, lg, g->col.p);
-        PRGPU_LAUNCHED("keys_low");
-    }
-    keys.reset();
     g->deg.alloc(n);
-    gather_u32<<<grid_for(n), kThreads, 0, st>>>(out_deg.p, g->old_of_new.p, g->deg.p, n);
+    gather_u32<<<grid_for(n), kThreads, 0, st>>>(out_deg, g->old_of_new.p, g->deg.p, n);
     PRGPU_LAUNCHED("gather_u32");
 
     // compact source ids: contributions are stored for out-degree > 0 only
@@ -440,17 +500,50 @@ std::unique_ptr<prgpu_graph> assemble(DevBuf<uint64_t>&& keys_in, uint64_t u, ui
         src_maps<<<grid_for(n), kThreads, 0, st>>>(g->deg.p, flags.p, n, g->rowinfo.p,
                                                    g->row_of_src.p);
         PRGPU_LAUNCHED("src_maps");
-        if (u) {
-            col_to_src<<<grid_for(u), kThreads, 0, st>>>(g->col.p, u, g->rowinfo.p);
-            PRGPU_LAUNCHED("col_to_src");
+    }
+    ph.mark("row_off + source ids");
+    return g;
+}
+
+// Second half: the engine edge array and the degree-bin counts.
+void assemble_edges(prgpu_graph* g, const uint64_t* off, const uint32_t* nbr, const uint32_t* out_deg,
+                    cudaStream_t st) {
+    PhaseLog ph("assemble", st);
+    const uint32_t n = g->n;
+    const uint64_t e = g->e;
+    // engine edges (+16 zero pad for the kernels' 128-bit colidx loads)
+    g->col.alloc(e + 16);
+    PRGPU_CUDA(cudaMemsetAsync(g->col.p + e, 0, 16 * sizeof(uint32_t), st));
+    if (e) {
+        DevBuf<uint32_t> src_of_old(n);
+        src_of_old_kernel<<<grid_for(n), kThreads, 0, st>>>(g->rowinfo.p, g->new_of_old.p, n, src_of_old.p);
+        PRGPU_LAUNCHED("src_of_old");
+        const uint64_t blocks = (e + kEdgeChunk - 1) / kEdgeChunk;
+        scatter_edges<<<(unsigned)blocks, kThreads, 0, st>>>(off, nbr, n, e, g->new_of_old.p, g->row_off.p,
+                                                             src_of_old.p, g->col.p);
+        PRGPU_LAUNCHED("scatter_edges");
+        // PRGPU_ROW_SORT=1 (tuning): sources ascending within each row instead
+        const char* rs = std::getenv("PRGPU_ROW_SORT");
+        if (rs && std::atoi(rs) && e < (1ull << 31)) {
+            DevBuf<uint32_t> sorted(e + 16);
+            size_t tmp = 0;
+            PRGPU_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, g->col.p, sorted.p, (int64_t)e, (int64_t)n,
+                                                          g->row_off.p, g->row_off.p + 1, st));
+            DevBuf<char> t(tmp);
+            PRGPU_CUDA(cub::DeviceSegmentedSort::SortKeys(t.p, tmp, g->col.p, sorted.p, (int64_t)e, (int64_t)n,
+                                                          g->row_off.p, g->row_off.p + 1, st));
+            g_launches.fetch_add(1);
+            PRGPU_CUDA(cudaMemsetAsync(sorted.p + e, 0, 16 * sizeof(uint32_t), st));
+            std::swap(g->col, sorted);
         }
     }
+    ph.mark("edges");
 
     DevBuf<unsigned long long> counts(4);
     PRGPU_CUDA(cudaMemsetAsync(counts.p, 0, 4 * sizeof(unsigned long long), st));
     bin_counts<<<grid_for(n), kThreads, 0, st>>>(g->row_off.p, n, counts.p);
     PRGPU_LAUNCHED("bin_counts");
-    count_zero<<<grid_for(n), kThreads, 0, st>>>(out_deg.p, n, counts.p + 3);
+    count_zero<<<grid_for(n), kThreads, 0, st>>>(out_deg, n, counts.p + 3);
     PRGPU_LAUNCHED("count_zero");
     unsigned long long c[4];
     uint64_t first_two[2];
@@ -463,6 +556,34 @@ std::unique_ptr<prgpu_graph> assemble(DevBuf<uint64_t>&& keys_in, uint64_t u, ui
     g->nonempty_end = (uint32_t)c[2];
     g->ndangling = (uint32_t)c[3];
     g->max_in_degree = (uint32_t)(first_two[1] - first_two[0]);
+    ph.mark("bins");
+}
+
+// Sorted unique original-id keys (target << lg | source) -> engine graph.
+// Consumes `keys`.
+std::unique_ptr<prgpu_graph> assemble(DevBuf<uint64_t>&& keys_in, uint64_t u, uint32_t n,
+                                      uint32_t lg, int device, cudaStream_t st) {
+    DevBuf<uint64_t> keys(std::move(keys_in));
+    DevBuf<uint32_t> in_deg(n), out_deg(n);
+    PRGPU_CUDA(cudaMemsetAsync(in_deg.p, 0, n * sizeof(uint32_t), st));
+    PRGPU_CUDA(cudaMemsetAsync(out_deg.p, 0, n * sizeof(uint32_t), st));
+    if (u) {
+        count_degrees<<<grid_for(u), kThreads, 0, st>>>(keys.p, u, lg, in_deg.p, out_deg.p);
+        PRGPU_LAUNCHED("count_degrees");
+    }
+    DevBuf<uint64_t> off((size_t)n + 1);
+    gather_deg_u64<<<grid_for((uint64_t)n + 1), kThreads, 0, st>>>(in_deg.p, nullptr, off.p, n);
+    PRGPU_LAUNCHED("gather_deg_u64");
+    exclusive_scan_u64(off.p, (uint64_t)n + 1, st);
+    DevBuf<uint32_t> nbr(std::max<uint64_t>(u, 1));
+    if (u) {
+        keys_low<<<grid_for(u), kThreads, 0, st>>>(keys.p, u, lg, nbr.p);
+        PRGPU_LAUNCHED("keys_low");
+    }
+    keys.reset();
+    in_deg.reset();
+    auto g = assemble_vertices(n, off.p, u, out_deg.p, lg, device, st);
+    assemble_edges(g.get(), off.p, nbr.p, out_deg.p, st);
     return g;
 }
 
@@ -483,7 +604,7 @@ std::unique_ptr<prgpu_graph> graph_build_device(uint32_t n, const uint32_t* d_pa
         sort_keys(keys, alt, m, 2 * (int)lg, st);
         m = unique_keys(keys, alt, m, st);
     }
-    return assemble(std::move(keys), m, n, lg, device, st, nullptr);
+    return assemble(std::move(keys), m, n, lg, device, st);
 }
 
 std::unique_ptr<prgpu_graph> graph_build_host(uint32_t n, const uint32_t* pairs, uint64_t m,
@@ -501,21 +622,46 @@ std::unique_ptr<prgpu_graph> graph_from_csr(uint32_t n, const uint64_t* off, con
     if (off[0] != 0) fail(PRGPU_EINVAL, "graph_from_csr: in_offsets[0] != 0");
     const uint64_t e = off[n];
     const uint32_t lg = bits_for(n);
+    PhaseLog ph("from_csr", st);
     DevBuf<uint64_t> d_off((size_t)n + 1);
     DevBuf<uint32_t> d_nbr(std::max<uint64_t>(e, 1)), d_deg(n);
+    // the neighbour array (the bulk) travels on a side stream while the
+    // vertex half of the build runs on `st`
+    Stream side;
+    Event ready, landed;
+    PRGPU_CUDA(cudaEventRecord(ready, st)); // d_nbr's allocation is ordered on st
+    PRGPU_CUDA(cudaStreamWaitEvent(side, ready, 0));
+    if (e) PRGPU_CUDA(cudaMemcpyAsync(d_nbr.p, nbr, e * 4, cudaMemcpyHostToDevice, side));
+    PRGPU_CUDA(cudaEventRecord(landed, side));
     PRGPU_CUDA(cudaMemcpyAsync(d_off.p, off, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, st));
-    if (e) PRGPU_CUDA(cudaMemcpyAsync(d_nbr.p, nbr, e * 4, cudaMemcpyHostToDevice, st));
     PRGPU_CUDA(cudaMemcpyAsync(d_deg.p, out_degree, (size_t)n * 4, cudaMemcpyHostToDevice, st));
-    DevBuf<uint64_t> keys(std::max<uint64_t>(e, 1));
     DevBuf<int> bad(1);
     PRGPU_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
-    csr_to_keys<<<grid_for(n), kThreads, 0, st>>>(d_off.p, d_nbr.p, n, lg, keys.p, bad.p);
-    PRGPU_LAUNCHED("csr_to_keys");
-    if (read_flag(bad, st))
-        fail(PRGPU_EINVAL, "graph_from_csr: offsets not monotone or neighbours not ascending/unique/in range");
-    d_nbr.reset();
-    d_off.reset();
-    return assemble(std::move(keys), e, n, lg, device, st, d_deg.p);
+    check_offsets<<<grid_for(n), kThreads, 0, st>>>(d_off.p, n, e, bad.p);
+    PRGPU_LAUNCHED("check_offsets");
+    if (read_flag(bad, st)) {
+        cudaStreamSynchronize(side);
+        fail(PRGPU_EINVAL, "graph_from_csr: offsets not monotone");
+    }
+    ph.mark("offsets h2d + check");
+    auto g = assemble_vertices(n, d_off.p, e, d_deg.p, lg, device, st);
+    PRGPU_CUDA(cudaStreamWaitEvent(st, landed, 0));
+    ph.mark("neighbours landed");
+    DevBuf<uint32_t> cnt(n);
+    PRGPU_CUDA(cudaMemsetAsync(cnt.p, 0, (size_t)n * 4, st));
+    if (e) {
+        check_edges<<<(unsigned)((e + kEdgeChunk - 1) / kEdgeChunk), kThreads, 0, st>>>(d_off.p, d_nbr.p, n, e,
+                                                                                      cnt.p, bad.p);
+        PRGPU_LAUNCHED("check_edges");
+        if (read_flag(bad, st))
+            fail(PRGPU_EINVAL, "graph_from_csr: neighbours not ascending/unique/in range");
+    }
+    compare_u32<<<grid_for(n), kThreads, 0, st>>>(cnt.p, d_deg.p, n, bad.p);
+    PRGPU_LAUNCHED("compare_u32");
+    if (read_flag(bad, st)) fail(PRGPU_EINVAL, "graph_from_csr: out_degree does not match in_neighbors");
+    ph.mark("validate edges");
+    assemble_edges(g.get(), d_off.p, d_nbr.p, d_deg.p, st);
+    return g;
 }
 
 std::unique_ptr<prgpu_graph> graph_generate_rmat(uint32_t scale, uint32_t ef, double a, double b,
@@ -548,7 +694,7 @@ std::unique_ptr<prgpu_graph> graph_generate_rmat(uint32_t scale, uint32_t ef, do
         PRGPU_CUDA(cudaStreamSynchronize(st));
         if (last == kSentinel) --u; // self-loop slots
     }
-    return assemble(std::move(keys), u, n, scale, device, st, nullptr);
+    return assemble(std::move(keys), u, n, scale, device, st);
 }
 
 std::unique_ptr<prgpu_graph> graph_generate_grid(uint32_t side, double p, double lr, uint64_t seed,
@@ -573,7 +719,7 @@ std::unique_ptr<prgpu_graph> graph_generate_grid(uint32_t side, double p, double
     PRGPU_CUDA(cudaMemcpyAsync(&last, keys.p + (u - 1), 8, cudaMemcpyDeviceToHost, st));
     PRGPU_CUDA(cudaStreamSynchronize(st));
     if (last == kSentinel) --u;
-    return assemble(std::move(keys), u, (uint32_t)n, lg, device, st, nullptr);
+    return assemble(std::move(keys), u, (uint32_t)n, lg, device, st);
 }
 
 void graph_download(const prgpu_graph* g, uint64_t* h_off, uint32_t* h_nbr, uint32_t* h_deg,
