@@ -259,3 +259,21 @@ def test_c3_grid_tolerance_norm_sweep(prl, oracle):
         r = prl.pagerank(g, prl.PageRankConfig(0.85, 1e-10, nk(prl, norm)))
         assert r.iterations == gold["runs"][norm]["iterations"]
         assert np.max(np.abs(r.ranks[idx] - arr[f"{norm}_final_sample"])) <= RANK_TOL
+
+
+def test_c4_rmat26_linf(prl, oracle):
+    """configs[3]: RMAT-26 (67M vertices, 1.06B edges), alpha .85, tau 1e-10,
+    Linf — graph fingerprint bit-exact, iteration count, sampled/top/total ranks."""
+    gold = load_golden("c4_rmat26.json")
+    arr = np.load(os.path.join(GOLD, "c4_rmat26.npz"))
+    g = prl.generate_rmat(26, 16, 0.57, 0.19, 0.19, gold["seed"])
+    assert g.edge_count() == gold["graph"]["e"]
+    for k, v in graph_hashes(oracle, g).items():
+        assert v == gold["graph"][k], k
+    r = prl.pagerank(g, prl.PageRankConfig(0.85, 1e-10, prl.NormKind.LInf))
+    assert iterations_match(r.iterations, gold["iterations"], arr["trace"], 1e-10)
+    assert r.converged == gold["converged"]
+    idx = arr["sample_idx"]
+    assert np.max(np.abs(r.ranks[idx] - arr["sample"])) <= RANK_TOL
+    assert np.max(np.abs(r.ranks[arr["top_idx"]] - arr["top"])) <= RANK_TOL
+    assert abs(float(np.sum(r.ranks.astype(np.longdouble))) - float(arr["total"])) <= 1e-9
