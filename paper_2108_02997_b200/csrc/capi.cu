@@ -48,6 +48,7 @@ void session_destroy(prgpu_session*);
 using SessionPtr = std::unique_ptr<prgpu_session, void (*)(prgpu_session*)>;
 double session_run(prgpu_session*);
 void session_results(prgpu_session*, prgpu_result*);
+void session_solve(prgpu_session*, prgpu_result*);
 void session_observed(prgpu_session*, prgpu_result*, prgpu_observer_fn, void*);
 double session_time_pull(prgpu_session*, int);
 double error_norm_device(int, const double*, const double*, uint64_t, int);
@@ -191,8 +192,7 @@ int prgpu_pagerank(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
         if (!out) prgpu::fail(PRGPU_EINVAL, "null result");
         if (g) check_device(g->device);
         prgpu::SessionPtr s(prgpu::session_create(g, p, true, 0, 0, nullptr, nullptr), prgpu::session_destroy);
-        prgpu::session_run(s.get());
-        prgpu::session_results(s.get(), out);
+        prgpu::session_solve(s.get(), out);
     });
 }
 

@@ -13,6 +13,8 @@
 #include <cstdlib>
 #include <memory>
 #include <vector>
+#include <chrono>
+#include <thread>
 
 #include "common.cuh"
 #include "pull.cuh"
@@ -272,8 +274,14 @@ struct prgpu_session {
     DevBuf<double> rank_partials;
     cudaStream_t ext_stream = nullptr;
     cudaStream_t cur() const { return ext_stream ? ext_stream : (cudaStream_t)stream; }
+    // lanes that stopped, written by the device (host-mapped), for copying
+    // results out while the other lanes still iterate (session_solve)
+    int* host_frozen = nullptr;
+    int* dev_frozen = nullptr;
+    std::unique_ptr<Stream> aux;
 
     ~prgpu_session() {
+        if (host_frozen) cudaFreeHost(host_frozen);
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
         if (e0) cudaEventDestroy(e0);
@@ -591,6 +599,13 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     P.lanes = s->lanes.p;
     P.gs = s->gs.p;
     P.use_cond = 0;
+    P.frozen_at = nullptr;
+    if (nranks == 0) {
+        PRGPU_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->host_frozen), K * sizeof(int), cudaHostAllocMapped));
+        std::fill(s->host_frozen, s->host_frozen + K, 0);
+        PRGPU_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&s->dev_frozen), s->host_frozen, 0));
+        P.frozen_at = s->dev_frozen;
+    }
     P.skip_mask = 0;
     if (const char* sk = std::getenv("PRGPU_SKIP")) P.skip_mask = (uint32_t)std::atoi(sk);
     // streams (colidx, offsets, row info) are loaded evict_first (l2mode 0);
@@ -726,6 +741,7 @@ void session_init(prgpu_session* s) {
     PRGPU_CUDA(cudaMemcpyAsync(s->gs.p, &gsh, sizeof(gsh), cudaMemcpyHostToDevice, s->cur()));
     launch_init(s->cfg, s->P, s->g->ndangling, s->cur());
     s->host_iter = 0;
+    if (s->host_frozen) std::fill(s->host_frozen, s->host_frozen + s->K, 0); // no kernel in flight
 }
 
 void launch_pull(prgpu_session* s) {
@@ -848,6 +864,63 @@ void session_results(prgpu_session* s, prgpu_result* out) {
     }
     out->run_iterations = gsh.iter;
     out->loop_ms = s->last_loop_ms;
+}
+
+// run + results with the rank copy-out overlapped: while the CUDA graph
+// iterates, every lane the device reports stopped (frozen_at) is permuted to
+// caller ids on a side stream and copied to the host by the copy engine, so
+// only the lanes stopping at the last iteration are copied after the loop.
+void session_solve(prgpu_session* s, prgpu_result* out) {
+    if (!out->ranks || !s->use_graph || !s->host_frozen) {
+        session_run(s);
+        session_results(s, out);
+        return;
+    }
+    DeviceGuard dg(s->g->device);
+    AllocScope scope(s->stream);
+    const size_t n = s->g->n;
+    const int K = s->K;
+    if (!s->aux) s->aux = std::make_unique<Stream>();
+    cudaStream_t ax = *s->aux;
+    DevBuf<double> tmp((size_t)K * n);
+    Event tmp_ready;
+    PRGPU_CUDA(cudaEventRecord(tmp_ready, s->stream));
+    PRGPU_CUDA(cudaStreamWaitEvent(ax, tmp_ready, 0));
+    session_init(s);
+    PRGPU_CUDA(cudaEventRecord(s->e0, s->stream));
+    PRGPU_CUDA(cudaGraphLaunch(s->exec, s->stream));
+    g_launches.fetch_add(1);
+    PRGPU_CUDA(cudaEventRecord(s->e1, s->stream));
+    uint32_t copied = 0;
+    auto copy_out = [&](int k) {
+        extract_ranks<<<blocks_for(n), kNT, 0, ax>>>(s->P, s->g->new_of_old.p, tmp.p + (size_t)k * n, k, 0);
+        PRGPU_LAUNCHED("extract_ranks");
+        PRGPU_CUDA(cudaMemcpyAsync(out->ranks + (size_t)s->user_of[k] * n, tmp.p + (size_t)k * n, n * 8,
+                                   cudaMemcpyDeviceToHost, ax));
+        copied |= 1u << k;
+    };
+    for (;;) {
+        const cudaError_t q = cudaEventQuery(s->e1);
+        if (q != cudaSuccess && q != cudaErrorNotReady) PRGPU_CUDA(q);
+        for (int k = 0; k < K; ++k)
+            if (!((copied >> k) & 1u) && *(volatile int*)(s->host_frozen + k)) copy_out(k);
+        if (q == cudaSuccess) break;
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+    for (int k = 0; k < K; ++k) // lanes not reported (defensive): copy after the loop
+        if (!((copied >> k) & 1u)) copy_out(k);
+    float ms = 0;
+    PRGPU_CUDA(cudaEventElapsedTime(&ms, s->e0, s->e1));
+    s->last_loop_ms = ms;
+    PRGPU_CUDA(cudaStreamSynchronize(ax));
+    Event done;
+    PRGPU_CUDA(cudaEventRecord(done, ax));
+    PRGPU_CUDA(cudaStreamWaitEvent(s->stream, done, 0)); // tmp is freed on s->stream
+    prgpu_result rest = *out;
+    rest.ranks = nullptr;
+    session_results(s, &rest);
+    out->run_iterations = rest.run_iterations;
+    out->loop_ms = rest.loop_ms;
 }
 
 void session_observed(prgpu_session* s, prgpu_result* out, prgpu_observer_fn fn, void* user) {

@@ -119,6 +119,7 @@ struct Params {
     double* rank_partials;       // [nranks][kNQ*KP]
     int use_cond;
     cudaGraphConditionalHandle cond;
+    int* frozen_at; // host-mapped [K]: iteration at which each lane stopped (0: live), or null
 };
 
 // ---- L2 residency control -------------------------------------------------------
@@ -698,6 +699,10 @@ __device__ void finalize_lanes(const Params& P, const double* s_tot, const doubl
         // teleport = (1 - alpha)/n + alpha*dangling_sum/n   (pagerank.hpp:87)
         const double a = L.alpha, nd = (double)P.n;
         L.c0 = __dadd_rn(__ddiv_rn(__dsub_rn(1.0, a), nd), __ddiv_rn(__dmul_rn(a, dang), nd));
+        if (!L.active && P.frozen_at) { // the host may now copy this lane out
+            __threadfence_system();
+            *(volatile int*)(P.frozen_at + k) = done;
+        }
     }
     __syncthreads();
     if (tid == 0) {
