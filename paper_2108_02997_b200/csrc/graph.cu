@@ -290,36 +290,27 @@ __global__ void check_offsets(const uint64_t* __restrict__ off, uint32_t n, uint
         if (off[v + 1] < off[v] || off[v + 1] > e) *bad = 1;
 }
 
-// in-neighbours in range, strictly ascending per row; out-degree histogram
-__global__ void check_edges(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr, uint32_t n,
-                            uint64_t e, uint32_t* __restrict__ out_cnt, int* bad) {
-    const uint64_t j0 = (uint64_t)blockIdx.x * kEdgeChunk, j1 = min(j0 + kEdgeChunk, e);
+// Engine CSR fill for edges [jb, je) of the original CSR: edge j of original
+// row o lands at row_off[new(o)] + (j - off[o]) as the engine source id of
+// its in-neighbour (rows keep the caller's neighbour order until sorted).
+// With `bad`, also validates: in-neighbours in range and strictly ascending
+// per row, and counts out-degrees into out_cnt (graph_from_csr).
+__global__ void place_edges(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr, uint32_t n,
+                            uint64_t jb, uint64_t je, const uint32_t* __restrict__ new_of_old,
+                            const uint64_t* __restrict__ row_off, const uint32_t* __restrict__ src_of_old,
+                            uint32_t* __restrict__ col, uint32_t* __restrict__ out_cnt, int* bad) {
+    const uint64_t j0 = jb + (uint64_t)blockIdx.x * kEdgeChunk, j1 = min(j0 + kEdgeChunk, je);
     uint32_t r0, r1;
     chunk_rows(off, n, j0, j1, r0, r1);
     for (uint64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
         const uint32_t u = nbr[j];
-        if (u >= n) { *bad = 1; continue; }
-        atomicAdd(out_cnt + u, 1u);
-        if (j > 0) {
-            const uint32_t o = last_row_le(off, r0, r1, j);
+        const uint32_t o = last_row_le(off, r0, r1, j);
+        if (bad) {
+            if (u >= n) { *bad = 1; continue; }
+            atomicAdd(out_cnt + u, 1u);
             if (j > off[o] && nbr[j - 1] >= u) *bad = 1;
         }
-    }
-}
-
-// engine CSR fill: edge j of original row o lands at row_off[new(o)] + (j - off[o])
-// as the engine source id of its in-neighbour; rows keep the caller's
-// (ascending original id) neighbour order — the reference's summation order
-__global__ void scatter_edges(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr, uint32_t n,
-                              uint64_t e, const uint32_t* __restrict__ new_of_old,
-                              const uint64_t* __restrict__ row_off, const uint32_t* __restrict__ src_of_old,
-                              uint32_t* __restrict__ col) {
-    const uint64_t j0 = (uint64_t)blockIdx.x * kEdgeChunk, j1 = min(j0 + kEdgeChunk, e);
-    uint32_t r0, r1;
-    chunk_rows(off, n, j0, j1, r0, r1);
-    for (uint64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-        const uint32_t o = last_row_le(off, r0, r1, j);
-        col[row_off[new_of_old[o]] + (j - off[o])] = src_of_old[nbr[j]];
+        col[row_off[new_of_old[o]] + (j - off[o])] = src_of_old[u];
     }
 }
 
@@ -603,49 +594,53 @@ std::unique_ptr<prgpu_graph> assemble_vertices(uint32_t n, const uint64_t* off, 
     return g;
 }
 
-// Second half: the engine edge array and the degree-bin counts.
-void assemble_edges(prgpu_graph* g, const uint64_t* off, const uint32_t* nbr, const uint32_t* out_deg,
-                    cudaStream_t st) {
-    PhaseLog ph("assemble", st);
-    const uint32_t n = g->n;
-    const uint64_t e = g->e;
-    // engine edges (+16 zero pad for the kernels' 128-bit colidx loads)
-    g->col.alloc(e + 16);
-    PRGPU_CUDA(cudaMemsetAsync(g->col.p + e, 0, 16 * sizeof(uint32_t), st));
-    if (e) {
-        DevBuf<uint32_t> src_of_old(n);
-        src_of_old_kernel<<<grid_for(n), kThreads, 0, st>>>(g->rowinfo.p, g->new_of_old.p, n, src_of_old.p);
+// Second half: the engine edge array, filled in edge ranges (graph_from_csr
+// places each slice of the neighbour array as it lands), then rows sorted.
+struct EdgeFill {
+    prgpu_graph* g;
+    DevBuf<uint32_t> src_of_old;
+    EdgeFill(prgpu_graph* gr, cudaStream_t st) : g(gr) {
+        // engine edges (+16 zero pad for the kernels' 128-bit colidx loads)
+        g->col.alloc(g->e + 16);
+        PRGPU_CUDA(cudaMemsetAsync(g->col.p + g->e, 0, 16 * sizeof(uint32_t), st));
+        src_of_old.alloc(g->n);
+        src_of_old_kernel<<<grid_for(g->n), kThreads, 0, st>>>(g->rowinfo.p, g->new_of_old.p, g->n,
+                                                               src_of_old.p);
         PRGPU_LAUNCHED("src_of_old");
-        const uint64_t blocks = (e + kEdgeChunk - 1) / kEdgeChunk;
-        scatter_edges<<<(unsigned)blocks, kThreads, 0, st>>>(off, nbr, n, e, g->new_of_old.p, g->row_off.p,
-                                                             src_of_old.p, g->col.p);
-        PRGPU_LAUNCHED("scatter_edges");
+    }
+    void place(const uint64_t* off, const uint32_t* nbr, uint64_t jb, uint64_t je, uint32_t* cnt, int* bad,
+               cudaStream_t st) {
+        if (je <= jb) return;
+        const uint64_t blocks = (je - jb + kEdgeChunk - 1) / kEdgeChunk;
+        place_edges<<<(unsigned)blocks, kThreads, 0, st>>>(off, nbr, g->n, jb, je, g->new_of_old.p,
+                                                           g->row_off.p, src_of_old.p, g->col.p, cnt, bad);
+        PRGPU_LAUNCHED("place_edges");
+    }
+    void finish(cudaStream_t st) {
+        src_of_old.reset();
         const char* rs = std::getenv("PRGPU_ROW_SORT"); // =0: leave rows unsorted (tuning)
-        if (!(rs && std::atoi(rs) == 0)) {
-            const uint32_t h = g->hub_end, m512 = g->sort_end[0], m128 = g->sort_end[1],
-                           m32 = g->warp_end, m8 = g->sort_end[2];
-            if (m512 > h) {
-                sort_rows_block<<<m512 - h, 256, 0, st>>>(g->row_off.p, h, (int)bits_for(std::max(g->nsrc, 2u)),
-                                                          g->col.p);
-                PRGPU_LAUNCHED("sort_rows_block");
-            }
-            if (m128 > m512) {
-                sort_rows_warp<16><<<(m128 - m512 + 7) / 8, 256, 0, st>>>(g->row_off.p, m512, m128, g->col.p);
-                PRGPU_LAUNCHED("sort_rows_warp16");
-            }
-            if (m32 > m128) {
-                sort_rows_warp<4><<<(m32 - m128 + 7) / 8, 256, 0, st>>>(g->row_off.p, m128, m32, g->col.p);
-                PRGPU_LAUNCHED("sort_rows_warp4");
-            }
-            if (m8 > m32) {
-                sort_rows_warp<1><<<(m8 - m32 + 7) / 8, 256, 0, st>>>(g->row_off.p, m32, m8, g->col.p);
-                PRGPU_LAUNCHED("sort_rows_warp1");
-            }
+        if (rs && std::atoi(rs) == 0) return;
+        const uint32_t h = g->hub_end, m512 = g->sort_end[0], m128 = g->sort_end[1], m32 = g->warp_end,
+                       m8 = g->sort_end[2];
+        if (m512 > h) {
+            sort_rows_block<<<m512 - h, 256, 0, st>>>(g->row_off.p, h, (int)bits_for(std::max(g->nsrc, 2u)),
+                                                      g->col.p);
+            PRGPU_LAUNCHED("sort_rows_block");
+        }
+        if (m128 > m512) {
+            sort_rows_warp<16><<<(m128 - m512 + 7) / 8, 256, 0, st>>>(g->row_off.p, m512, m128, g->col.p);
+            PRGPU_LAUNCHED("sort_rows_warp16");
+        }
+        if (m32 > m128) {
+            sort_rows_warp<4><<<(m32 - m128 + 7) / 8, 256, 0, st>>>(g->row_off.p, m128, m32, g->col.p);
+            PRGPU_LAUNCHED("sort_rows_warp4");
+        }
+        if (m8 > m32) {
+            sort_rows_warp<1><<<(m8 - m32 + 7) / 8, 256, 0, st>>>(g->row_off.p, m32, m8, g->col.p);
+            PRGPU_LAUNCHED("sort_rows_warp1");
         }
     }
-    ph.mark("edges");
-}
-
+};
 
 // Sorted unique original-id keys (target << lg | source) -> engine graph.
 // Consumes `keys`.
@@ -671,7 +666,9 @@ std::unique_ptr<prgpu_graph> assemble(DevBuf<uint64_t>&& keys_in, uint64_t u, ui
     keys.reset();
     in_deg.reset();
     auto g = assemble_vertices(n, off.p, u, out_deg.p, lg, device, st);
-    assemble_edges(g.get(), off.p, nbr.p, out_deg.p, st);
+    EdgeFill fill(g.get(), st);
+    fill.place(off.p, nbr.p, 0, u, nullptr, nullptr, st);
+    fill.finish(st);
     return g;
 }
 
@@ -713,16 +710,23 @@ std::unique_ptr<prgpu_graph> graph_from_csr(uint32_t n, const uint64_t* off, con
     PhaseLog ph("from_csr", st);
     DevBuf<uint64_t> d_off((size_t)n + 1);
     DevBuf<uint32_t> d_nbr(std::max<uint64_t>(e, 1)), d_deg(n);
-    // the neighbour array (the bulk) travels on a side stream while the
-    // vertex half of the build runs on `st`
-    Stream side;
-    Event ready, landed;
-    PRGPU_CUDA(cudaEventRecord(ready, st)); // d_nbr's allocation is ordered on st
-    PRGPU_CUDA(cudaStreamWaitEvent(side, ready, 0));
-    if (e) PRGPU_CUDA(cudaMemcpyAsync(d_nbr.p, nbr, e * 4, cudaMemcpyHostToDevice, side));
-    PRGPU_CUDA(cudaEventRecord(landed, side));
+    // offsets and degrees first; the neighbour array (the bulk) follows on a
+    // side stream in slices, while `st` runs the vertex half of the build and
+    // then places each slice as it lands
     PRGPU_CUDA(cudaMemcpyAsync(d_off.p, off, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, st));
     PRGPU_CUDA(cudaMemcpyAsync(d_deg.p, out_degree, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    Stream side;
+    Event meta;
+    PRGPU_CUDA(cudaEventRecord(meta, st)); // also orders d_nbr's allocation
+    PRGPU_CUDA(cudaStreamWaitEvent(side, meta, 0));
+    const uint64_t slice = std::max<uint64_t>(8ull << 20, (e + 7) / 8);
+    std::vector<std::unique_ptr<Event>> landed;
+    for (uint64_t j = 0; j < e; j += slice) {
+        const uint64_t k = std::min(slice, e - j);
+        PRGPU_CUDA(cudaMemcpyAsync(d_nbr.p + j, nbr + j, k * 4, cudaMemcpyHostToDevice, side));
+        landed.emplace_back(std::make_unique<Event>());
+        PRGPU_CUDA(cudaEventRecord(*landed.back(), side));
+    }
     DevBuf<int> bad(1);
     PRGPU_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
     check_offsets<<<grid_for(n), kThreads, 0, st>>>(d_off.p, n, e, bad.p);
@@ -732,23 +736,30 @@ std::unique_ptr<prgpu_graph> graph_from_csr(uint32_t n, const uint64_t* off, con
         fail(PRGPU_EINVAL, "graph_from_csr: offsets not monotone");
     }
     ph.mark("offsets h2d + check");
-    auto g = assemble_vertices(n, d_off.p, e, d_deg.p, lg, device, st);
-    PRGPU_CUDA(cudaStreamWaitEvent(st, landed, 0));
-    ph.mark("neighbours landed");
+    std::unique_ptr<prgpu_graph> g;
     DevBuf<uint32_t> cnt(n);
-    PRGPU_CUDA(cudaMemsetAsync(cnt.p, 0, (size_t)n * 4, st));
-    if (e) {
-        check_edges<<<(unsigned)((e + kEdgeChunk - 1) / kEdgeChunk), kThreads, 0, st>>>(d_off.p, d_nbr.p, n, e,
-                                                                                      cnt.p, bad.p);
-        PRGPU_LAUNCHED("check_edges");
+    try {
+        g = assemble_vertices(n, d_off.p, e, d_deg.p, lg, device, st);
+        ph.mark("vertex half");
+        PRGPU_CUDA(cudaMemsetAsync(cnt.p, 0, (size_t)n * 4, st));
+        EdgeFill fill(g.get(), st);
+        for (size_t c = 0; c < landed.size(); ++c) {
+            PRGPU_CUDA(cudaStreamWaitEvent(st, *landed[c], 0));
+            const uint64_t j = c * slice;
+            fill.place(d_off.p, d_nbr.p, j, std::min(e, j + slice), cnt.p, bad.p, st);
+        }
         if (read_flag(bad, st))
             fail(PRGPU_EINVAL, "graph_from_csr: neighbours not ascending/unique/in range");
+        compare_u32<<<grid_for(n), kThreads, 0, st>>>(cnt.p, d_deg.p, n, bad.p);
+        PRGPU_LAUNCHED("compare_u32");
+        if (read_flag(bad, st)) fail(PRGPU_EINVAL, "graph_from_csr: out_degree does not match in_neighbors");
+        ph.mark("edges placed");
+        fill.finish(st);
+        ph.mark("rows sorted");
+    } catch (...) {
+        cudaStreamSynchronize(side); // no copy may still target d_nbr
+        throw;
     }
-    compare_u32<<<grid_for(n), kThreads, 0, st>>>(cnt.p, d_deg.p, n, bad.p);
-    PRGPU_LAUNCHED("compare_u32");
-    if (read_flag(bad, st)) fail(PRGPU_EINVAL, "graph_from_csr: out_degree does not match in_neighbors");
-    ph.mark("validate edges");
-    assemble_edges(g.get(), d_off.p, d_nbr.p, d_deg.p, st);
     return g;
 }
 
