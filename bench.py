@@ -470,11 +470,31 @@ def measure_e2e(args, cfg, g, prl, torch, dev, lane_its):
 
     for _ in range(max(1, args.warmup // 2)):
         step()
-    steps = max(1, min(args.steps, 5))
-    t0 = time.perf_counter()
+    # host-side timing per step; the median is reported (host<->device copies
+    # on a shared PCIe host vary run to run), the mean and each step alongside
+    steps = max(3, min(args.steps, 9))
+    per = []
     for _ in range(steps):
+        t0 = time.perf_counter()
         step()
-    dt = (time.perf_counter() - t0) / steps
+        per.append(time.perf_counter() - t0)
+    dt = statistics.median(per)
+    # plain pinned-copy bandwidth right after, for context
+    bw = {}
+    try:
+        dbuf = torch.empty(nbr.numel(), dtype=nbr.dtype, device=f"cuda:{dev}")
+        for name, fn in (("h2d_gbs", lambda: dbuf.copy_(nbr, non_blocking=True)),
+                         ("d2h_gbs", lambda: nbr.copy_(dbuf, non_blocking=True))):
+            fn()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize(dev)
+            bw[name] = round(3 * nbr.numel() * 4 / (time.perf_counter() - t0) / 1e9, 1)
+        del dbuf
+    except Exception:
+        pass
     if os.environ.get("PRGPU_TIMING_LOG"):
         for a_, b_, c_ in split:
             print(f"e2e split: from_csr {a_ * 1e3:.1f} ms, pagerank {b_ * 1e3:.1f} ms, free {c_ * 1e3:.1f} ms",
@@ -482,7 +502,9 @@ def measure_e2e(args, cfg, g, prl, torch, dev, lane_its):
     h2d = 8 * (n + 1) + 4 * e + 4 * n + 8 * K
     d2h = 8 * K * n + 13 * K
     return {"value": lane_its * e / dt / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3, "steps": steps,
+            "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3, "steps": steps, "statistic": "median",
+            "ms_mean": statistics.mean(per) * 1e3, "ms_each": [round(x * 1e3, 2) for x in per],
+            "pinned_copy": bw,
             "path": "prgpu_graph_from_csr + prgpu_pagerank (C ABI, pinned host buffers)"}
 
 
