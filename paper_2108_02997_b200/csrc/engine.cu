@@ -30,7 +30,7 @@ __global__ void init_kernel(Params P, uint32_t ndangling) {
          v += (size_t)gridDim.x * blockDim.x) {
         const uint2 ri = P.rowinfo[v];
         if (v < P.empty_begin)
-            for (uint32_t k = 0; k < P.K; ++k) P.rank[0][k * n + v] = r0;
+            for (uint32_t k = 0; k < P.K; ++k) P.rank[0][v * KS + k] = r0;
         if (ri.x) {
             const double cv = __ddiv_rn(r0, (double)ri.x);
             double* c = caddr<KS>(P, 0, ri.y);
@@ -67,13 +67,13 @@ __global__ void extract_ranks(Params P, const uint32_t* __restrict__ new_of_old,
     const int k1 = lane_only >= 0 ? lane_only + 1 : (int)P.K;
     for (int k = k0; k < k1; ++k) {
         const int buf = use_current ? (P.gs->iter & 1) : (P.lanes[k].iterations & 1);
-        const double* src = P.rank[buf] + (size_t)k * n;
+        const double* src = P.rank[buf] + k; // row-major [row][ks]
         const double c0 = P.lanes[k].c0_used; // rows with no in-edges hold c0
         double* dst = out + (size_t)(k - k0) * n;
         for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n;
              v += (size_t)gridDim.x * blockDim.x) {
             const uint32_t r = new_of_old[v];
-            dst[v] = r >= P.empty_begin ? c0 : src[r];
+            dst[v] = r >= P.empty_begin ? c0 : src[(size_t)r * P.ks];
         }
     }
 }
@@ -541,8 +541,8 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     cudaStream_t st = s->stream;
     PhaseLog ph("session", st);
 
-    s->rank.alloc(2 * (size_t)K * n);
     const int KS = s->cfg.KS;
+    s->rank.alloc(2 * (size_t)KS * n);
     double* cbase = ext_contrib;
     if (!cbase) {
         s->contrib.alloc(2 * nsrc * KS);
@@ -593,7 +593,8 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     P.col = g->col.p;
     P.rowinfo = g->rowinfo.p;
     P.rank[0] = s->rank.p;
-    P.rank[1] = s->rank.p + (size_t)K * n;
+    P.rank[1] = s->rank.p + (size_t)s->cfg.KS * n;
+    P.ks = (uint32_t)s->cfg.KS;
     P.ref = s->ref.p;
     P.trace = s->trace.p;
     P.lanes = s->lanes.p;
@@ -793,8 +794,9 @@ void part_local_ranks(prgpu_session* s, int user_lane, double* out) {
     const prgpu_partition& me = s->parts[s->part_rank];
     const uint32_t stored_end = std::min(me.row_end, s->P.empty_begin);
     if (stored_end > me.row_begin)
-        PRGPU_CUDA(cudaMemcpyAsync(out, s->P.rank[L.iterations & 1] + (size_t)slot * s->g->n + me.row_begin,
-                                   (size_t)(stored_end - me.row_begin) * 8, cudaMemcpyDeviceToHost, s->cur()));
+        PRGPU_CUDA(cudaMemcpy2DAsync(out, 8, s->P.rank[L.iterations & 1] + (size_t)me.row_begin * s->P.ks + slot,
+                                     (size_t)s->P.ks * 8, 8, stored_end - me.row_begin, cudaMemcpyDeviceToHost,
+                                     s->cur()));
     PRGPU_CUDA(cudaStreamSynchronize(s->cur()));
     for (uint32_t r = std::max(me.row_begin, stored_end); r < me.row_end; ++r) out[r - me.row_begin] = L.c0_used;
 }

@@ -88,7 +88,8 @@ struct Params {
     const uint64_t* __restrict__ row_off;
     const uint32_t* __restrict__ col;  // source ids
     const uint2* __restrict__ rowinfo; // {out-degree, source id}
-    double* rank[2];                   // [K][n] (rows < empty_begin only)
+    double* rank[2];                   // [n][ks] row-major, K lanes per row (rows < empty_begin only)
+    uint32_t ks;                       // rank / contribution row stride (doubles)
     double* cbase;                     // contributions [parity][src][KS], see caddr()
     uint64_t cold_off[2];              // first row of each parity buffer (in rows of KS)
     const double* ref;                 // [n] engine ids, or null
@@ -109,7 +110,8 @@ struct Params {
     uint32_t G;
     uint32_t hot_src;            // sources [0, hot_src) in the L2-resident region
     uint32_t l2mode;             // 0 evict hints, 1 persisting window, 2 no hints
-    uint32_t skip_mask;          // profiling only (PRGPU_SKIP): 1 chunk, 2 packed, 4 empty tasks
+    uint32_t skip_mask;          // profiling only (PRGPU_SKIP): 1 chunk, 2 packed, 4 empty tasks,
+                                 // 8 rank stores, 16 rank loads, 32 contribution stores
     // multi-GPU partition (1D row ranges): this rank runs tasks [task_begin, task_end)
     // and leaves its partial vector in rank_partials[part_rank]; a separate
     // finalize reduces all ranks' vectors in rank order after the exchange
@@ -347,23 +349,49 @@ struct Warp {
         epilogue_with<true>(v, sl, acc, ri, acc);
     }
 
-    // the epilogue with the row's info and previous ranks already at hand
+    // the epilogue with the row's info and previous ranks already at hand.
+    // Ranks are row-major [row][KS]: a lane group reads and writes one
+    // contiguous row (3 sectors at K = 11) instead of K scattered words.
     template <bool LOAD_PREV = false>
     __device__ __forceinline__ void epilogue_with(uint32_t v, int sl, const double (&acc)[W], uint2 ri,
-                                                  const double (&o)[W]) {
+                                                  const double (&o_in)[W]) {
         const uint32_t d = ri.x;
-        const size_t n = P.n;
-        double cv[W];
+        double o[W];
+        if constexpr (LOAD_PREV) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) o[w] = 0.0;
+            if (lane_ok(sl) && !(P.skip_mask & 16)) {
+                const double* rr = rp + (size_t)v * KS + sl * W;
+                if constexpr (W % 2 == 0) {
+#pragma unroll
+                    for (int w = 0; w < W; w += 2) {
+                        const double2 x = __ldcs(reinterpret_cast<const double2*>(rr + w));
+                        o[w] = x.x;
+                        o[w + 1] = x.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) o[w] = __ldcs(rr + w);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int w = 0; w < W; ++w) o[w] = o_in[w];
+        }
+        double cv[W], nr[W];
+        bool act[W];
         bool any = false;
 #pragma unroll
         for (int w = 0; w < W; ++w) {
             const int k = sl * W + w;
             cv[w] = 0.0;
-            if (k < (int)P.K && s_active[k]) {
+            nr[w] = 0.0;
+            act[w] = k < (int)P.K && s_active[k];
+            if (act[w]) {
                 any = true;
                 // next[v] = teleport + alpha*acc, two roundings (pagerank.hpp:92)
                 const double r = __dadd_rn(s_c0[k], __dmul_rn(s_alpha[k], acc[w]));
-                const double df = __dsub_rn(r, LOAD_PREV ? __ldcs(rp + (size_t)k * n + v) : o[w]);
+                const double df = __dsub_rn(r, o[w]);
                 const double ad = fabs(df);
                 part.add(0, w, ad);
                 part.add(1, w, df * df);
@@ -371,11 +399,28 @@ struct Warp {
                 if (d == 0) part.add(3, w, r);
                 if constexpr ((QM & 16) != 0)
                     if (P.ref) part.add(4, w, fabs(__dsub_rn(r, __ldg(P.ref + v))));
-                __stcs(rn + (size_t)k * n + v, r);
+                nr[w] = r;
                 if (d) cv[w] = __ddiv_rn(r, (double)d); // prev[u]/out_degree[u] (:91)
             }
         }
-        if (d && any && lane_ok(sl)) write_contrib(ri.y, sl, cv);
+        if (any && !(P.skip_mask & 8)) { // frozen lanes keep their final value: masked stores
+            double* rw = rn + (size_t)v * KS + sl * W;
+            if constexpr (W % 2 == 0) {
+#pragma unroll
+                for (int w = 0; w < W; w += 2) {
+                    if (act[w] && act[w + 1]) __stcs(reinterpret_cast<double2*>(rw + w), make_double2(nr[w], nr[w + 1]));
+                    else {
+                        if (act[w]) __stcs(rw + w, nr[w]);
+                        if (act[w + 1]) __stcs(rw + w + 1, nr[w + 1]);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int w = 0; w < W; ++w)
+                    if (act[w]) __stcs(rw + w, nr[w]);
+            }
+        }
+        if (d && any && lane_ok(sl) && !(P.skip_mask & 32)) write_contrib(ri.y, sl, cv);
     }
 
     // Accumulate edges [lo, hi) into acc with 128-bit colidx loads; slot s
