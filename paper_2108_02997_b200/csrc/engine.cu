@@ -175,11 +175,13 @@ struct LaneCfg {
     KernelFn fn;        // pull_kernel instance
     int QM = kQmAll;
     KernelFn fin = nullptr; // matching part_finalize_kernel (multi-GPU)
+    int paths = 3;          // task kinds compiled in (pull_kernel PATHS)
     int KP() const { return LG * W; }
     size_t smem() const {
         const size_t staged = KP() == 1 ? (size_t)kWarps * 2 * WIN * sizeof(double) // STAGED
                                         : 0;
-        const size_t cols = W >= 6 ? (size_t)popc_c(QM) * W * kNT * sizeof(double) : 0;    // Partials
+        const bool smemp = W >= 6 || (paths == 2 && KP() > 1);
+        const size_t cols = smemp ? (size_t)popc_c(QM) * W * kNT * sizeof(double) : 0;     // Partials
         return staged + cols;
     }
 };
@@ -192,41 +194,48 @@ inline int variant() {
 
 // `all_q`: the run needs every partial (all norms / the reference trace);
 // otherwise only L1 + dangling (the damping sweep's stopping rule).
-template <int LG, int W, int WIN, int QJ, int MINB, int QM, int KS>
+template <int LG, int W, int WIN, int QJ, int MINB, int QM, int KS, int PATHS = 3>
 LaneCfg mk_cfg() {
-    return LaneCfg{LG, W, WIN, KS ? KS : LG * W, pull_kernel<LG, W, WIN, QJ, MINB, QM, KS>, QM,
-                   part_finalize_kernel<LG, W, WIN, QJ, MINB, QM, KS>};
+    return LaneCfg{LG, W, WIN, KS ? KS : LG * W, pull_kernel<LG, W, WIN, QJ, MINB, QM, KS, PATHS>, QM,
+                   part_finalize_kernel<LG, W, WIN, QJ, MINB, QM, KS>, PATHS};
 }
 
-template <int LG, int W, int WIN, int MINB, int KS = LG * W>
+template <int LG, int W, int WIN, int MINB, int KS = LG * W, int PATHS = 3>
 LaneCfg wide_cfg(bool all_q) {
-    return all_q ? mk_cfg<LG, W, WIN, 0, MINB, kQmAll, KS>() : mk_cfg<LG, W, WIN, 0, MINB, kQmL1, KS>();
+    return all_q ? mk_cfg<LG, W, WIN, 0, MINB, kQmAll, KS, PATHS>()
+                 : mk_cfg<LG, W, WIN, 0, MINB, kQmL1, KS, PATHS>();
 }
 
+// Defaults measured on B200 (scripts/gpu_variants*.sh).
+// Wide lanes: two doubles per thread (one 16-byte load per edge), LG = KS/2
+// threads per edge, rows padded to whole 32-byte sectors.
+template <int PATHS>
+LaneCfg lane_cfg_t(int K, bool all_q) {
+    if (K == 1) return mk_cfg<1, 1, 256, 2, 3, kQmAll, 0, PATHS>();
+    if (K == 2) return wide_cfg<1, 2, 64, 4, 2, PATHS>(all_q);
+    if (K <= 4) return wide_cfg<2, 2, 128, 4, 4, PATHS>(all_q);
+    if (K <= 8) return wide_cfg<4, 2, 128, 4, 8, PATHS>(all_q);
+    if (K <= 12) return wide_cfg<8, 2, 128, 4, 12, PATHS>(all_q);
+    return wide_cfg<8, 2, 128, 4, 16, PATHS>(all_q);
+}
+
+// One kernel per iteration (PATHS = 3); PRGPU_VARIANT selects the
+// alternatives that lost (tuning only).
 inline LaneCfg lane_cfg(int K, bool all_q) {
-    // Defaults measured on B200 (scripts/gpu_variants*.sh);
-    // PRGPU_VARIANT selects the alternatives that lost.
     const int var = variant();
     if (K == 1) {
         switch (var) {
         case 1: return mk_cfg<1, 1, 256, 4, 2, kQmAll, 0>();
         case 2: return mk_cfg<1, 1, 256, 4, 3, kQmAll, 0>();
         case 3: return mk_cfg<1, 1, 256, 2, 4, kQmAll, 0>();
-        default: return mk_cfg<1, 1, 256, 2, 3, kQmAll, 0>();
+        default: break;
         }
-    }
-    // wide lanes: two doubles per thread (one 16-byte load per edge),
-    // LG = KS/2 threads per edge, rows padded to whole 32-byte sectors
-    if (K == 2) return wide_cfg<1, 2, 64, 4>(all_q);
-    if (K <= 4) return wide_cfg<2, 2, 128, 4>(all_q);
-    if (K <= 8) return wide_cfg<4, 2, 128, 4>(all_q);
-    if (K <= 12) {
+    } else if (K > 8 && K <= 12) {
         if (var == 1) return wide_cfg<8, 2, 64, 4, 12>(all_q);
         if (var == 2) return wide_cfg<8, 2, 128, 3, 12>(all_q);
         if (var == 3) return wide_cfg<8, 2, 64, 3, 12>(all_q);
-        return wide_cfg<8, 2, 128, 4, 12>(all_q);
     }
-    return wide_cfg<8, 2, 128, 4>(all_q);
+    return lane_cfg_t<3>(K, all_q);
 }
 
 void launch_init(const LaneCfg& c, const Params& P, uint32_t ndangling, cudaStream_t st) {
@@ -253,7 +262,11 @@ using namespace prgpu;
 struct prgpu_session {
     prgpu_graph* g = nullptr;
     int K = 1, KP = 1, max_iter = 500;
-    LaneCfg cfg{};
+    LaneCfg cfg{};   // the (first) pull kernel
+    LaneCfg cfg2{};  // split iteration: the packed + empty kernel
+    bool split = false;
+    Params P1{};     // split iteration: the hub-chunk kernel's parameters
+    size_t smem1 = 0, smem2 = 0;
     Params P{};
     Stream stream;
     DevBuf<double> rank, contrib, partials, trace, ref, chunk_acc;
@@ -402,7 +415,7 @@ void build_tasks(prgpu_session* s) {
     }
     // rows with no in-edges: only those with out-edges need a task (their next
     // contribution c0/d), unless the reference trace needs every row
-    const uint32_t er = 8 * (32 / s->cfg.LG);
+    const uint32_t er = 8 * (32 / s->cfg2.LG); // empty tasks run in the (second) kernel
     const uint32_t iso_begin = std::max(phi, n - count_isolated(g, st));
     const uint32_t n_empty_rows = (s->P.ref ? n : iso_begin) - phi;
     s->P.iso_begin = iso_begin;
@@ -533,6 +546,23 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         const uint32_t mask = p->stop_mask ? p->stop_mask : (1u << p->norm);
         const bool l1_only = mask == 1u && p->norm == PRGPU_NORM_L1 && !p->ref_ranks;
         s->cfg = lane_cfg(s->K, !l1_only);
+        s->cfg2 = s->cfg;
+        // split iteration (hub-chunk kernel, then packed + empty kernel) for
+        // the single-GPU run; PRGPU_SPLIT=0 or a tuning variant: one kernel
+        const char* sp = std::getenv("PRGPU_SPLIT");
+        // (measured: -2% at C2 K=11, +3% at K=1 on the same graph: K > 1 only)
+        s->split = nranks == 0 && s->K > 1 && !(sp && std::atoi(sp) == 0) && variant() == 0;
+        if (s->split) {
+            s->cfg = lane_cfg_t<1>(s->K, !l1_only);
+            s->cfg2 = lane_cfg_t<2>(s->K, !l1_only);
+            if (const char* v2 = std::getenv("PRGPU_VARIANT2")) { // tuning only
+                const int var2 = std::atoi(v2);
+                if (s->K > 8 && s->K <= 12 && var2 == 1) s->cfg2 = wide_cfg<16, 1, 128, 4, 12, 2>(!l1_only);
+                if (s->K > 8 && s->K <= 12 && var2 == 2) s->cfg2 = wide_cfg<8, 2, 128, 5, 12, 2>(!l1_only);
+                if (s->K > 8 && s->K <= 12 && var2 == 3) s->cfg2 = wide_cfg<16, 1, 128, 5, 12, 2>(!l1_only);
+                if (s->K > 8 && s->K <= 12 && var2 == 4) s->cfg2 = wide_cfg<8, 2, 128, 3, 12, 2>(!l1_only);
+            }
+        }
     }
     s->KP = s->cfg.KP();
     s->max_iter = p->max_iterations;
@@ -642,20 +672,41 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     }
 
     ph.mark("init + tasks");
-    // persistent grid: resident CTAs, but at least ~4 tasks per warp
-    const size_t smem = s->cfg.smem();
-    PRGPU_CUDA(cudaFuncSetAttribute((const void*)s->cfg.fn,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int dev_sms = 0, per_sm = 0;
+    // persistent grids: resident CTAs, but at least ~4 tasks per warp
+    int dev_sms = 0;
     PRGPU_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, g->device));
-    PRGPU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)s->cfg.fn, kNT, smem));
-    per_sm = std::max(1, per_sm);
-    const uint64_t tasks = (uint64_t)P.task_end - P.task_begin;
-    const uint64_t want = (tasks + kWarps * 4 - 1) / (kWarps * 4);
-    const uint32_t G = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)dev_sms * per_sm, want));
-    P.G = G;
-    s->partials.alloc((size_t)kNQ * KP * G);
+    auto grid_for_cfg = [&](const LaneCfg& c, uint64_t tasks, size_t& smem) -> uint32_t {
+        smem = c.smem();
+        PRGPU_CUDA(cudaFuncSetAttribute((const void*)c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        PRGPU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)c.fn, kNT, smem));
+        per_sm = std::max(1, per_sm);
+        const uint64_t want = (tasks + kWarps * 4 - 1) / (kWarps * 4);
+        return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)dev_sms * per_sm, want));
+    };
+    if (s->split && P.n_chunk == 0) s->split = false; // no hub rows: the packed + empty kernel alone
+    uint32_t G1 = 0;
+    if (s->split) {
+        G1 = grid_for_cfg(s->cfg, P.n_chunk, s->smem1);
+        P.task_begin = P.n_chunk;
+        P.G = grid_for_cfg(s->cfg2, (uint64_t)P.task_end - P.task_begin, s->smem2);
+    } else { // one kernel: cfg2 (== cfg unless the split was dropped for lack of hub rows)
+        P.G = grid_for_cfg(s->cfg2, (uint64_t)P.task_end - P.task_begin, s->smem2);
+    }
+    const uint32_t G = P.G;
+    P.gtot = G1 + G;
+    P.pcol0 = G1;
+    P.no_finalize = 0;
+    s->partials.alloc((size_t)kNQ * KP * P.gtot);
     P.partials = s->partials.p;
+    if (s->split) {
+        s->P1 = P;
+        s->P1.task_begin = 0;
+        s->P1.task_end = P.n_chunk;
+        s->P1.G = G1;
+        s->P1.pcol0 = 0;
+        s->P1.no_finalize = 1;
+    }
 
     PRGPU_CUDA(cudaEventCreate(&s->e0));
     PRGPU_CUDA(cudaEventCreate(&s->e1));
@@ -676,18 +727,32 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         cudaGraphNode_t cnode;
         PRGPU_CUDA(cudaGraphAddNode(&cnode, s->graph, nullptr, 0, &cp));
         cudaGraph_t body = cp.conditional.phGraph_out[0];
+        cudaGraphNode_t k1node = nullptr;
+        if (s->split) {
+            Params P1 = s->P1;
+            P1.use_cond = 1;
+            P1.cond = h;
+            cudaKernelNodeParams kp1 = {};
+            kp1.func = (void*)s->cfg.fn;
+            kp1.gridDim = dim3(P1.G);
+            kp1.blockDim = dim3(kNT);
+            kp1.sharedMemBytes = (unsigned)s->smem1;
+            void* args1[] = {&P1};
+            kp1.kernelParams = args1;
+            PRGPU_CUDA(cudaGraphAddKernelNode(&k1node, body, nullptr, 0, &kp1));
+        }
         Params PG = P;
         PG.use_cond = 1;
         PG.cond = h;
         cudaKernelNodeParams kp = {};
-        kp.func = (void*)s->cfg.fn;
+        kp.func = (void*)s->cfg2.fn;
         kp.gridDim = dim3(G);
         kp.blockDim = dim3(kNT);
-        kp.sharedMemBytes = (unsigned)smem;
+        kp.sharedMemBytes = (unsigned)s->smem2;
         void* args[] = {&PG};
         kp.kernelParams = args;
         cudaGraphNode_t knode;
-        PRGPU_CUDA(cudaGraphAddKernelNode(&knode, body, nullptr, 0, &kp));
+        PRGPU_CUDA(cudaGraphAddKernelNode(&knode, body, k1node ? &k1node : nullptr, k1node ? 1 : 0, &kp));
         PRGPU_CUDA(cudaGraphInstantiate(&s->exec, s->graph, 0));
         s->use_graph = true;
     }
@@ -746,9 +811,15 @@ void session_init(prgpu_session* s) {
 }
 
 void launch_pull(prgpu_session* s) {
+    if (s->split) {
+        Params P1 = s->P1;
+        P1.use_cond = 0;
+        s->cfg.fn<<<P1.G, kNT, s->smem1, s->cur()>>>(P1);
+        PRGPU_LAUNCHED("pull_kernel (hub chunks)");
+    }
     Params P = s->P;
     P.use_cond = 0;
-    s->cfg.fn<<<P.G, kNT, s->cfg.smem(), s->cur()>>>(P);
+    s->cfg2.fn<<<P.G, kNT, s->smem2, s->cur()>>>(P);
     PRGPU_LAUNCHED("pull_kernel");
 }
 

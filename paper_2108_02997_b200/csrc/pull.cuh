@@ -122,6 +122,12 @@ struct Params {
     int use_cond;
     cudaGraphConditionalHandle cond;
     int* frozen_at; // host-mapped [K]: iteration at which each lane stopped (0: live), or null
+    // split iteration (single GPU): the hub-chunk tasks run as a first kernel
+    // that only leaves its CTA partials (no_finalize), the packed and empty
+    // tasks as a second kernel whose last CTA reduces both kernels' columns.
+    // partials is [kNQ*KP][gtot]; this kernel's CTAs own columns pcol0 + blockIdx.x
+    uint32_t pcol0, gtot;
+    int no_finalize;
 };
 
 // ---- L2 residency control -------------------------------------------------------
@@ -182,6 +188,16 @@ __device__ __forceinline__ uint2 ld_stream_u2(const uint2* p, uint64_t pol) {
         : "=r"(r.x), "=r"(r.y)
         : "l"(p), "l"(pol));
     return r;
+}
+
+// asynchronous 16-byte global -> shared copies (LDGSTS): gathers in flight
+// without holding registers
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
 // gathers: plain read-only loads (measured: L2 residency hints on the
@@ -289,7 +305,7 @@ struct PullCfg {
     static constexpr int SMEM_WARP = STAGED ? EMAX * KS : 0; // doubles per warp
 };
 
-template <int LG, int W, int WIN, int QJ_ = 0, int QM = kQmAll, int KS_ = 0>
+template <int LG, int W, int WIN, int QJ_ = 0, int QM = kQmAll, int KS_ = 0, bool SMEMP_ = (W >= 6)>
 struct Warp {
     using C = PullCfg<LG, W, WIN, QJ_, KS_>;
     static constexpr int KP = C::KP, ES = C::ES, KS = C::KS;
@@ -301,7 +317,7 @@ struct Warp {
     const double* s_alpha;
     const double* s_c0;
     const int* s_active;
-    static constexpr bool SMEMP = (W >= 6);
+    static constexpr bool SMEMP = SMEMP_; // partials in a shared-memory column (frees registers)
     Partials<W, QM, SMEMP> part;
 
     __device__ Warp(const Params& p, int parity, int ln, const double* a, const double* c0,
@@ -668,6 +684,88 @@ struct Warp {
         }
     }
 
+    // K > 1 packed run, software-pipelined: each slot issues the next row's
+    // offsets, row info and previous ranks before gathering the current row,
+    // so a row costs the colidx -> gather chain only.
+    __device__ void packed_pipe(uint32_t t, double* __restrict__ stage) {
+        const uint64_t sp = stream_policy(P);
+        const uint32_t r0 = P.packed_r0[t], r1 = P.packed_r0[t + 1];
+        const uint32_t R = r1 - r0;
+        uint32_t i = slot;
+        if (i >= R) return;
+        const bool ok = slice_live();
+        const bool lok = lane_ok(slice);
+        auto load_prev = [&](uint32_t v, double (&o)[W]) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) o[w] = 0.0;
+            if (lok) {
+                const double* rr = rp + (size_t)v * KS + slice * W;
+                if constexpr (W % 2 == 0) {
+#pragma unroll
+                    for (int w = 0; w < W; w += 2) {
+                        const double2 x = __ldcs(reinterpret_cast<const double2*>(rr + w));
+                        o[w] = x.x;
+                        o[w + 1] = x.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) o[w] = __ldcs(rr + w);
+                }
+            }
+        };
+        uint32_t v = r0 + i;
+        uint64_t lo = ld_stream_u64(P.row_off + v, sp), hi = ld_stream_u64(P.row_off + v + 1, sp);
+        uint2 ri = ld_stream_u2(P.rowinfo + v, sp);
+        double o[W];
+        load_prev(v, o);
+        for (;;) {
+            const uint32_t in = i + ES;
+            const bool more = in < R;
+            const uint32_t vn = r0 + (more ? in : i);
+            // next row's metadata, in flight during this row's gathers
+            const uint64_t nlo = ld_stream_u64(P.row_off + vn, sp), nhi = ld_stream_u64(P.row_off + vn + 1, sp);
+            const uint2 nri = ld_stream_u2(P.rowinfo + vn, sp);
+            double no[W];
+            load_prev(vn, no);
+            double acc[W];
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[w] = 0.0;
+            const uint32_t* __restrict__ cb = P.col + (lo & ~3ull);
+            const uint32_t off0 = (uint32_t)(lo & 3ull);
+            const uint32_t ne = (uint32_t)(hi - lo) + off0;
+            for (uint32_t q = 0; q < ne; q += 8) {
+                const uint4 a = ld_stream_u4(cb + q, sp);
+                const uint4 b = ld_stream_u4(cb + q + 4, sp); // in bounds: colidx is padded by 16
+                const uint32_t us[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                // valid positions of this 8-edge window as a bit mask: one
+                // predicate per gather instead of a compare chain
+                const uint32_t lo_b = q < off0 ? off0 - q : 0u;
+                const uint32_t hi_b = min(8u, ne - q);
+                const uint32_t vb = ok ? (((1u << hi_b) - 1u) & ~((1u << lo_b) - 1u)) : 0u;
+                double vals[8][W];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) vals[j][w] = 0.0;
+                    if (vb & (1u << j)) load_w<W>(cpl + (size_t)us[j] * KS, vals[j]);
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int w = 0; w < W; ++w) acc[w] += vals[j][w];
+            }
+            epilogue_with<false>(v, slice, acc, ri, o);
+            if (!more) break;
+            i = in;
+            v = vn;
+            lo = nlo;
+            hi = nhi;
+            ri = nri;
+#pragma unroll
+            for (int w = 0; w < W; ++w) o[w] = no[w];
+        }
+    }
+
     // ---- rows with no in-edges: rank = c0; write c0/d for rows with out-edges,
     //      and (sweep mode) the L1 distance to the reference -------------------------
     __device__ void empty_task(uint32_t t) {
@@ -761,7 +859,10 @@ __device__ void finalize_lanes(const Params& P, const double* s_tot, const doubl
     }
 }
 
-template <int LG, int W, int WIN, int QJ_, int MINB, int QM = kQmAll, int KS_ = 0>
+// PATHS: which task kinds this instance compiles (1 hub chunks, 2 packed +
+// empty); a split iteration runs a PATHS=1 and a PATHS=2 instance, each with
+// only its own path's register pressure.
+template <int LG, int W, int WIN, int QJ_, int MINB, int QM = kQmAll, int KS_ = 0, int PATHS = 3>
 __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     using C = PullCfg<LG, W, WIN, QJ_, KS_>;
     constexpr int KP = C::KP;
@@ -785,23 +886,32 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     __syncthreads();
     if (!s_flag) return; // speculative launch after convergence (host-loop mode)
 
-    // dynamic smem: [kWarps][SMEM_WARP] staged gathers, then the per-thread
+    // dynamic smem: [kWarps][SMEM_WARP + ASYNC_WARP] staged gathers, then the per-thread
     // partial columns when W >= 6
-    Warp<LG, W, WIN, QJ_, QM, KS_> w(P, s_iter & 1, lane, s_alpha, s_c0, s_active,
-                                     s_dyn + (size_t)kWarps * C::SMEM_WARP, tid);
-    double* sv = s_dyn + (size_t)warp * C::SMEM_WARP;
+    constexpr int ASYNC_WARP = 0; // (LDGSTS-staged packed gathers measured no faster)
+    constexpr int PER_WARP = C::SMEM_WARP + ASYNC_WARP;
+    // the packed + empty instance of a split iteration keeps its partials in
+    // shared memory: the registers go to gathers in flight
+    constexpr bool SMEMP = (W >= 6) || (PATHS == 2 && C::KP > 1);
+    Warp<LG, W, WIN, QJ_, QM, KS_, SMEMP> w(P, s_iter & 1, lane, s_alpha, s_c0, s_active,
+                                     s_dyn + (size_t)kWarps * PER_WARP, tid);
+    double* sv = s_dyn + (size_t)warp * PER_WARP;
     const uint32_t TW = P.G * kWarps;
     const uint32_t T1 = P.n_chunk, T2 = T1 + P.n_packed;
     for (uint32_t t = P.task_begin + blockIdx.x * kWarps + warp; t < P.task_end; t += TW) {
         if (t < T1) {
-            if (!(P.skip_mask & 1)) w.chunk_task(t);
-        } else if (t < T2) {
-            if (!(P.skip_mask & 2)) {
-                if constexpr (C::STAGED) w.packed_task(t - T1, sv);
-                else w.packed_direct(t - T1);
+            if constexpr ((PATHS & 1) != 0)
+                if (!(P.skip_mask & 1)) w.chunk_task(t);
+        } else if constexpr ((PATHS & 2) != 0) {
+            if (t < T2) {
+                if (!(P.skip_mask & 2)) {
+                    if constexpr (C::STAGED) w.packed_task(t - T1, sv);
+                    else if constexpr (PATHS == 2) w.packed_pipe(t - T1, sv);
+                    else w.packed_direct(t - T1);
+                }
+            } else if (!(P.skip_mask & 4)) {
+                w.empty_task(t - T2);
             }
-        } else if (!(P.skip_mask & 4)) {
-            w.empty_task(t - T2);
         }
     }
 
@@ -824,8 +934,10 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
         double v = 0.0;
 #pragma unroll
         for (int wp = 0; wp < kWarps; ++wp) v = (q == 2) ? fmax(v, s_red[wp][t]) : v + s_red[wp][t];
-        P.partials[(size_t)t * P.G + blockIdx.x] = v;
+        P.partials[(size_t)t * P.gtot + P.pcol0 + blockIdx.x] = v;
     }
+
+    if (P.no_finalize) return; // first kernel of a split iteration
 
     // ---- last CTA: reduce partials, convergence, next teleport --------------------------
     __threadfence();
@@ -844,14 +956,14 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
         const int q = t / KP;
         if (!((QM >> q) & 1) || (t % KP) >= (int)P.K) continue;
         double v = 0.0;
-        const double* col = P.partials + (size_t)t * P.G;
+        const double* col = P.partials + (size_t)t * P.gtot;
         uint32_t b = lane;
-        for (; b + 96 < P.G; b += 128) {
+        for (; b + 96 < P.gtot; b += 128) {
             const double x0 = __ldcg(col + b), x1 = __ldcg(col + b + 32), x2 = __ldcg(col + b + 64),
                          x3 = __ldcg(col + b + 96);
             v = (q == 2) ? fmax(fmax(fmax(fmax(v, x0), x1), x2), x3) : (((v + x0) + x1) + x2) + x3;
         }
-        for (; b < P.G; b += 32) {
+        for (; b < P.gtot; b += 32) {
             const double x = __ldcg(col + b);
             v = (q == 2) ? fmax(v, x) : v + x;
         }

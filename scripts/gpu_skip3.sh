@@ -1,0 +1,3 @@
+run() { timeout 300 python scripts/prof_pull.py --config $1 --launches 8 2>&1 | tail -n 1 | sed 's/N=[0-9]* E=[0-9]* hub=[0-9]* warp=[0-9]* thread=[0-9]* empty=[0-9]*//'; }
+for c in c2 c2k1 c4; do for s in 0 6 5 3 7; do echo "$c skip=$s $(PRGPU_SKIP=$s run $c)"; done; done
+python scripts/prof_pull.py --config c2 --launches 1 2>&1 | tail -1
