@@ -179,8 +179,9 @@ struct LaneCfg {
     int KP() const { return LG * W; }
     size_t smem() const {
         const size_t staged = KP() == 1 ? (size_t)kWarps * 2 * WIN * sizeof(double) // STAGED
-                                        : 0;
-        const bool smemp = W >= 6 || (paths == 2 && KP() > 1);
+                              : paths == 2 ? (size_t)kWarps * (kPackOff + (2 * WIN + 8) / 2) * sizeof(double)
+                                           : 0; // packed_pipe stage
+        const bool smemp = W >= 6 || (paths != 3 && KP() > 1);
         const size_t cols = smemp ? (size_t)popc_c(QM) * W * kNT * sizeof(double) : 0;     // Partials
         return staged + cols;
     }

@@ -59,7 +59,8 @@ constexpr bool kBcast = false; // tuning builds only
 #else
 constexpr bool kBcast = true;
 #endif
-constexpr int kNQ = 5; // partials: L1, L2^2, Linf, dangling sum, L1-vs-ref
+constexpr int kNQ = 5;
+constexpr int kPackOff = 40; // staged row offsets per packed run (>= rows per run + 1) // partials: L1, L2^2, Linf, dangling sum, L1-vs-ref
 
 struct LaneState {
     double alpha;
@@ -684,86 +685,87 @@ struct Warp {
         }
     }
 
-    // K > 1 packed run, software-pipelined: each slot issues the next row's
-    // offsets, row info and previous ranks before gathering the current row,
-    // so a row costs the colidx -> gather chain only.
+    // K > 1 packed run.  The warp stages the run's row offsets and colidx in
+    // shared memory with coalesced loads (two round trips for the whole run);
+    // then each slot walks its rows issuing the next row's row info and
+    // previous ranks before gathering the current one, so a row costs a
+    // single gather round trip.
     __device__ void packed_pipe(uint32_t t, double* __restrict__ stage) {
+        constexpr int WIN_ = C::EMAX / 2;
         const uint64_t sp = stream_policy(P);
         const uint32_t r0 = P.packed_r0[t], r1 = P.packed_r0[t + 1];
-        const uint32_t R = r1 - r0;
+        const uint32_t R = r1 - r0; // <= 2*WIN / max(1, WIN/32) + 1
+        uint64_t* s_off = reinterpret_cast<uint64_t*>(stage);                 // [kPackOff]
+        uint32_t* s_col = reinterpret_cast<uint32_t*>(s_off + kPackOff);     // [2*WIN + 8]
+        for (uint32_t x = lane; x <= R; x += 32) s_off[x] = ld_stream_u64(P.row_off + r0 + x, sp);
+        __syncwarp();
+        const uint64_t e0 = s_off[0];
+        const uint32_t ne_all = (uint32_t)(s_off[R] - e0);
+        for (uint32_t x = lane; x < ne_all; x += 32) s_col[x] = ld_stream_u32(P.col + e0 + x, sp);
+        __syncwarp();
         uint32_t i = slot;
-        if (i >= R) return;
-        const bool ok = slice_live();
-        const bool lok = lane_ok(slice);
-        auto load_prev = [&](uint32_t v, double (&o)[W]) {
+        if (i < R) {
+            const bool ok = slice_live();
+            const bool lok = lane_ok(slice);
+            auto load_prev = [&](uint32_t v, double (&o)[W]) {
 #pragma unroll
-            for (int w = 0; w < W; ++w) o[w] = 0.0;
-            if (lok) {
-                const double* rr = rp + (size_t)v * KS + slice * W;
-                if constexpr (W % 2 == 0) {
+                for (int w = 0; w < W; ++w) o[w] = 0.0;
+                if (lok) {
+                    const double* rr = rp + (size_t)v * KS + slice * W;
+                    if constexpr (W % 2 == 0) {
 #pragma unroll
-                    for (int w = 0; w < W; w += 2) {
-                        const double2 x = __ldcs(reinterpret_cast<const double2*>(rr + w));
-                        o[w] = x.x;
-                        o[w + 1] = x.y;
+                        for (int w = 0; w < W; w += 2) {
+                            const double2 x = __ldcs(reinterpret_cast<const double2*>(rr + w));
+                            o[w] = x.x;
+                            o[w + 1] = x.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int w = 0; w < W; ++w) o[w] = __ldcs(rr + w);
                     }
-                } else {
-#pragma unroll
-                    for (int w = 0; w < W; ++w) o[w] = __ldcs(rr + w);
                 }
-            }
-        };
-        uint32_t v = r0 + i;
-        uint64_t lo = ld_stream_u64(P.row_off + v, sp), hi = ld_stream_u64(P.row_off + v + 1, sp);
-        uint2 ri = ld_stream_u2(P.rowinfo + v, sp);
-        double o[W];
-        load_prev(v, o);
-        for (;;) {
-            const uint32_t in = i + ES;
-            const bool more = in < R;
-            const uint32_t vn = r0 + (more ? in : i);
-            // next row's metadata, in flight during this row's gathers
-            const uint64_t nlo = ld_stream_u64(P.row_off + vn, sp), nhi = ld_stream_u64(P.row_off + vn + 1, sp);
-            const uint2 nri = ld_stream_u2(P.rowinfo + vn, sp);
-            double no[W];
-            load_prev(vn, no);
-            double acc[W];
+            };
+            uint32_t v = r0 + i;
+            uint2 ri = ld_stream_u2(P.rowinfo + v, sp);
+            double o[W];
+            load_prev(v, o);
+            for (;;) {
+                const uint32_t in = i + ES;
+                const bool more = in < R;
+                const uint32_t vn = r0 + (more ? in : i);
+                // next row's info and previous ranks, in flight during this row's gathers
+                const uint2 nri = ld_stream_u2(P.rowinfo + vn, sp);
+                double no[W];
+                load_prev(vn, no);
+                double acc[W];
 #pragma unroll
-            for (int w = 0; w < W; ++w) acc[w] = 0.0;
-            const uint32_t* __restrict__ cb = P.col + (lo & ~3ull);
-            const uint32_t off0 = (uint32_t)(lo & 3ull);
-            const uint32_t ne = (uint32_t)(hi - lo) + off0;
-            for (uint32_t q = 0; q < ne; q += 8) {
-                const uint4 a = ld_stream_u4(cb + q, sp);
-                const uint4 b = ld_stream_u4(cb + q + 4, sp); // in bounds: colidx is padded by 16
-                const uint32_t us[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-                // valid positions of this 8-edge window as a bit mask: one
-                // predicate per gather instead of a compare chain
-                const uint32_t lo_b = q < off0 ? off0 - q : 0u;
-                const uint32_t hi_b = min(8u, ne - q);
-                const uint32_t vb = ok ? (((1u << hi_b) - 1u) & ~((1u << lo_b) - 1u)) : 0u;
-                double vals[8][W];
+                for (int w = 0; w < W; ++w) acc[w] = 0.0;
+                const uint32_t lo = (uint32_t)(s_off[i] - e0), hi = (uint32_t)(s_off[i + 1] - e0);
+                for (uint32_t q = lo; q < hi; q += 8) {
+                    const uint32_t nv = min(8u, hi - q);
+                    const uint32_t vb = ok ? ((1u << nv) - 1u) : 0u; // valid positions as a bit mask
+                    double vals[8][W];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
+                    for (int j = 0; j < 8; ++j) {
 #pragma unroll
-                    for (int w = 0; w < W; ++w) vals[j][w] = 0.0;
-                    if (vb & (1u << j)) load_w<W>(cpl + (size_t)us[j] * KS, vals[j]);
+                        for (int w = 0; w < W; ++w) vals[j][w] = 0.0;
+                        if (vb & (1u << j)) load_w<W>(cpl + (size_t)s_col[q + j] * KS, vals[j]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+#pragma unroll
+                        for (int w = 0; w < W; ++w) acc[w] += vals[j][w];
                 }
+                epilogue_with<false>(v, slice, acc, ri, o);
+                if (!more) break;
+                i = in;
+                v = vn;
+                ri = nri;
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-#pragma unroll
-                    for (int w = 0; w < W; ++w) acc[w] += vals[j][w];
+                for (int w = 0; w < W; ++w) o[w] = no[w];
             }
-            epilogue_with<false>(v, slice, acc, ri, o);
-            if (!more) break;
-            i = in;
-            v = vn;
-            lo = nlo;
-            hi = nhi;
-            ri = nri;
-#pragma unroll
-            for (int w = 0; w < W; ++w) o[w] = no[w];
         }
+        __syncwarp(); // the next task reuses the stage
     }
 
     // ---- rows with no in-edges: rank = c0; write c0/d for rows with out-edges,
@@ -888,11 +890,12 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
 
     // dynamic smem: [kWarps][SMEM_WARP + ASYNC_WARP] staged gathers, then the per-thread
     // partial columns when W >= 6
-    constexpr int ASYNC_WARP = 0; // (LDGSTS-staged packed gathers measured no faster)
-    constexpr int PER_WARP = C::SMEM_WARP + ASYNC_WARP;
-    // the packed + empty instance of a split iteration keeps its partials in
-    // shared memory: the registers go to gathers in flight
-    constexpr bool SMEMP = (W >= 6) || (PATHS == 2 && C::KP > 1);
+    // K > 1 packed runs (PATHS == 2): staged row offsets + colidx, in doubles
+    constexpr int PACK_WARP = (PATHS == 2 && !C::STAGED) ? kPackOff + (2 * WIN + 8) / 2 : 0;
+    constexpr int PER_WARP = C::SMEM_WARP + PACK_WARP;
+    // the instances of a split iteration keep their partials in shared
+    // memory: the registers go to gathers in flight
+    constexpr bool SMEMP = (W >= 6) || (PATHS != 3 && C::KP > 1);
     Warp<LG, W, WIN, QJ_, QM, KS_, SMEMP> w(P, s_iter & 1, lane, s_alpha, s_c0, s_active,
                                      s_dyn + (size_t)kWarps * PER_WARP, tid);
     double* sv = s_dyn + (size_t)warp * PER_WARP;
