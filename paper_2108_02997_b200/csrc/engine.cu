@@ -239,6 +239,25 @@ inline LaneCfg lane_cfg(int K, bool all_q) {
     return lane_cfg_t<3>(K, all_q);
 }
 
+// Lane-width modes of a K > 1 run (Params::mode_id): the same row stride KS,
+// window and task tables, a lane group of kp/2 threads.  Returns false when
+// (KS, kp) has no instance.
+// Lane-width modes of a K > 1 run (Params::mode_id): the same window and task
+// tables, a lane group of kp/2 threads; a narrow mode's contribution rows hold
+// just its kp lanes (KS = kp), the widest mode's the run's full stride.
+// Returns false when (KS, kp) has no instance.
+template <int PATHS>
+bool mode_cfg(int KS, int kp, bool all_q, LaneCfg& out) {
+    switch (KS * 100 + kp) {
+    case 202: out = wide_cfg<1, 2, 128, 4, 2, PATHS>(all_q); return true;
+    case 404: out = wide_cfg<2, 2, 128, 4, 4, PATHS>(all_q); return true;
+    case 808: out = wide_cfg<4, 2, 128, 4, 8, PATHS>(all_q); return true;
+    case 1216: out = wide_cfg<8, 2, 128, 4, 12, PATHS>(all_q); return true;
+    case 1616: out = wide_cfg<8, 2, 128, 4, 16, PATHS>(all_q); return true;
+    default: return false;
+    }
+}
+
 void launch_init(const LaneCfg& c, const Params& P, uint32_t ndangling, cudaStream_t st) {
     const unsigned grid = (unsigned)std::min<uint64_t>((P.n + kNT - 1) / kNT, 148ull * 16);
     switch (c.KS) {
@@ -263,14 +282,24 @@ using namespace prgpu;
 struct prgpu_session {
     prgpu_graph* g = nullptr;
     int K = 1, KP = 1, max_iter = 500;
-    LaneCfg cfg{};   // the (first) pull kernel
-    LaneCfg cfg2{};  // split iteration: the packed + empty kernel
-    bool split = false;
-    Params P1{};     // split iteration: the hub-chunk kernel's parameters
-    size_t smem1 = 0, smem2 = 0;
+    LaneCfg cfg{};   // base configuration (window, stride, lanes per row; multi-GPU kernels)
+    // the kernels of one iteration, in launch order: one pull kernel, or per
+    // lane-width mode a hub-chunk kernel and a packed + empty kernel (only
+    // the mode selected by the previous finalizer does work)
+    struct Launch {
+        KernelFn fn;
+        Params P;
+        size_t smem;
+        bool repack; // repack_kernel(P, nsrc) instead of a pull kernel
+    };
+    std::vector<Launch> launches;
+    int mode0 = 0;   // lane-width mode of the first iteration
+    bool all_q = true; // every partial quantity tracked (not only the L1 stopping rule)
     Params P{};
     Stream stream;
     DevBuf<double> rank, contrib, partials, trace, ref, chunk_acc;
+    DevBuf<double> mode_contrib[kMaxModes]; // narrow modes' contribution buffers (after `stream`:
+                                            // freed on it before it is destroyed)
     DevBuf<LaneState> lanes;
     DevBuf<GlobalState> gs;
     DevBuf<uint32_t> chunk_row, chunk_first, packed_r0;
@@ -416,7 +445,7 @@ void build_tasks(prgpu_session* s) {
     }
     // rows with no in-edges: only those with out-edges need a task (their next
     // contribution c0/d), unless the reference trace needs every row
-    const uint32_t er = 8 * (32 / s->cfg2.LG); // empty tasks run in the (second) kernel
+    const uint32_t er = 8 * (32 / s->cfg.LG);
     const uint32_t iso_begin = std::max(phi, n - count_isolated(g, st));
     const uint32_t n_empty_rows = (s->P.ref ? n : iso_begin) - phi;
     s->P.iso_begin = iso_begin;
@@ -429,6 +458,7 @@ void build_tasks(prgpu_session* s) {
     P.n_chunk = (uint32_t)n_chunk;
     P.n_packed = (uint32_t)n_packed;
     P.n_empty_tasks = (n_empty_rows + er - 1) / er;
+    P.er = er;
     P.empty_begin = phi;
     P.task_begin = 0;
     P.task_end = P.n_chunk + P.n_packed + P.n_empty_tasks;
@@ -547,23 +577,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         const uint32_t mask = p->stop_mask ? p->stop_mask : (1u << p->norm);
         const bool l1_only = mask == 1u && p->norm == PRGPU_NORM_L1 && !p->ref_ranks;
         s->cfg = lane_cfg(s->K, !l1_only);
-        s->cfg2 = s->cfg;
-        // split iteration (hub-chunk kernel, then packed + empty kernel) for
-        // the single-GPU run; PRGPU_SPLIT=0 or a tuning variant: one kernel
-        const char* sp = std::getenv("PRGPU_SPLIT");
-        // (measured: -2% at C2 K=11, +3% at K=1 on the same graph: K > 1 only)
-        s->split = nranks == 0 && s->K > 1 && !(sp && std::atoi(sp) == 0) && variant() == 0;
-        if (s->split) {
-            s->cfg = lane_cfg_t<1>(s->K, !l1_only);
-            s->cfg2 = lane_cfg_t<2>(s->K, !l1_only);
-            if (const char* v2 = std::getenv("PRGPU_VARIANT2")) { // tuning only
-                const int var2 = std::atoi(v2);
-                if (s->K > 8 && s->K <= 12 && var2 == 1) s->cfg2 = wide_cfg<16, 1, 128, 4, 12, 2>(!l1_only);
-                if (s->K > 8 && s->K <= 12 && var2 == 2) s->cfg2 = wide_cfg<8, 2, 128, 5, 12, 2>(!l1_only);
-                if (s->K > 8 && s->K <= 12 && var2 == 3) s->cfg2 = wide_cfg<16, 1, 128, 5, 12, 2>(!l1_only);
-                if (s->K > 8 && s->K <= 12 && var2 == 4) s->cfg2 = wide_cfg<8, 2, 128, 3, 12, 2>(!l1_only);
-            }
-        }
+        s->all_q = !l1_only;
     }
     s->KP = s->cfg.KP();
     s->max_iter = p->max_iterations;
@@ -605,7 +619,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     }
     PRGPU_CUDA(cudaMemcpyAsync(s->lanes.p, s->lanes_host.data(), K * sizeof(LaneState),
                                cudaMemcpyHostToDevice, st));
-    GlobalState gsh{0, 1, 0u, s->max_iter};
+    GlobalState gsh{0, 1, 0u, s->max_iter, s->mode0, s->mode0};
     PRGPU_CUDA(cudaMemcpyAsync(s->gs.p, &gsh, sizeof(gsh), cudaMemcpyHostToDevice, st));
 
     if (p->ref_ranks) {
@@ -685,29 +699,101 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         const uint64_t want = (tasks + kWarps * 4 - 1) / (kWarps * 4);
         return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)dev_sms * per_sm, want));
     };
-    if (s->split && P.n_chunk == 0) s->split = false; // no hub rows: the packed + empty kernel alone
-    uint32_t G1 = 0;
-    if (s->split) {
-        G1 = grid_for_cfg(s->cfg, P.n_chunk, s->smem1);
-        P.task_begin = P.n_chunk;
-        P.G = grid_for_cfg(s->cfg2, (uint64_t)P.task_end - P.task_begin, s->smem2);
-    } else { // one kernel: cfg2 (== cfg unless the split was dropped for lack of hub rows)
-        P.G = grid_for_cfg(s->cfg2, (uint64_t)P.task_end - P.task_begin, s->smem2);
+    // the iteration's kernels.  Single-GPU runs with K > 1 get one kernel
+    // pair per lane-width mode (narrowest first): a hub-chunk kernel that only
+    // leaves CTA partials and a packed + empty kernel that finalizes; once the
+    // live lanes fit a narrower mode the wide pairs exit at once.  Multi-GPU
+    // partitions and K = 1 run the one base kernel.
+    std::vector<std::pair<int, std::pair<LaneCfg, LaneCfg>>> modes; // kp, (chunk, packed)
+    {
+        const char* sp = std::getenv("PRGPU_SPLIT");   // =0: base kernel only (tuning)
+        const char* mm = std::getenv("PRGPU_MODES");   // =0: widest mode only (tuning)
+        const bool modal = nranks == 0 && s->K > 1 && !(sp && std::atoi(sp) == 0) && variant() == 0;
+        if (modal) {
+            for (int kp = 2; kp <= s->cfg.KP(); kp *= 2) {
+                if (kp < s->cfg.KP() && mm && std::atoi(mm) == 0) continue;
+                LaneCfg a, b;
+                const int ks = kp == s->cfg.KP() ? s->cfg.KS : kp;
+                if (mode_cfg<1>(ks, kp, s->all_q, a) && mode_cfg<2>(ks, kp, s->all_q, b))
+                    modes.push_back({kp, {a, b}});
+            }
+            if (modes.empty() || modes.back().first != s->cfg.KP()) modes.clear(); // no instances: base kernel
+        }
     }
-    const uint32_t G = P.G;
-    P.gtot = G1 + G;
-    P.pcol0 = G1;
+    P.nmodes = modes.empty() ? 1 : (int)modes.size();
+    for (int m = 0; m < kMaxModes; ++m)
+        P.mode_kp[m] = modes.empty() ? KP : (m < (int)modes.size() ? modes[m].first : KP);
+    s->mode0 = 0;
+    for (int m = P.nmodes - 1; m >= 0; --m)
+        if (P.mode_kp[m] > K - 1) s->mode0 = m; // narrowest mode covering every lane
     P.no_finalize = 0;
-    s->partials.alloc((size_t)kNQ * KP * P.gtot);
-    P.partials = s->partials.p;
-    if (s->split) {
-        s->P1 = P;
-        s->P1.task_begin = 0;
-        s->P1.task_end = P.n_chunk;
-        s->P1.G = G1;
-        s->P1.pcol0 = 0;
-        s->P1.no_finalize = 1;
+    // contribution buffers per mode: the widest mode uses the run's buffers
+    for (int m = 0; m < kMaxModes; ++m) {
+        P.mode_cbase[m] = P.cbase;
+        P.mode_cold_off[m][0] = P.cold_off[0];
+        P.mode_cold_off[m][1] = P.cold_off[1];
+        P.mode_ks[m] = s->cfg.KS;
     }
+    for (int m = 0; m + 1 < (int)modes.size(); ++m) {
+        const int kp = modes[m].first;
+        s->mode_contrib[m].alloc(2 * nsrc * kp);
+        PRGPU_CUDA(cudaMemsetAsync(s->mode_contrib[m].p, 0, 2 * nsrc * kp * sizeof(double), st));
+        P.mode_cbase[m] = s->mode_contrib[m].p;
+        P.mode_cold_off[m][0] = 0;
+        P.mode_cold_off[m][1] = nsrc;
+        P.mode_ks[m] = kp;
+    }
+    size_t part_cols = 0; // partials: max over modes of kNQ * kp * columns
+    s->launches.clear();
+    if (modes.empty()) {
+        size_t smem = 0;
+        P.G = grid_for_cfg(s->cfg, (uint64_t)P.task_end - P.task_begin, smem);
+        P.gtot = P.G;
+        P.pcol0 = 0;
+        P.mode_id = 0;
+        s->launches.push_back({s->cfg.fn, P, smem, false});
+        part_cols = (size_t)kNQ * KP * P.gtot;
+    } else {
+        const uint32_t T1 = P.n_chunk, T3 = P.task_end;
+        for (int m = 0; m < (int)modes.size(); ++m) {
+            const LaneCfg& A = modes[m].second.first;
+            const LaneCfg& B = modes[m].second.second;
+            size_t sa = 0, sb = 0;
+            const uint32_t GA = T1 ? grid_for_cfg(A, T1, sa) : 0;
+            const uint32_t GB = grid_for_cfg(B, T3 - T1, sb);
+            Params PM = P;
+            PM.mode_id = m;
+            PM.cbase = P.mode_cbase[m];
+            PM.cold_off[0] = P.mode_cold_off[m][0];
+            PM.cold_off[1] = P.mode_cold_off[m][1];
+            if (m + 1 < (int)modes.size()) { // narrow mode: repack on entry
+                PM.G = (uint32_t)dev_sms * 8;
+                s->launches.push_back({nullptr, PM, 0, true});
+            }
+            Params PA = PM, PB = PM;
+            PA.mode_id = PB.mode_id = m;
+            PA.gtot = PB.gtot = GA + GB;
+            if (GA) {
+                PA.task_begin = 0;
+                PA.task_end = T1;
+                PA.G = GA;
+                PA.pcol0 = 0;
+                PA.no_finalize = 1;
+                s->launches.push_back({A.fn, PA, sa, false});
+            }
+            PB.task_begin = T1;
+            PB.task_end = T3;
+            PB.G = GB;
+            PB.pcol0 = GA;
+            s->launches.push_back({B.fn, PB, sb, false});
+            part_cols = std::max(part_cols, (size_t)kNQ * modes[m].first * (GA + GB));
+        }
+    }
+    s->partials.alloc(part_cols);
+    P.partials = s->partials.p;
+    for (auto& l : s->launches) l.P.partials = s->partials.p;
+    P.G = s->launches.back().P.G;
+    P.gtot = s->launches.back().P.gtot;
 
     PRGPU_CUDA(cudaEventCreate(&s->e0));
     PRGPU_CUDA(cudaEventCreate(&s->e1));
@@ -728,32 +814,23 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         cudaGraphNode_t cnode;
         PRGPU_CUDA(cudaGraphAddNode(&cnode, s->graph, nullptr, 0, &cp));
         cudaGraph_t body = cp.conditional.phGraph_out[0];
-        cudaGraphNode_t k1node = nullptr;
-        if (s->split) {
-            Params P1 = s->P1;
-            P1.use_cond = 1;
-            P1.cond = h;
-            cudaKernelNodeParams kp1 = {};
-            kp1.func = (void*)s->cfg.fn;
-            kp1.gridDim = dim3(P1.G);
-            kp1.blockDim = dim3(kNT);
-            kp1.sharedMemBytes = (unsigned)s->smem1;
-            void* args1[] = {&P1};
-            kp1.kernelParams = args1;
-            PRGPU_CUDA(cudaGraphAddKernelNode(&k1node, body, nullptr, 0, &kp1));
+        cudaGraphNode_t prev = nullptr;
+        uint32_t nsrc32 = (uint32_t)nsrc;
+        for (const auto& l : s->launches) {
+            Params PG = l.P;
+            PG.use_cond = 1;
+            PG.cond = h;
+            cudaKernelNodeParams kp = {};
+            kp.func = l.repack ? (void*)repack_kernel : (void*)l.fn;
+            kp.gridDim = dim3(PG.G);
+            kp.blockDim = dim3(kNT);
+            kp.sharedMemBytes = (unsigned)l.smem;
+            void* args[] = {&PG, &nsrc32};
+            kp.kernelParams = args;
+            cudaGraphNode_t node;
+            PRGPU_CUDA(cudaGraphAddKernelNode(&node, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+            prev = node;
         }
-        Params PG = P;
-        PG.use_cond = 1;
-        PG.cond = h;
-        cudaKernelNodeParams kp = {};
-        kp.func = (void*)s->cfg2.fn;
-        kp.gridDim = dim3(G);
-        kp.blockDim = dim3(kNT);
-        kp.sharedMemBytes = (unsigned)s->smem2;
-        void* args[] = {&PG};
-        kp.kernelParams = args;
-        cudaGraphNode_t knode;
-        PRGPU_CUDA(cudaGraphAddKernelNode(&knode, body, k1node ? &k1node : nullptr, k1node ? 1 : 0, &kp));
         PRGPU_CUDA(cudaGraphInstantiate(&s->exec, s->graph, 0));
         s->use_graph = true;
     }
@@ -804,7 +881,7 @@ void session_init(prgpu_session* s) {
     // pageable host sources: the copies are staged before the call returns
     PRGPU_CUDA(cudaMemcpyAsync(s->lanes.p, s->lanes_host.data(), s->K * sizeof(LaneState),
                                cudaMemcpyHostToDevice, s->cur()));
-    GlobalState gsh{0, 1, 0u, s->max_iter};
+    GlobalState gsh{0, 1, 0u, s->max_iter, s->mode0, s->mode0};
     PRGPU_CUDA(cudaMemcpyAsync(s->gs.p, &gsh, sizeof(gsh), cudaMemcpyHostToDevice, s->cur()));
     launch_init(s->cfg, s->P, s->g->ndangling, s->cur());
     s->host_iter = 0;
@@ -812,16 +889,14 @@ void session_init(prgpu_session* s) {
 }
 
 void launch_pull(prgpu_session* s) {
-    if (s->split) {
-        Params P1 = s->P1;
-        P1.use_cond = 0;
-        s->cfg.fn<<<P1.G, kNT, s->smem1, s->cur()>>>(P1);
-        PRGPU_LAUNCHED("pull_kernel (hub chunks)");
+    const uint32_t nsrc = std::max<uint32_t>(s->g->nsrc, 1);
+    for (const auto& l : s->launches) {
+        Params P = l.P;
+        P.use_cond = 0;
+        if (l.repack) repack_kernel<<<P.G, kNT, 0, s->cur()>>>(P, nsrc);
+        else l.fn<<<P.G, kNT, l.smem, s->cur()>>>(P);
+        PRGPU_LAUNCHED("pull_kernel");
     }
-    Params P = s->P;
-    P.use_cond = 0;
-    s->cfg2.fn<<<P.G, kNT, s->smem2, s->cur()>>>(P);
-    PRGPU_LAUNCHED("pull_kernel");
 }
 
 int read_any_active(prgpu_session* s) {

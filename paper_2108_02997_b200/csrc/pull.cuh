@@ -82,7 +82,11 @@ struct GlobalState {
     int any_active;
     unsigned int counter;
     int max_iter;
+    int mode;   // lane-width mode of the next iteration (see Params::mode_id)
+    int layout; // mode whose contribution buffer holds the current contributions
 };
+
+constexpr int kMaxModes = 4;
 
 struct Params {
     uint32_t n, K;
@@ -129,6 +133,19 @@ struct Params {
     // partials is [kNQ*KP][gtot]; this kernel's CTAs own columns pcol0 + blockIdx.x
     uint32_t pcol0, gtot;
     int no_finalize;
+    // lane-width modes: one kernel pair per mode m covering lanes [0, mode_kp[m]);
+    // an instance runs only when gs->mode == mode_id, and the finalizer picks
+    // the narrowest mode covering the highest still-active lane for the next
+    // iteration (lanes are stored slowest first, so the live ones are a prefix)
+    int mode_id, nmodes;
+    int mode_kp[kMaxModes];
+    // each mode gathers from its own contribution buffers, rows of mode_ks
+    // doubles (narrow modes: just their lanes, so the table is small enough to
+    // stay in L2); repack_kernel converts on a mode change
+    double* mode_cbase[kMaxModes];
+    uint64_t mode_cold_off[kMaxModes][2];
+    int mode_ks[kMaxModes];
+    uint32_t er; // rows per empty task
 };
 
 // ---- L2 residency control -------------------------------------------------------
@@ -378,7 +395,7 @@ struct Warp {
 #pragma unroll
             for (int w = 0; w < W; ++w) o[w] = 0.0;
             if (lane_ok(sl) && !(P.skip_mask & 16)) {
-                const double* rr = rp + (size_t)v * KS + sl * W;
+                const double* rr = rp + (size_t)v * P.ks + sl * W; // rank rows: stride ks
                 if constexpr (W % 2 == 0) {
 #pragma unroll
                     for (int w = 0; w < W; w += 2) {
@@ -421,7 +438,7 @@ struct Warp {
             }
         }
         if (any && !(P.skip_mask & 8)) { // frozen lanes keep their final value: masked stores
-            double* rw = rn + (size_t)v * KS + sl * W;
+            double* rw = rn + (size_t)v * P.ks + sl * W;
             if constexpr (W % 2 == 0) {
 #pragma unroll
                 for (int w = 0; w < W; w += 2) {
@@ -711,7 +728,7 @@ struct Warp {
 #pragma unroll
                 for (int w = 0; w < W; ++w) o[w] = 0.0;
                 if (lok) {
-                    const double* rr = rp + (size_t)v * KS + slice * W;
+                    const double* rr = rp + (size_t)v * P.ks + slice * W;
                     if constexpr (W % 2 == 0) {
 #pragma unroll
                         for (int w = 0; w < W; w += 2) {
@@ -772,11 +789,10 @@ struct Warp {
     //      and (sweep mode) the L1 distance to the reference -------------------------
     __device__ void empty_task(uint32_t t) {
         const uint64_t sp = stream_policy(P);
-        const uint32_t base = P.empty_begin + t * C::ER;
+        const uint32_t base = P.empty_begin + t * P.er;
+        const uint32_t end = min(base + P.er, P.n);
 #pragma unroll 2
-        for (int rd = 0; rd < 8; ++rd) {
-            const uint32_t v = base + rd * ES + slot;
-            if (v >= P.n) break;
+        for (uint32_t v = base + slot; v < end; v += ES) {
             const uint2 ri = ld_stream_u2(P.rowinfo + v, sp);
             double cv[W];
             bool any = false;
@@ -803,7 +819,7 @@ template <int KP, int QM>
 __device__ void finalize_lanes(const Params& P, const double* s_tot, const double* s_c0,
                                const int* s_active, int iter) {
     const int tid = threadIdx.x;
-    if (tid < (int)P.K && s_active[tid]) {
+    if (tid < (int)P.K && tid < KP && s_active[tid]) { // lanes >= KP are frozen in this mode
         const int k = tid;
         LaneState& L = P.lanes[k];
         // rows with no in-edges all moved from prev_empty to c0 (exactly); add
@@ -851,8 +867,14 @@ __device__ void finalize_lanes(const Params& P, const double* s_tot, const doubl
     }
     __syncthreads();
     if (tid == 0) {
-        int any = 0;
-        for (uint32_t k = 0; k < P.K; ++k) any |= P.lanes[k].active;
+        int any = 0, top = -1;
+        for (uint32_t k = 0; k < P.K; ++k)
+            if (P.lanes[k].active) { any = 1; top = (int)k; }
+        int mode = P.nmodes - 1; // narrowest mode that still covers every live lane
+        for (int m = P.nmodes - 1; m >= 0; --m)
+            if (P.mode_kp[m] > top) mode = m;
+        P.gs->mode = mode;
+        if (!P.no_finalize) P.gs->layout = P.mode_id; // this iteration wrote our buffer
         P.gs->iter = iter + 1;
         P.gs->any_active = any;
         P.gs->counter = 0;
@@ -877,7 +899,8 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         s_iter = P.gs->iter;
-        s_flag = P.gs->any_active;
+        // not this instance's lane-width mode, or a speculative launch after convergence
+        s_flag = P.gs->any_active && P.gs->mode == P.mode_id;
     }
     if (tid < KP) {
         const bool real = tid < (int)P.K;
@@ -886,7 +909,7 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
         s_active[tid] = real ? P.lanes[tid].active : 0;
     }
     __syncthreads();
-    if (!s_flag) return; // speculative launch after convergence (host-loop mode)
+    if (!s_flag) return;
 
     // dynamic smem: [kWarps][SMEM_WARP + ASYNC_WARP] staged gathers, then the per-thread
     // partial columns when W >= 6
@@ -984,6 +1007,31 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
         return;
     }
     finalize_lanes<KP, QM>(P, s_tot, s_c0, s_active, s_iter);
+}
+
+// Mode change (Params::mode_id): copy the current contributions (parity of
+// this iteration) of lanes [0, mode_ks[m]) from the buffer of the mode that
+// wrote them into this mode's narrower buffer.  A no-op launch otherwise.
+__global__ void __launch_bounds__(kNT) repack_kernel(const Params P, uint32_t nsrc) {
+    __shared__ int s_go, s_from, s_par;
+    if (threadIdx.x == 0) {
+        const int mode = P.gs->mode, from = P.gs->layout;
+        s_go = P.gs->any_active && mode == P.mode_id && from != P.mode_id;
+        s_from = from;
+        s_par = P.gs->iter & 1;
+    }
+    __syncthreads();
+    if (!s_go) return;
+    const int m = P.mode_id, f = s_from, par = s_par;
+    const int ks_t = P.mode_ks[m], ks_f = P.mode_ks[f];
+    const double* __restrict__ src = P.mode_cbase[f] + P.mode_cold_off[f][par] * ks_f;
+    double* __restrict__ dst = P.mode_cbase[m] + P.mode_cold_off[m][par] * ks_t;
+    const uint64_t total = (uint64_t)nsrc * ks_t;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t u = i / ks_t, k = i - u * ks_t;
+        dst[i] = src[u * ks_f + k];
+    }
 }
 
 // Multi-GPU finalize (one CTA, identical on every rank): the ranks' partial
