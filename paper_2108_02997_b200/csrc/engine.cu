@@ -249,6 +249,9 @@ inline LaneCfg lane_cfg(int K, bool all_q) {
 template <int PATHS>
 bool mode_cfg(int KS, int kp, bool all_q, LaneCfg& out) {
     switch (KS * 100 + kp) {
+    case 101:
+        out = all_q ? mk_cfg<1, 1, 128, 2, 3, kQmAll, 1, PATHS>() : mk_cfg<1, 1, 128, 2, 3, kQmL1, 1, PATHS>();
+        return true;
     case 202: out = wide_cfg<1, 2, 128, 4, 2, PATHS>(all_q); return true;
     case 404: out = wide_cfg<2, 2, 128, 4, 4, PATHS>(all_q); return true;
     case 808: out = wide_cfg<4, 2, 128, 4, 8, PATHS>(all_q); return true;
@@ -710,7 +713,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         const char* mm = std::getenv("PRGPU_MODES");   // =0: widest mode only (tuning)
         const bool modal = nranks == 0 && s->K > 1 && !(sp && std::atoi(sp) == 0) && variant() == 0;
         if (modal) {
-            for (int kp = 2; kp <= s->cfg.KP(); kp *= 2) {
+            for (int kp = 1; kp <= s->cfg.KP(); kp *= 2) {
                 if (kp < s->cfg.KP() && mm && std::atoi(mm) == 0) continue;
                 LaneCfg a, b;
                 const int ks = kp == s->cfg.KP() ? s->cfg.KS : kp;
@@ -814,12 +817,37 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         cudaGraphNode_t cnode;
         PRGPU_CUDA(cudaGraphAddNode(&cnode, s->graph, nullptr, 0, &cp));
         cudaGraph_t body = cp.conditional.phGraph_out[0];
-        cudaGraphNode_t prev = nullptr;
+        // body: per lane-width mode an IF node (narrowest first) around that
+        // mode's kernels; only the mode armed by the previous finalizer runs
         uint32_t nsrc32 = (uint32_t)nsrc;
+        const int nm = P.nmodes;
+        cudaGraphConditionalHandle mh[kMaxModes] = {};
+        cudaGraph_t mbody[kMaxModes] = {};
+        cudaGraphNode_t prev_if = nullptr;
+        if (nm > 1) {
+            for (int m = 0; m < nm; ++m) {
+                PRGPU_CUDA(cudaGraphConditionalHandleCreate(&mh[m], body, m == s->mode0 ? 1u : 0u,
+                                                            cudaGraphCondAssignDefault));
+                cudaGraphNodeParams ip = {};
+                ip.type = cudaGraphNodeTypeConditional;
+                ip.conditional.handle = mh[m];
+                ip.conditional.type = cudaGraphCondTypeIf;
+                ip.conditional.size = 1;
+                cudaGraphNode_t inode;
+                PRGPU_CUDA(cudaGraphAddNode(&inode, body, prev_if ? &prev_if : nullptr, prev_if ? 1 : 0, &ip));
+                mbody[m] = ip.conditional.phGraph_out[0];
+                prev_if = inode;
+            }
+        }
+        cudaGraphNode_t prev[kMaxModes] = {};
         for (const auto& l : s->launches) {
             Params PG = l.P;
             PG.use_cond = 1;
             PG.cond = h;
+            PG.use_mode_cond = nm > 1;
+            for (int m = 0; m < kMaxModes; ++m) PG.mode_cond[m] = mh[m];
+            const int m = nm > 1 ? PG.mode_id : 0;
+            cudaGraph_t tgt = nm > 1 ? mbody[m] : body;
             cudaKernelNodeParams kp = {};
             kp.func = l.repack ? (void*)repack_kernel : (void*)l.fn;
             kp.gridDim = dim3(PG.G);
@@ -828,8 +856,8 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
             void* args[] = {&PG, &nsrc32};
             kp.kernelParams = args;
             cudaGraphNode_t node;
-            PRGPU_CUDA(cudaGraphAddKernelNode(&node, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
-            prev = node;
+            PRGPU_CUDA(cudaGraphAddKernelNode(&node, tgt, prev[m] ? &prev[m] : nullptr, prev[m] ? 1 : 0, &kp));
+            prev[m] = node;
         }
         PRGPU_CUDA(cudaGraphInstantiate(&s->exec, s->graph, 0));
         s->use_graph = true;

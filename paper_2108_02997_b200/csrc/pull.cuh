@@ -86,7 +86,7 @@ struct GlobalState {
     int layout; // mode whose contribution buffer holds the current contributions
 };
 
-constexpr int kMaxModes = 4;
+constexpr int kMaxModes = 5;
 
 struct Params {
     uint32_t n, K;
@@ -145,6 +145,9 @@ struct Params {
     double* mode_cbase[kMaxModes];
     uint64_t mode_cold_off[kMaxModes][2];
     int mode_ks[kMaxModes];
+    // CUDA-graph runs: one IF node per mode; the finalizer arms the next mode's
+    int use_mode_cond;
+    cudaGraphConditionalHandle mode_cond[kMaxModes];
     uint32_t er; // rows per empty task
 };
 
@@ -874,6 +877,8 @@ __device__ void finalize_lanes(const Params& P, const double* s_tot, const doubl
         for (int m = P.nmodes - 1; m >= 0; --m)
             if (P.mode_kp[m] > top) mode = m;
         P.gs->mode = mode;
+        if (P.use_cond && P.use_mode_cond)
+            for (int m = 0; m < P.nmodes; ++m) cudaGraphSetConditional(P.mode_cond[m], m == mode ? 1u : 0u);
         if (!P.no_finalize) P.gs->layout = P.mode_id; // this iteration wrote our buffer
         P.gs->iter = iter + 1;
         P.gs->any_active = any;
