@@ -713,14 +713,15 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         const char* mm = std::getenv("PRGPU_MODES");   // =0: widest mode only (tuning)
         const bool modal = nranks == 0 && s->K > 1 && !(sp && std::atoi(sp) == 0) && variant() == 0;
         if (modal) {
-            for (int kp = 1; kp <= s->cfg.KP(); kp *= 2) {
-                if (kp < s->cfg.KP() && mm && std::atoi(mm) == 0) continue;
+            const int wide = s->cfg.KP(); // (measured: 12 lanes as 4 threads x 3 lost 30%)
+            for (int kp = 1; kp <= wide; kp *= 2) {
+                if (kp < wide && mm && std::atoi(mm) == 0) continue;
                 LaneCfg a, b;
-                const int ks = kp == s->cfg.KP() ? s->cfg.KS : kp;
+                const int ks = kp == wide ? s->cfg.KS : kp;
                 if (mode_cfg<1>(ks, kp, s->all_q, a) && mode_cfg<2>(ks, kp, s->all_q, b))
                     modes.push_back({kp, {a, b}});
             }
-            if (modes.empty() || modes.back().first != s->cfg.KP()) modes.clear(); // no instances: base kernel
+            if (modes.empty() || modes.back().first != wide) modes.clear(); // no instances: base kernel
         }
     }
     P.nmodes = modes.empty() ? 1 : (int)modes.size();
