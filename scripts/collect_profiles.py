@@ -54,20 +54,17 @@ def main(tag):
     with open(os.path.join(PROF, f"{tag}_launches.md"), "w") as f:
         f.write("\n".join(md))
     rep = os.path.join(OUT, f"{tag}_c2_pull.ncu-rep")
-    s = summary(rep)[0]
+    kernels = summary(rep)  # the kernels of one all-lanes-live iteration (hub chunks, packed + empty)
     with open(os.path.join(PROF, f"{tag}_ncu_pull.json"), "w") as f:
-        json.dump(s, f, indent=1)
+        json.dump(kernels if len(kernels) > 1 else kernels[0], f, indent=1)
 
-    def val(k):
-        return float(s[k].split()[0])
-
-    def to_bytes(k):
+    def to_bytes(s, k):
         v, u = s[k].split()[:2]
         return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
-    traffic = to_bytes("dram__bytes_read.sum") + to_bytes("dram__bytes_write.sum")
+    traffic = sum(to_bytes(s, "dram__bytes_read.sum") + to_bytes(s, "dram__bytes_write.sum") for s in kernels)
     with open(os.path.join(PROF, "traffic.json"), "w") as f:
-        json.dump({"c2": traffic, "source": f"profiles/{tag}_ncu_pull.json (one ncu --set full "
-                   "capture of pull_kernel at C2, all 11 lanes active)"}, f, indent=1)
+        json.dump({"c2": traffic, "source": f"profiles/{tag}_ncu_pull.json (ncu --set full of the "
+                   "pull kernels of one C2 iteration, all 11 lanes active; summed)"}, f, indent=1)
     print("profiles written; pull traffic per launch", traffic / 1e9, "GB")
 
 
