@@ -277,3 +277,24 @@ def test_c4_rmat26_linf(prl, oracle):
     assert np.max(np.abs(r.ranks[idx] - arr["sample"])) <= RANK_TOL
     assert np.max(np.abs(r.ranks[arr["top_idx"]] - arr["top"])) <= RANK_TOL
     assert abs(float(np.sum(r.ranks.astype(np.longdouble))) - float(arr["total"])) <= 1e-9
+
+
+@pytest.mark.parametrize("K", [2, 3, 5, 8, 9, 12, 13, 16])
+def test_batched_lane_modes_vs_oracle(prl, oracle, K):
+    """Batched runs of every lane-width family, lanes freezing in an order the
+    slowest-first storage does not predict (per-lane tolerances), so the run
+    walks through the narrow modes and their repacks; every lane must match
+    the oracle's single run: iterations (+-1 rule) and ranks <= 1e-10."""
+    rng = np.random.default_rng(1000 + K)
+    n, pairs = oracle.rmat(14, 16, 0.57, 0.19, 0.19, 77)
+    h = oracle.build_csr_handle(n, pairs)
+    g = prl.generate_rmat(14, 16, 0.57, 0.19, 0.19, 77)
+    alphas = list(np.round(rng.uniform(0.3, 0.99, K), 3))
+    tols = 10.0 ** -rng.uniform(4, 10, K)
+    br = prl.pagerank_batched(g, alphas, tols, prl.NormKind.L1, 500)
+    for k in range(K):
+        want = oracle.pagerank(h, alphas[k], tols[k], "l1", 500, trace=True)
+        got = br.results[k]
+        assert iterations_match(got.iterations, want["iterations"], want["err_trace"], tols[k]), k
+        assert np.max(np.abs(got.ranks - want["ranks"])) <= RANK_TOL, k
+    oracle.free_csr(h)
