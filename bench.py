@@ -414,6 +414,48 @@ def run_partitioned(args, cfg):
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
     value = lane_its * e / (ms_per_step / 1e3) / 1e9
+    # roofline: the job's algorithmic bytes over the loop time, per GPU
+    n_src = n - int(g.info.dangling_count)
+    bytes_run = bytes_over_run(n, e, n_src, iters)
+    peak, peak_kind = measured_peak_gbs()
+    per_gpu = bytes_run / (ms_per_step / 1e3) / 1e9 / world
+    roof = {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s", "frac": per_gpu / peak,
+            "traffic": None, "peak_source": peak_kind,
+            "kernel": "pull kernels + exchange, whole loop (per GPU, aggregate bytes / N)"}
+    # e2e through the public API at N GPUs: every rank uploads the reference-layout
+    # CSR from pinned host memory, runs the partitioned solve, the ranks are
+    # gathered to the host (distributed.run_distributed(want_ranks=True))
+    e2e = None
+    if not args.no_e2e:
+        import ctypes as C
+        from paper_2108_02997_b200 import _lib
+        off = torch.from_numpy(g.in_offsets).pin_memory()
+        nbr = torch.from_numpy(g.in_neighbors).pin_memory()
+        deg = torch.from_numpy(g.out_degree).pin_memory()
+
+        def e2e_step():
+            h = C.c_void_p()
+            _lib.check(_lib.lib().prgpu_graph_from_csr(n, off.data_ptr(), nbr.data_ptr(), deg.data_ptr(), local,
+                                                       C.byref(h)), "graph_from_csr")
+            gh = prl.CsrGraph(h, local)  # owns the handle
+            distributed.run_distributed(gh, cfg["alphas"], cfg["tol"], prl.NormKind(cfg["norm"]), 500,
+                                        cfg.get("stop_mask", 0), want_ranks=True)
+            del gh
+        e2e_step()
+        per = []
+        for _ in range(3):
+            tdist.barrier()
+            t0 = time.perf_counter()
+            e2e_step()
+            per.append(time.perf_counter() - t0)
+        tt = torch.tensor([statistics.median(per)], device=f"cuda:{local}", dtype=torch.float64)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        dt = float(tt.item())
+        K = len(cfg["alphas"])
+        e2e = {"value": lane_its * e / dt / 1e9, "unit": "GTEPS",
+               "h2d_bytes_per_step": world * (8 * (n + 1) + 4 * e + 4 * n), "d2h_bytes_per_step": 8 * K * n,
+               "ms_per_step": dt * 1e3, "steps": 3, "statistic": "median, max over ranks",
+               "path": "prgpu_graph_from_csr on every rank + distributed.run_distributed(want_ranks=True)"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
@@ -427,6 +469,9 @@ def run_partitioned(args, cfg):
                        "wall_s": wall},
             "gpu_launches": args.steps * r.run_iterations * 2,
             "clocks": clk.summary(),
+            "roofline": roof,
+            "cpu_baseline": None,
+            "e2e": e2e,
         }
         print(json.dumps(line), flush=True)
     tdist.barrier()

@@ -184,6 +184,10 @@ PRGPU_API int prgpu_part_finalize(prgpu_session* s);
 PRGPU_API int prgpu_part_active(prgpu_session* s, int* any_active);
 /* Final ranks of caller lane `lane` for this rank's engine rows [row_begin, row_end). */
 PRGPU_API int prgpu_part_local_ranks(prgpu_session* s, int lane, double* out);
+/* The same for every lane at once into DEVICE memory, out[lane * ld + i] for
+ * row row_begin + i, enqueued on the session's stream (no host sync): for a
+ * device-side gather of the ranks across the job. */
+PRGPU_API int prgpu_part_local_ranks_device(prgpu_session* s, double* dev_out, uint64_t ld);
 /* Engine row -> caller vertex id, [n]. */
 PRGPU_API int prgpu_graph_permutation(const prgpu_graph* g, uint32_t* old_of_new);
 

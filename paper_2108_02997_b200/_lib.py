@@ -25,6 +25,7 @@ EXPORTS = [
     "prgpu_version", "prgpu_kernel_launch_count", "prgpu_part_buffer_sizes", "prgpu_part_create",
     "prgpu_part_plan", "prgpu_part_exchange", "prgpu_part_set_stream", "prgpu_part_init",
     "prgpu_part_step", "prgpu_part_finalize", "prgpu_part_active", "prgpu_part_local_ranks",
+    "prgpu_part_local_ranks_device",
     "prgpu_graph_permutation",
 ]
 
@@ -110,6 +111,7 @@ def lib():
             "prgpu_part_finalize": ([vp], i32),
             "prgpu_part_active": ([vp, C.POINTER(i32)], i32),
             "prgpu_part_local_ranks": ([vp, i32, vp], i32),
+            "prgpu_part_local_ranks_device": ([vp, vp, u64], i32),
             "prgpu_graph_permutation": ([vp, vp], i32),
         }
         for name, (args, res) in sig.items():

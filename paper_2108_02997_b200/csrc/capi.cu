@@ -39,6 +39,7 @@ void part_exchange(prgpu_session*, prgpu_exchange*);
 int part_step(prgpu_session*);
 void part_finalize(prgpu_session*);
 void part_local_ranks(prgpu_session*, int, double*);
+void part_local_ranks_device(prgpu_session*, double*, uint64_t);
 void session_init(prgpu_session*);
 int read_any_active(prgpu_session*);
 void part_plan_copy(prgpu_session*, prgpu_partition*);
@@ -321,6 +322,13 @@ int prgpu_part_local_ranks(prgpu_session* s, int lane, double* out) {
     return guarded([&] {
         if (!s || !out) prgpu::fail(PRGPU_EINVAL, "null argument");
         prgpu::part_local_ranks(s, lane, out);
+    });
+}
+
+int prgpu_part_local_ranks_device(prgpu_session* s, double* dev_out, uint64_t ld) {
+    return guarded([&] {
+        if (!s || !dev_out) prgpu::fail(PRGPU_EINVAL, "null argument");
+        prgpu::part_local_ranks_device(s, dev_out, ld);
     });
 }
 

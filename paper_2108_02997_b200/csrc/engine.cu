@@ -78,6 +78,30 @@ __global__ void extract_ranks(Params P, const uint32_t* __restrict__ new_of_old,
     }
 }
 
+__global__ void strided_copy(const double* __restrict__ src, uint32_t stride, double* __restrict__ dst,
+                             uint32_t rows) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < rows; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[i * stride];
+}
+
+struct LaneMap {
+    int user_of[16]; // device slot -> caller lane
+};
+
+// every lane of rows [row_begin, row_begin + rows) into out[caller lane][i]
+__global__ void local_ranks_kernel(Params P, LaneMap map, uint32_t row_begin, uint32_t rows,
+                                   double* __restrict__ out, uint64_t ld) {
+    const uint64_t total = (uint64_t)rows * P.K;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = (uint32_t)(x / rows), i = (uint32_t)(x - (uint64_t)k * rows);
+        const uint32_t r = row_begin + i;
+        const LaneState& L = P.lanes[k];
+        const double v = r >= P.empty_begin ? L.c0_used : P.rank[L.iterations & 1][(size_t)r * P.ks + k];
+        out[(size_t)map.user_of[k] * ld + i] = v;
+    }
+}
+
 __global__ void scatter_ref(const double* __restrict__ in, const uint32_t* __restrict__ new_of_old,
                             double* __restrict__ out, uint32_t n) {
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n;
@@ -958,6 +982,21 @@ void part_finalize(prgpu_session* s) {
     PRGPU_LAUNCHED("part_finalize");
 }
 
+void part_local_ranks_device(prgpu_session* s, double* out, uint64_t ld) {
+    DeviceGuard dg(s->g->device);
+    if (s->parts.empty()) fail(PRGPU_EINVAL, "not a partition session");
+    const prgpu_partition& me = s->parts[s->part_rank];
+    const uint32_t rows = me.row_end - me.row_begin;
+    if (ld < rows) fail(PRGPU_EINVAL, "local_ranks_device: ld smaller than the rank's row count");
+    LaneMap map{};
+    for (int k = 0; k < s->K; ++k) map.user_of[k] = s->user_of[k];
+    if (rows) {
+        local_ranks_kernel<<<blocks_for((uint64_t)rows * s->K), kNT, 0, s->cur()>>>(s->P, map, me.row_begin, rows,
+                                                                                  out, ld);
+        PRGPU_LAUNCHED("local_ranks_kernel");
+    }
+}
+
 void part_local_ranks(prgpu_session* s, int user_lane, double* out) {
     DeviceGuard dg(s->g->device);
     int slot = -1;
@@ -970,9 +1009,17 @@ void part_local_ranks(prgpu_session* s, int user_lane, double* out) {
     const prgpu_partition& me = s->parts[s->part_rank];
     const uint32_t stored_end = std::min(me.row_end, s->P.empty_begin);
     if (stored_end > me.row_begin)
-        PRGPU_CUDA(cudaMemcpy2DAsync(out, 8, s->P.rank[L.iterations & 1] + (size_t)me.row_begin * s->P.ks + slot,
-                                     (size_t)s->P.ks * 8, 8, stored_end - me.row_begin, cudaMemcpyDeviceToHost,
-                                     s->cur()));
+    {
+        // one lane's column of the row-major ranks, made contiguous on the device
+        AllocScope scope(s->cur());
+        const uint32_t rows = stored_end - me.row_begin;
+        DevBuf<double> tmp(rows);
+        strided_copy<<<blocks_for(rows), kNT, 0, s->cur()>>>(
+            s->P.rank[L.iterations & 1] + (size_t)me.row_begin * s->P.ks + slot, s->P.ks, tmp.p, rows);
+        PRGPU_LAUNCHED("strided_copy");
+        PRGPU_CUDA(cudaMemcpyAsync(out, tmp.p, (size_t)rows * 8, cudaMemcpyDeviceToHost, s->cur()));
+        PRGPU_CUDA(cudaStreamSynchronize(s->cur()));
+    }
     PRGPU_CUDA(cudaStreamSynchronize(s->cur()));
     for (uint32_t r = std::max(me.row_begin, stored_end); r < me.row_end; ++r) out[r - me.row_begin] = L.c0_used;
 }

@@ -219,6 +219,10 @@ def _run_distributed_on(g, alphas, tolerance, norm, max_iterations, stop_mask, w
     dist.barrier()
     start.record()
     its = 0
+    # the stop flag is read back every WINDOW iterations only: launches after
+    # convergence are no-ops on the device (the pull and finalize kernels
+    # exit when no lane is active; the exchange re-sends unchanged rows)
+    WINDOW = 4
     while its < max_iterations:
         par = part.step()
         if world > 1:
@@ -228,17 +232,40 @@ def _run_distributed_on(g, alphas, tolerance, norm, max_iterations, stop_mask, w
             dist.all_gather_into_tensor(part.partials, mine)
         part.finalize()
         its += 1
-        if not part.active():
+        if its % WINDOW == 0 and not part.active():
             break
     stop.record()
     torch.cuda.synchronize()
     K = len(alphas)
-    res = PartResult(iterations=_lane_iterations(part), ranks=None, run_iterations=its,
+    lane_its = _lane_iterations(part)
+    res = PartResult(iterations=lane_its, ranks=None, run_iterations=int(lane_its.max()),
                      loop_ms=start.elapsed_time(stop))
     if want_ranks:
-        local = [part.local_ranks(k) for k in range(K)]
-        gathered = [None] * world
-        dist.all_gather_object(gathered, local)
-        res.ranks = _assemble(g, gathered, K)
+        res.ranks = _gather_ranks(part, g, K, world)
     part.close()
     return res
+
+
+def _gather_ranks(part: _Part, g: CsrGraph, K: int, world: int) -> np.ndarray:
+    """Every rank's rows of every lane gathered on the devices (one
+    all-gather), put back in caller order there, one copy to the host."""
+    import torch
+    import torch.distributed as dist
+    dev = part.contrib.device
+    rows = [q.row_end - q.row_begin for q in part.parts]
+    ld = max(rows)
+    local = torch.empty((K, ld), dtype=torch.float64, device=dev)
+    check(lib().prgpu_part_local_ranks_device(part._s, C.c_void_p(local.data_ptr()), ld), "local ranks")
+    if world > 1:
+        gathered = torch.empty((world, K, ld), dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(gathered, local)
+    else:
+        gathered = local.unsqueeze(0)
+    eng = torch.cat([gathered[r, :, :rows[r]] for r in range(world)], dim=1)  # [K][n], engine rows
+    perm = torch.from_numpy(_permutation(g).astype(np.int64)).to(dev)
+    out = torch.empty_like(eng)
+    out[:, perm] = eng
+    host = torch.empty(out.shape, dtype=torch.float64, pin_memory=True)
+    host.copy_(out)
+    torch.cuda.current_stream(dev).synchronize()
+    return host.numpy()
