@@ -398,7 +398,8 @@ def run_partitioned(args, cfg):
         g = prl.generate_grid(cfg["side"], 0.6, 0.01, SEED, device=local)
     n, e = g.vertex_count, g.edge_count()
     run = lambda: distributed.run_distributed(g, cfg["alphas"], cfg["tol"],  # noqa: E731
-                                              prl.NormKind(cfg["norm"]), 500, cfg.get("stop_mask", 0))
+                                              prl.NormKind(cfg["norm"]), 500, cfg.get("stop_mask", 0),
+                                              exchange=args.exchange)
     for _ in range(args.warmup):
         r = run()
     iters = r.iterations
@@ -439,7 +440,7 @@ def run_partitioned(args, cfg):
                                                        C.byref(h)), "graph_from_csr")
             gh = prl.CsrGraph(h, local)  # owns the handle
             distributed.run_distributed(gh, cfg["alphas"], cfg["tol"], prl.NormKind(cfg["norm"]), 500,
-                                        cfg.get("stop_mask", 0), want_ranks=True)
+                                        cfg.get("stop_mask", 0), want_ranks=True, exchange=args.exchange)
             del gh
         e2e_step()
         per = []
@@ -464,7 +465,9 @@ def run_partitioned(args, cfg):
             "data": "synthetic: seeded RMAT/grid generated on the device (DESIGN.md)",
             "config": {"workload": cfg["workload"], "vertices": n, "edges": e,
                        "iterations_per_lane": iters.tolist(), "lane_iterations": lane_its,
-                       "parallelism": f"1D row partition x{world}, NCCL exchange per iteration",
+                       "parallelism": f"1D row partition x{world}, " + (
+                           "fused peer-memory exchange (NVLink stores from the pull kernel, CUDA graph loop)"
+                           if args.exchange == "peer" else "NCCL exchange per iteration"),
                        "timed_scope": "iteration loop incl. exchange, CUDA events, max over ranks",
                        "wall_s": wall},
             "gpu_launches": args.steps * r.run_iterations * 2,
@@ -563,6 +566,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="N>1 partitioned solve: fused peer-memory exchange (default) or NCCL calls")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas (weak scaling) instead of the 1D partition")
     args = ap.parse_args()

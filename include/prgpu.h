@@ -188,6 +188,27 @@ PRGPU_API int prgpu_part_local_ranks(prgpu_session* s, int lane, double* out);
  * row row_begin + i, enqueued on the session's stream (no host sync): for a
  * device-side gather of the ranks across the job. */
 PRGPU_API int prgpu_part_local_ranks_device(prgpu_session* s, double* dev_out, uint64_t ld);
+/* Fused exchange over peer memory (NVLink / NVSwitch), instead of the
+ * caller moving buffers between steps: the peers' contribution buffers,
+ * rank-partials buffers (sized 2 x prgpu_part_buffer_sizes' partials: one
+ * block per iteration parity) and arrival counters, as device pointers valid
+ * in this process (CUDA IPC), `npeers` = nranks - 1 in rank order skipping
+ * this rank; `arrive` is this rank's own counter (peers' pointers to it are
+ * their peer_arrive).  The pull kernel then stores each contribution row and
+ * the rank's partials straight into every peer's buffers and signals arrival;
+ * the finalize kernel waits for all ranks.  After prgpu_part_init (and a
+ * host barrier across ranks), prgpu_part_launch enqueues the whole loop as
+ * one CUDA graph; host-driven prgpu_part_step/_finalize also work. */
+PRGPU_API int prgpu_part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib,
+                                   double* const* peer_partials, unsigned int* const* peer_arrive,
+                                   unsigned int* arrive);
+PRGPU_API int prgpu_part_launch(prgpu_session* s);
+/* CUDA IPC for the fused exchange's buffers (any pointer inside a device
+ * allocation): export a 64-byte handle + offset; open it in another process
+ * of the same node (peer access enabled); close with the pointer open gave. */
+PRGPU_API int prgpu_ipc_export(const void* dev_ptr, void* handle64, uint64_t* offset);
+PRGPU_API int prgpu_ipc_open(const void* handle64, uint64_t offset, int device, void** dev_ptr);
+PRGPU_API int prgpu_ipc_close(void* dev_ptr, uint64_t offset);
 /* Engine row -> caller vertex id, [n]. */
 PRGPU_API int prgpu_graph_permutation(const prgpu_graph* g, uint32_t* old_of_new);
 

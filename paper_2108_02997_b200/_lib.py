@@ -25,7 +25,8 @@ EXPORTS = [
     "prgpu_version", "prgpu_kernel_launch_count", "prgpu_part_buffer_sizes", "prgpu_part_create",
     "prgpu_part_plan", "prgpu_part_exchange", "prgpu_part_set_stream", "prgpu_part_init",
     "prgpu_part_step", "prgpu_part_finalize", "prgpu_part_active", "prgpu_part_local_ranks",
-    "prgpu_part_local_ranks_device",
+    "prgpu_part_local_ranks_device", "prgpu_part_set_peers", "prgpu_part_launch",
+    "prgpu_ipc_export", "prgpu_ipc_open", "prgpu_ipc_close",
     "prgpu_graph_permutation",
 ]
 
@@ -112,6 +113,11 @@ def lib():
             "prgpu_part_active": ([vp, C.POINTER(i32)], i32),
             "prgpu_part_local_ranks": ([vp, i32, vp], i32),
             "prgpu_part_local_ranks_device": ([vp, vp, u64], i32),
+            "prgpu_part_set_peers": ([vp, i32, vp, vp, vp, vp], i32),
+            "prgpu_part_launch": ([vp], i32),
+            "prgpu_ipc_export": ([vp, vp, C.POINTER(u64)], i32),
+            "prgpu_ipc_open": ([vp, u64, i32, C.POINTER(vp)], i32),
+            "prgpu_ipc_close": ([vp, u64], i32),
             "prgpu_graph_permutation": ([vp, vp], i32),
         }
         for name, (args, res) in sig.items():

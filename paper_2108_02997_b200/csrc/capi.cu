@@ -40,6 +40,8 @@ int part_step(prgpu_session*);
 void part_finalize(prgpu_session*);
 void part_local_ranks(prgpu_session*, int, double*);
 void part_local_ranks_device(prgpu_session*, double*, uint64_t);
+void part_set_peers(prgpu_session*, int, double* const*, double* const*, unsigned int* const*, unsigned int*);
+void part_launch(prgpu_session*);
 void session_init(prgpu_session*);
 int read_any_active(prgpu_session*);
 void part_plan_copy(prgpu_session*, prgpu_partition*);
@@ -329,6 +331,61 @@ int prgpu_part_local_ranks_device(prgpu_session* s, double* dev_out, uint64_t ld
     return guarded([&] {
         if (!s || !dev_out) prgpu::fail(PRGPU_EINVAL, "null argument");
         prgpu::part_local_ranks_device(s, dev_out, ld);
+    });
+}
+
+int prgpu_part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, double* const* peer_partials,
+                         unsigned int* const* peer_arrive, unsigned int* arrive) {
+    return guarded([&] {
+        if (!s || (npeers > 0 && (!peer_contrib || !peer_partials || !peer_arrive)))
+            prgpu::fail(PRGPU_EINVAL, "null argument");
+        prgpu::part_set_peers(s, npeers, peer_contrib, peer_partials, peer_arrive, arrive);
+    });
+}
+
+int prgpu_part_launch(prgpu_session* s) {
+    return guarded([&] {
+        if (!s) prgpu::fail(PRGPU_EINVAL, "null session");
+        prgpu::part_launch(s);
+    });
+}
+
+int prgpu_ipc_export(const void* dev_ptr, void* handle64, uint64_t* offset) {
+    return guarded([&] {
+        if (!dev_ptr || !handle64 || !offset) prgpu::fail(PRGPU_EINVAL, "null argument");
+        // the allocation's base through the driver entry point (no libcuda link)
+        using AddrRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        PRGPU_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) prgpu::fail(PRGPU_ECUDA, "cuMemGetAddressRange unavailable");
+        unsigned long long base = 0;
+        size_t size = 0;
+        if (reinterpret_cast<AddrRange>(fn)(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0)
+            prgpu::fail(PRGPU_EINVAL, "ipc_export: not a device allocation");
+        cudaIpcMemHandle_t h;
+        PRGPU_CUDA(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base));
+        std::memcpy(handle64, &h, sizeof(h));
+        *offset = (uint64_t)((uintptr_t)dev_ptr - base);
+    });
+}
+
+int prgpu_ipc_open(const void* handle64, uint64_t offset, int device, void** dev_ptr) {
+    return guarded([&] {
+        if (!handle64 || !dev_ptr) prgpu::fail(PRGPU_EINVAL, "null argument");
+        prgpu::DeviceGuard dg(device);
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle64, sizeof(h));
+        void* base = nullptr;
+        PRGPU_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+        *dev_ptr = static_cast<char*>(base) + offset;
+    });
+}
+
+int prgpu_ipc_close(void* dev_ptr, uint64_t offset) {
+    return guarded([&] {
+        if (!dev_ptr) prgpu::fail(PRGPU_EINVAL, "null argument");
+        PRGPU_CUDA(cudaIpcCloseMemHandle(static_cast<char*>(dev_ptr) - offset));
     });
 }
 

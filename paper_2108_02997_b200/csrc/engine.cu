@@ -343,6 +343,7 @@ struct prgpu_session {
     std::vector<prgpu_partition> parts;
     DevBuf<double> rank_partials;
     cudaStream_t ext_stream = nullptr;
+    double* ext_contrib_base = nullptr; // caller-provided contribution buffer (partition sessions)
     cudaStream_t cur() const { return ext_stream ? ext_stream : (cudaStream_t)stream; }
     // lanes that stopped, written by the device (host-mapped), for copying
     // results out while the other lanes still iterate (session_solve)
@@ -616,6 +617,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     const int KS = s->cfg.KS;
     s->rank.alloc(2 * (size_t)KS * n);
     double* cbase = ext_contrib;
+    s->ext_contrib_base = ext_contrib;
     if (!cbase) {
         s->contrib.alloc(2 * nsrc * KS);
         cbase = s->contrib.p;
@@ -673,6 +675,9 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     P.gs = s->gs.p;
     P.use_cond = 0;
     P.frozen_at = nullptr;
+    P.fused = 0;
+    P.npeers = 0;
+    P.arrive = nullptr;
     if (nranks == 0) {
         PRGPU_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->host_frozen), K * sizeof(int), cudaHostAllocMapped));
         std::fill(s->host_frozen, s->host_frozen + K, 0);
@@ -899,6 +904,92 @@ void part_plan_copy(prgpu_session* s, prgpu_partition* parts) {
 
 void part_set_stream(prgpu_session* s, void* stream) { s->ext_stream = (cudaStream_t)stream; }
 
+// Fused exchange over peer memory (Params::fused): the peers' buffers as
+// device pointers valid in this process (CUDA IPC or same-device buffers),
+// and the iteration loop as a CUDA graph WHILE { pull ; finalize } that runs
+// with no host involvement until every lane has stopped.
+void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, double* const* peer_rp,
+                    unsigned int* const* peer_arrive, unsigned int* arrive) {
+    DeviceGuard dg(s->g->device);
+    if (s->parts.empty()) fail(PRGPU_EINVAL, "not a partition session");
+    if (npeers < 0 || npeers > kMaxPeers || npeers != s->nranks - 1)
+        fail(PRGPU_EINVAL, "set_peers: npeers must be nranks - 1 (<= " + std::to_string(kMaxPeers) + ")");
+    if (!arrive) fail(PRGPU_EINVAL, "set_peers: null arrival counter");
+    if (!s->ext_contrib_base) fail(PRGPU_EINVAL, "set_peers: the session needs caller-provided buffers");
+    Params& P = s->P;
+    P.fused = 1;
+    P.npeers = npeers;
+    for (int q = 0; q < npeers; ++q) {
+        if (!peer_contrib[q] || !peer_rp[q] || !peer_arrive[q]) fail(PRGPU_EINVAL, "set_peers: null peer pointer");
+        // peers' buffers share this rank's layout: same base offsets
+        P.peer_cbase[q] = peer_contrib[q] + (P.cbase - s->ext_contrib_base);
+        P.peer_rp[q] = peer_rp[q];
+        P.peer_arrive[q] = peer_arrive[q];
+    }
+    P.arrive = arrive;
+    for (auto& l : s->launches) {
+        Params keep = l.P;
+        l.P = P;
+        l.P.G = keep.G;
+        l.P.gtot = keep.gtot;
+        l.P.pcol0 = keep.pcol0;
+        l.P.task_begin = keep.task_begin;
+        l.P.task_end = keep.task_end;
+    }
+    if (s->exec) { cudaGraphExecDestroy(s->exec); s->exec = nullptr; }
+    if (s->graph) { cudaGraphDestroy(s->graph); s->graph = nullptr; }
+    PRGPU_CUDA(cudaGraphCreate(&s->graph, 0));
+    cudaGraphConditionalHandle h;
+    PRGPU_CUDA(cudaGraphConditionalHandleCreate(&h, s->graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    PRGPU_CUDA(cudaGraphAddNode(&cnode, s->graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cudaGraphNode_t prev = nullptr;
+    for (const auto& l : s->launches) {
+        Params PG = l.P;
+        PG.use_cond = 1;
+        PG.cond = h;
+        cudaKernelNodeParams kp = {};
+        kp.func = (void*)l.fn;
+        kp.gridDim = dim3(PG.G);
+        kp.blockDim = dim3(kNT);
+        kp.sharedMemBytes = (unsigned)l.smem;
+        void* args[] = {&PG};
+        kp.kernelParams = args;
+        cudaGraphNode_t node;
+        PRGPU_CUDA(cudaGraphAddKernelNode(&node, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+        prev = node;
+    }
+    {
+        Params PF = P;
+        PF.use_cond = 1;
+        PF.cond = h;
+        cudaKernelNodeParams kp = {};
+        kp.func = (void*)s->cfg.fin;
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(kNT);
+        void* args[] = {&PF};
+        kp.kernelParams = args;
+        cudaGraphNode_t node;
+        PRGPU_CUDA(cudaGraphAddKernelNode(&node, body, &prev, 1, &kp));
+    }
+    PRGPU_CUDA(cudaGraphInstantiate(&s->exec, s->graph, 0));
+    s->use_graph = true;
+}
+
+// the whole fused partitioned loop, enqueued on the session's stream
+void part_launch(prgpu_session* s) {
+    DeviceGuard dg(s->g->device);
+    if (!s->P.fused || !s->exec) fail(PRGPU_EINVAL, "part_launch: call prgpu_part_set_peers first");
+    PRGPU_CUDA(cudaGraphLaunch(s->exec, s->cur()));
+    g_launches.fetch_add(1);
+}
+
 void graph_permutation(const prgpu_graph* g, uint32_t* old_of_new) {
     DeviceGuard dg(g->device);
     PRGPU_CUDA(cudaMemcpy(old_of_new, g->old_of_new.p, (size_t)g->n * 4, cudaMemcpyDeviceToHost));
@@ -938,6 +1029,8 @@ void session_init(prgpu_session* s) {
     PRGPU_CUDA(cudaMemcpyAsync(s->gs.p, &gsh, sizeof(gsh), cudaMemcpyHostToDevice, s->cur()));
     launch_init(s->cfg, s->P, s->g->ndangling, s->cur());
     s->host_iter = 0;
+    if (s->P.fused && s->P.arrive) // peers add to it only after the caller's barrier
+        PRGPU_CUDA(cudaMemsetAsync(s->P.arrive, 0, sizeof(unsigned int), s->cur()));
     if (s->host_frozen) std::fill(s->host_frozen, s->host_frozen + s->K, 0); // no kernel in flight
 }
 
@@ -978,7 +1071,7 @@ int part_step(prgpu_session* s) {
 
 void part_finalize(prgpu_session* s) {
     DeviceGuard dg(s->g->device);
-    s->cfg.fin<<<1, kNT, 0, s->cur()>>>(s->P);
+    s->cfg.fin<<<1, kNT, 0, s->cur()>>>(s->P); // fused: waits for the peers' arrivals
     PRGPU_LAUNCHED("part_finalize");
 }
 

@@ -87,6 +87,7 @@ struct GlobalState {
 };
 
 constexpr int kMaxModes = 5;
+constexpr int kMaxPeers = 7; // up to 8 GPUs of one NVSwitch domain
 
 struct Params {
     uint32_t n, K;
@@ -149,6 +150,18 @@ struct Params {
     int use_mode_cond;
     cudaGraphConditionalHandle mode_cond[kMaxModes];
     uint32_t er; // rows per empty task
+    // fused multi-GPU exchange over peer memory (NVLink/NVSwitch): every
+    // contribution row this rank computes is also stored into each peer's
+    // buffer (same layout), the rank's partial vector into each peer's
+    // rank_partials slot [parity][rank], and the last CTA then bumps every
+    // rank's arrival counter; part_finalize_kernel waits for nranks arrivals
+    // per iteration.  No host round trip, no collective call.
+    int fused;
+    int npeers;
+    double* peer_cbase[kMaxPeers];
+    double* peer_rp[kMaxPeers];
+    unsigned int* peer_arrive[kMaxPeers];
+    unsigned int* arrive; // this rank's arrival counter (peers add to it)
 };
 
 // ---- L2 residency control -------------------------------------------------------
@@ -377,6 +390,10 @@ struct Warp {
             store_w_pol<W>(dst, cv, pol);
         } else {
             store_w<W>(dst, cv);
+        }
+        if (P.fused) { // the same row into every peer's buffer (NVLink stores)
+            const size_t off = (size_t)(dst - P.cbase);
+            for (int q = 0; q < P.npeers; ++q) store_w<W>(P.peer_cbase[q] + off, cv);
         }
     }
 
@@ -971,7 +988,8 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     if (P.no_finalize) return; // first kernel of a split iteration
 
     // ---- last CTA: reduce partials, convergence, next teleport --------------------------
-    __threadfence();
+    if (P.fused) __threadfence_system(); // this CTA's peer stores before its ticket
+    else __threadfence();
     __syncthreads();
     if (tid == 0) s_flag = (atomicAdd(&P.gs->counter, 1u) == P.G - 1);
     __syncthreads();
@@ -1007,8 +1025,21 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     }
     __syncthreads();
     if (P.part_mode) { // multi-GPU: publish this rank's vector; finalize runs after the exchange
-        for (int t = tid; t < kNQ * KP; t += kNT) P.rank_partials[(size_t)P.part_rank * kNQ * KP + t] = s_tot[t];
-        if (tid == 0) P.gs->counter = 0;
+        const size_t slot = ((P.fused ? (size_t)(s_iter & 1) * P.nranks : 0) + P.part_rank) * kNQ * KP;
+        for (int t = tid; t < kNQ * KP; t += kNT) {
+            P.rank_partials[slot + t] = s_tot[t];
+            if (P.fused)
+                for (int q = 0; q < P.npeers; ++q) P.peer_rp[q][slot + t] = s_tot[t];
+        }
+        __syncthreads();
+        if (tid == 0) {
+            P.gs->counter = 0;
+            if (P.fused) { // every CTA's rows and this vector are out: arrive everywhere
+                __threadfence_system();
+                for (int q = 0; q < P.npeers; ++q) atomicAdd_system(P.peer_arrive[q], 1u);
+                atomicAdd_system(P.arrive, 1u);
+            }
+        }
         return;
     }
     finalize_lanes<KP, QM>(P, s_tot, s_c0, s_active, s_iter);
@@ -1054,17 +1085,36 @@ __global__ void __launch_bounds__(kNT) part_finalize_kernel(const Params P) {
         s_c0[tid] = real ? P.lanes[tid].c0 : 0.0;
         s_active[tid] = real ? P.lanes[tid].active : 0;
     }
+    __shared__ int s_go;
+    if (tid == 0) s_go = P.gs->any_active;
+    __syncthreads();
+    if (!s_go) return; // speculative launch after convergence
+    if (P.fused && tid == 0) {
+        // every rank's rows and partials for this iteration have landed once
+        // nranks arrivals are counted (a bounded wait: a lost peer traps
+        // instead of hanging the device)
+        const unsigned target = P.nranks * (unsigned)(s_iter + 1);
+        const long long t0 = clock64();
+        unsigned seen;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(seen) : "l"(P.arrive) : "memory");
+            if (seen >= target) break;
+            __nanosleep(256);
+            if (clock64() - t0 > 40000000000ll) __trap(); // ~20 s
+        }
+    }
+    __syncthreads();
+    const size_t pbase = P.fused ? (size_t)(s_iter & 1) * P.nranks * kNQ * KP : 0;
     for (int t = tid; t < kNQ * KP; t += kNT) {
         const int q = t / KP;
         double v = 0.0;
         for (uint32_t r = 0; r < P.nranks; ++r) {
-            const double x = P.rank_partials[(size_t)r * kNQ * KP + t];
+            const double x = __ldcg(P.rank_partials + pbase + (size_t)r * kNQ * KP + t);
             v = (q == 2) ? fmax(v, x) : v + x;
         }
         s_tot[t] = v;
     }
     __syncthreads();
-    if (!P.gs->any_active) return;
     finalize_lanes<KP, QM>(P, s_tot, s_c0, s_active, s_iter);
 }
 

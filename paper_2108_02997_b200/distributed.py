@@ -43,12 +43,13 @@ class _Part:
     """One rank's engine session plus its exchange buffers (torch tensors)."""
 
     def __init__(self, g: CsrGraph, alphas, tolerance, norm, max_iterations, stop_mask, rank,
-                 nranks, device):
+                 nranks, device, fused: bool = False):
         import torch
         self.torch = torch
         self.g = g
         self.K = len(alphas)
         self.rank, self.nranks = rank, nranks
+        self.fused = fused
         p, self._keep = _params(list(alphas), tolerance, norm, max_iterations, stop_mask)
         self._p = p
         nc, npart = C.c_uint64(), C.c_uint64()
@@ -56,7 +57,10 @@ class _Part:
                                             C.byref(npart)), "part sizes")
         dev = torch.device("cuda", device)
         self.contrib = torch.empty(nc.value, dtype=torch.float64, device=dev)
-        self.partials = torch.zeros(npart.value, dtype=torch.float64, device=dev)
+        # fused exchange: partials double-buffered by iteration parity, plus
+        # the arrival counter the peers increment
+        self.partials = torch.zeros(npart.value * (2 if fused else 1), dtype=torch.float64, device=dev)
+        self.arrive = torch.zeros(1, dtype=torch.int32, device=dev) if fused else None
         self._s = C.c_void_p()
         check(lib().prgpu_part_create(g.handle, C.byref(p), rank, nranks, self.contrib.data_ptr(),
                                       self.partials.data_ptr(), C.byref(self._s)), "part create")
@@ -72,7 +76,7 @@ class _Part:
         # views of the two parity buffers and of each rank's rows in them
         self.buf = [self.contrib[(ex.contrib[i] - base) // 8:(ex.contrib[i] - base) // 8 +
                                  self.nsrc * self.stride] for i in (0, 1)]
-        self.slot = self.partials.view(nranks, self.ppr)
+        self.slot = self.partials.view(-1, self.ppr)[:nranks]
 
     def chunk(self, parity, r):
         q = self.parts[r]
@@ -87,6 +91,16 @@ class _Part:
 
     def init(self):
         check(lib().prgpu_part_init(self._s), "part init")
+
+    def set_peers(self, peer_contrib, peer_partials, peer_arrive):
+        """Fused exchange: device pointers (ints) of the other ranks' buffers, rank order."""
+        n = len(peer_contrib)
+        arr = (C.c_void_p * max(n, 1))
+        check(lib().prgpu_part_set_peers(self._s, n, arr(*peer_contrib), arr(*peer_partials),
+                                         arr(*peer_arrive), C.c_void_p(self.arrive.data_ptr())), "set peers")
+
+    def launch(self):
+        check(lib().prgpu_part_launch(self._s), "part launch")
 
     def step(self) -> int:
         par = C.c_int()
@@ -137,34 +151,51 @@ def _assemble(g: CsrGraph, chunks_by_rank, K) -> np.ndarray:
 
 def emulate(g: CsrGraph, alphas: Sequence[float], nranks: int, tolerance=1e-6,
             norm: NormKind = NormKind.L1, max_iterations: int = 500, stop_mask: int = 0,
-            want_ranks: bool = True) -> PartResult:
-    """All `nranks` partitions in this process on this GPU; the exchange is a
-    device copy of each rank's rows into every other rank's buffers."""
+            want_ranks: bool = True, fused: bool = False, graph: bool = False) -> PartResult:
+    """All `nranks` partitions in this process on this GPU.  Default: the
+    exchange is a device copy of each rank's rows into every other rank's
+    buffers (what NCCL does between GPUs).  fused=True: the ranks' kernels
+    store into each other's buffers and count arrivals themselves (the
+    peer-memory path); the ranks run one after another, so no kernel ever
+    waits on another.  graph=True (one rank only): the fused loop as the
+    CUDA graph prgpu_part_launch enqueues."""
     import torch
+    if graph and (not fused or nranks != 1):
+        raise ValueError("emulate: graph=True needs fused=True and nranks == 1 (ranks would wait on each other)")
     dev = g.device
-    parts = [_Part(g, alphas, tolerance, norm, max_iterations, stop_mask, r, nranks, dev)
+    parts = [_Part(g, alphas, tolerance, norm, max_iterations, stop_mask, r, nranks, dev, fused=fused)
              for r in range(nranks)]
     stream = torch.cuda.Stream(device=dev)  # a real stream: the legacy default is handle 0
     with torch.cuda.stream(stream):
-        return _emulate_on(parts, alphas, max_iterations, want_ranks, g)
+        return _emulate_on(parts, alphas, max_iterations, want_ranks, g, fused, graph)
 
 
-def _emulate_on(parts, alphas, max_iterations, want_ranks, g):
+def _emulate_on(parts, alphas, max_iterations, want_ranks, g, fused=False, graph=False):
     import torch
     for p in parts:
         p.set_stream()
+    if fused:
+        for p in parts:
+            peers = [q for q in parts if q is not p]
+            p.set_peers([q.contrib.data_ptr() for q in peers], [q.partials.data_ptr() for q in peers],
+                        [q.arrive.data_ptr() for q in peers])
+    for p in parts:
         p.init()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
     its = 0
-    while its < max_iterations:
+    if graph:
+        parts[0].launch()
+        its = -1
+    while 0 <= its < max_iterations:
         pars = [p.step() for p in parts]
         par = pars[0]
-        for dst in parts:
-            for r, src in enumerate(parts):
-                if src is not dst:
-                    dst.chunk(par, r).copy_(src.chunk(par, r))
-                    dst.slot[r].copy_(src.slot[r])
+        if not fused:
+            for dst in parts:
+                for r, src in enumerate(parts):
+                    if src is not dst:
+                        dst.chunk(par, r).copy_(src.chunk(par, r))
+                        dst.slot[r].copy_(src.slot[r])
         for p in parts:
             p.finalize()
         its += 1
@@ -173,12 +204,13 @@ def _emulate_on(parts, alphas, max_iterations, want_ranks, g):
     stop.record()
     torch.cuda.synchronize()
     K = len(alphas)
-    res = PartResult(iterations=np.zeros(K, np.int32), ranks=None, run_iterations=its,
+    res = PartResult(iterations=np.zeros(K, np.int32), ranks=None, run_iterations=0,
                      loop_ms=start.elapsed_time(stop))
     if want_ranks:
         chunks = [[p.local_ranks(k) for k in range(K)] for p in parts]
         res.ranks = _assemble(g, chunks, K)
     res.iterations[:] = _lane_iterations(parts[0])
+    res.run_iterations = int(res.iterations.max())
     for p in parts:
         p.close()
     return res
@@ -195,17 +227,88 @@ def _lane_iterations(part: _Part) -> np.ndarray:
 
 def run_distributed(g: CsrGraph, alphas: Sequence[float], tolerance=1e-6,
                     norm: NormKind = NormKind.L1, max_iterations: int = 500, stop_mask: int = 0,
-                    want_ranks: bool = False) -> PartResult:
+                    want_ranks: bool = False, exchange: str = "nccl") -> PartResult:
     """One rank of an N-GPU run (torch.distributed initialised with NCCL,
-    one process per GPU).  Contribution rows of rank r travel by a broadcast
-    from r; the partial vectors by an all-gather."""
+    one process per GPU).
+
+    exchange="nccl": contribution rows of rank r travel by a broadcast from r,
+    the partial vectors by an all-gather, between host-enqueued pull and
+    finalize kernels.  exchange="peer": the fused path — the ranks map each
+    other's buffers (CUDA IPC), the pull kernel stores every contribution row
+    and the partials straight into all peers over NVLink and the finalize
+    kernel waits for the arrivals; the whole loop is one CUDA graph per rank,
+    no collective call and no host round trip per iteration."""
     import torch
     import torch.distributed as dist
     rank, world = dist.get_rank(), dist.get_world_size()
     stream = torch.cuda.Stream(device=g.device)  # engine, copies and NCCL share it
     with torch.cuda.stream(stream):
+        if exchange == "peer":
+            return _run_peer_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ranks,
+                                rank, world)
+        if exchange != "nccl":
+            raise ValueError("exchange must be 'nccl' or 'peer'")
         return _run_distributed_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ranks,
                                    rank, world)
+
+
+def _ipc_export(ptr: int):
+    h = (C.c_char * 64)()
+    off = C.c_uint64()
+    check(lib().prgpu_ipc_export(C.c_void_p(ptr), h, C.byref(off)), "ipc export")
+    return bytes(h), off.value
+
+
+def _ipc_open(handle: bytes, offset: int, device: int) -> int:
+    p = C.c_void_p()
+    check(lib().prgpu_ipc_open((C.c_char * 64).from_buffer_copy(handle), offset, device, C.byref(p)),
+          "ipc open")
+    return p.value
+
+
+def _run_peer_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ranks, rank, world):
+    import torch
+    import torch.distributed as dist
+    part = _Part(g, alphas, tolerance, norm, max_iterations, stop_mask, rank, world, g.device, fused=True)
+    part.set_stream()
+    mine = [_ipc_export(t.data_ptr()) for t in (part.contrib, part.partials, part.arrive)] if world > 1 else []
+    table = [None] * world
+    if world > 1:
+        dist.all_gather_object(table, mine)
+    opened = []  # (ptr, offset) to close
+    peers = ([], [], [])
+    for r in range(world):
+        if r == rank:
+            continue
+        for j in range(3):
+            hnd, off = table[r][j]
+            ptr = _ipc_open(hnd, off, g.device)
+            opened.append((ptr, off))
+            peers[j].append(ptr)
+    try:
+        part.set_peers(*peers)
+        part.init()
+        torch.cuda.current_stream(part.contrib.device).synchronize()
+        if world > 1:
+            dist.barrier()  # every rank's counters are reset before anyone arrives
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        part.launch()
+        stop.record()
+        torch.cuda.current_stream(part.contrib.device).synchronize()
+        K = len(alphas)
+        lane_its = _lane_iterations(part)
+        res = PartResult(iterations=lane_its, ranks=None, run_iterations=int(lane_its.max()),
+                         loop_ms=start.elapsed_time(stop))
+        if world > 1:
+            dist.barrier()  # no peer still stores into our buffers
+        if want_ranks:
+            res.ranks = _gather_ranks(part, g, K, world)
+    finally:
+        for ptr, off in opened:
+            lib().prgpu_ipc_close(C.c_void_p(ptr), off)
+        part.close()
+    return res
 
 
 def _run_distributed_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ranks, rank, world):

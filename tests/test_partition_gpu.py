@@ -56,3 +56,48 @@ def test_nccl_world_of_one(prl):
             assert np.max(np.abs(got.ranks[k] - want.results[k].ranks)) <= 1e-13
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 3, 5])
+@pytest.mark.parametrize("alphas", [[0.85], [0.5, 0.85, 1.0]])
+def test_fused_peer_exchange_emulated(prl, nranks, alphas):
+    """The peer-memory exchange: each rank's kernels store into the other
+    ranks' buffers and count arrivals (ranks run one after another on this
+    GPU, so nothing waits); must equal the fused single-GPU run."""
+    from paper_2108_02997_b200 import distributed
+    g = prl.generate_rmat(14, 16, 0.57, 0.19, 0.19, 2108)
+    want = prl.pagerank_batched(g, alphas, 1e-9)
+    got = distributed.emulate(g, alphas, nranks, 1e-9, fused=True)
+    for k in range(len(alphas)):
+        assert got.iterations[k] == want.results[k].iterations
+        assert np.max(np.abs(got.ranks[k] - want.results[k].ranks)) <= 1e-13
+
+
+def test_fused_peer_graph_loop_single_rank(prl):
+    """One rank, the whole loop as the CUDA graph prgpu_part_launch enqueues
+    (the finalize kernel's arrival wait included)."""
+    from paper_2108_02997_b200 import distributed
+    g = prl.generate_rmat(14, 16, 0.57, 0.19, 0.19, 2108)
+    want = prl.pagerank_batched(g, [0.6, 0.85], 1e-9)
+    got = distributed.emulate(g, [0.6, 0.85], 1, 1e-9, fused=True, graph=True)
+    for k in range(2):
+        assert got.iterations[k] == want.results[k].iterations
+        assert np.max(np.abs(got.ranks[k] - want.results[k].ranks)) <= 1e-13
+
+
+def test_nccl_world_of_one_peer_exchange(prl):
+    import torch
+    import torch.distributed as dist
+    from paper_2108_02997_b200 import distributed
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = "29514"
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        g = prl.generate_rmat(14, 16, 0.57, 0.19, 0.19, 2108)
+        want = prl.pagerank_batched(g, [0.75, 0.85], 1e-8)
+        got = distributed.run_distributed(g, [0.75, 0.85], 1e-8, want_ranks=True, exchange="peer")
+        for k in range(2):
+            assert got.iterations[k] == want.results[k].iterations
+            assert np.max(np.abs(got.ranks[k] - want.results[k].ranks)) <= 1e-13
+    finally:
+        dist.destroy_process_group()
