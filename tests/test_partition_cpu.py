@@ -105,3 +105,90 @@ def test_split_rows_balanced(oracle):
     cost = np.diff(g.in_offsets.astype(np.int64)) + 2
     loads = [cost[a:b].sum() for a, b in parts]
     assert max(loads) <= 1.25 * (cost.sum() / 4) + cost.max()
+
+
+def peer_worker(rank, world, names, n, off, nbr, deg, alpha, tol, out):
+    """The fused peer-memory protocol of paper_2108_02997_b200 (pull.cuh,
+    Params::fused) restated with processes and shared memory: a rank stores
+    its new contribution rows and its partial vector straight into every
+    rank's buffers (partials in slot [iteration parity][rank]), then bumps
+    every rank's arrival counter; it reads the next iteration's inputs only
+    after its own counter reaches world * (iteration + 1)."""
+    import time
+    from multiprocessing import shared_memory
+    shm = {k: shared_memory.SharedMemory(name=v) for k, v in names.items()}
+    contrib = [np.ndarray((2, n), np.float64, buffer=shm[f"c{r}"].buf) for r in range(world)]
+    parts = [np.ndarray((2, world, 4), np.float64, buffer=shm[f"p{r}"].buf) for r in range(world)]
+    arrive = np.ndarray((world,), np.int64, buffer=shm["a"].buf)
+    locks = out["locks"]
+    lo, hi = split_rows(off, world)[rank]
+    dang = deg == 0
+    prev = np.full(hi - lo, 1.0 / n)                 # this rank's rows only
+    c0 = (1.0 - alpha) / n + alpha * (float(np.sum(dang)) / n) / n
+    it = 0
+    while True:
+        par = it & 1
+        c = contrib[rank][par]                       # every source's contribution, parity par
+        nxt = np.empty(hi - lo)
+        for i, v in enumerate(range(lo, hi)):
+            nxt[i] = c0 + alpha * sum(c[nbr[j]] for j in range(off[v], off[v + 1]))
+        d = nxt - prev
+        mine = np.array([np.sum(np.abs(d)), np.sum(d * d), np.max(np.abs(d)) if d.size else 0.0,
+                         float(np.sum(nxt[dang[lo:hi]]))])
+        new_c = np.where(deg[lo:hi] > 0, nxt / np.maximum(deg[lo:hi], 1), 0.0)
+        for r in range(world):                       # peer stores: rows and partials
+            contrib[r][par ^ 1][lo:hi] = new_c
+            parts[r][par][rank] = mine
+        for r in range(world):                       # then arrive everywhere
+            with locks[r]:
+                arrive[r] += 1
+        while arrive[rank] < world * (it + 1):       # the finalize kernel's wait
+            time.sleep(0.0005)
+        tot = np.zeros(4)
+        for r in range(world):                       # rank order
+            p = parts[rank][par][r]
+            tot[0] += p[0]; tot[1] += p[1]; tot[2] = max(tot[2], p[2]); tot[3] += p[3]
+        c0 = (1.0 - alpha) / n + alpha * tot[3] / n  # next teleport from the dangling sum
+        prev = nxt
+        it += 1
+        if not (tot[0] >= tol and it < 500):
+            break
+    if rank == 0:
+        out["q"].put(it)
+    for s in shm.values():
+        s.close()
+
+
+def test_peer_exchange_protocol_two_processes(oracle):
+    from multiprocessing import shared_memory
+    ctx = mp.get_context("spawn")
+    n, pairs = oracle.rmat(8, 8, 0.57, 0.19, 0.19, 11)
+    g = oracle.build_csr(n, pairs)
+    h = oracle.build_csr_handle(n, pairs)
+    want = oracle.pagerank(h, 0.85, 1e-9, "l1")
+    oracle.free_csr(h)
+    world = 2
+    deg = g.out_degree.astype(np.float64)
+    shms = {}
+    for r in range(world):
+        shms[f"c{r}"] = shared_memory.SharedMemory(create=True, size=2 * n * 8)
+        np.ndarray((2, n), np.float64, buffer=shms[f"c{r}"].buf)[0] = np.where(deg > 0, (1.0 / n) / np.maximum(deg, 1), 0)
+        shms[f"p{r}"] = shared_memory.SharedMemory(create=True, size=2 * world * 4 * 8)
+    shms["a"] = shared_memory.SharedMemory(create=True, size=world * 8)
+    np.ndarray((world,), np.int64, buffer=shms["a"].buf)[:] = 0
+    out = {"q": ctx.Queue(), "locks": [ctx.Lock() for _ in range(world)]}
+    names = {k: v.name for k, v in shms.items()}
+    procs = [ctx.Process(target=peer_worker, args=(r, world, names, n, g.in_offsets, g.in_neighbors,
+                                                   deg, 0.85, 1e-9, out)) for r in range(world)]
+    try:
+        for p in procs:
+            p.start()
+        it = out["q"].get(timeout=300)
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+        assert it == want["iterations"]
+    finally:
+        for s in shms.values():
+            s.close()
+            s.unlink()
