@@ -5,7 +5,9 @@ Each rank owns a contiguous, cost-balanced row range, pulls its rows from the
 full previous contribution vector, then the ranks all-gather (a) their new
 contribution rows and (b) their partial sums, and every rank reduces the
 partials in rank order.  The run must reproduce the single-process oracle:
-same iteration count, ranks within 1e-12."""
+same iteration count, ranks within 1e-12.  A second test restates the fused
+peer-memory exchange (stores into every rank's buffers, parity-blocked
+partials, arrival counters) with two processes over shared memory."""
 import os
 import sys
 
