@@ -64,6 +64,8 @@ CONFIGS = {
                kind="grid", side=4096, alphas=[0.85], tol=1e-10, norm=0, stop_mask=7),
     "c4": dict(workload="C4: RMAT-26 alpha .85 tau 1e-10 Linf", kind="rmat", scale=26,
                alphas=[0.85], tol=1e-10, norm=2),
+    "c5": dict(workload="C5: RMAT-28 alpha sweep {.75,.85,.95} batched K=3, tau 1e-6, L2",
+               kind="rmat", scale=28, alphas=[0.95, 0.85, 0.75], tol=1e-6, norm=1),
 }
 
 

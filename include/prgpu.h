@@ -88,6 +88,12 @@ PRGPU_API int prgpu_graph_get_info(const prgpu_graph* g, prgpu_graph_info* info)
  * in_offsets[n+1], in_neighbors[e], out_degree[n], dangling[dangling_count]. */
 PRGPU_API int prgpu_graph_download(const prgpu_graph* g, uint64_t* in_offsets, uint32_t* in_neighbors,
                          uint32_t* out_degree, uint32_t* dangling);
+/* In-neighbours of selected rows only (original ids, ascending per row, as
+ * in_neighbors): off[nrows+1] is always filled and *total set; nbr is
+ * filled when total <= cap.  For graphs too large to download whole (the
+ * scale-28 config); no reference counterpart (test/diagnostic call). */
+PRGPU_API int prgpu_graph_rows(const prgpu_graph* g, const uint32_t* rows, uint32_t nrows, uint64_t* off,
+                     uint32_t* nbr, uint64_t cap, uint64_t* total);
 PRGPU_API void prgpu_graph_free(prgpu_graph* g);
 
 /* ---- engine (replaces pagerank, pagerank.hpp:70-108) --------------------

@@ -411,6 +411,30 @@ int orc_pagerank(const orc_csr* g, double alpha, double tol, int norm, int max_i
     return 0;
 }
 
+/* One iteration of pagerank.hpp:85-93 for selected rows only, from the full
+ * previous rank vector: the dangling sum over ascending ids (:85-86, the
+ * dangling list is ascending, graph.hpp:230-231), the teleport (:87), and
+ * each row's in-neighbour sum in ascending source order (:89-92).  Lets the
+ * tests check a graph too large for a full oracle run (C5) one step at a
+ * time against the GPU's own previous iterate. */
+double orc_pagerank_step_rows(uint32_t n, const double* prev, const uint32_t* out_degree,
+                              double alpha, uint32_t nrows, const uint64_t* off,
+                              const uint32_t* nbr, double* out) {
+    double dangling_sum = 0.0;
+    for (uint32_t v = 0; v < n; ++v)
+        if (out_degree[v] == 0) dangling_sum += prev[v];
+    const double teleport = (1.0 - alpha) / n + alpha * dangling_sum / n;
+    for (uint32_t i = 0; i < nrows; ++i) {
+        double acc = 0.0;
+        for (uint64_t j = off[i]; j < off[i + 1]; ++j) {
+            const uint32_t u = nbr[j];
+            acc += prev[u] / out_degree[u];
+        }
+        out[i] = teleport + alpha * acc;
+    }
+    return teleport;
+}
+
 /* tests/support/dense_oracle.hpp:24-62 */
 int orc_dense_pagerank(uint32_t n, const uint32_t* pairs, uint64_t m, double alpha,
                        double tol, int norm, int max_iter, double* ranks_out,

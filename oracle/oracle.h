@@ -81,6 +81,12 @@ double orc_error_norm(int kind, const double* r, const double* s, uint64_t n);
 int orc_pagerank(const orc_csr* g, double alpha, double tol, int norm, int max_iter,
                  double* ranks_out, int* iterations, int* converged, double* err_trace);
 
+/* pagerank.hpp:85-93 for rows off/nbr (reference layout, ascending) from the
+ * full prev vector; returns the teleport term.  out[nrows]. */
+double orc_pagerank_step_rows(uint32_t n, const double* prev, const uint32_t* out_degree,
+                              double alpha, uint32_t nrows, const uint64_t* off,
+                              const uint32_t* nbr, double* out);
+
 /* tests/support/dense_oracle.hpp:24-62 */
 int orc_dense_pagerank(uint32_t n, const uint32_t* pairs, uint64_t m, double alpha,
                        double tol, int norm, int max_iter, double* ranks_out,

@@ -98,6 +98,9 @@ class Oracle:
         L.orc_dense_pagerank.argtypes = [C.c_uint32, _u32p, C.c_uint64, C.c_double, C.c_double,
                                          C.c_int, C.c_int, _f64p, C.POINTER(C.c_int),
                                          C.POINTER(C.c_int)]
+        L.orc_pagerank_step_rows.argtypes = [C.c_uint32, _f64p, _u32p, C.c_double, C.c_uint32,
+                                             _u64p, _u32p, _f64p]
+        L.orc_pagerank_step_rows.restype = C.c_double
         L.orc_estimate_iterations.argtypes = [C.c_double, C.c_double]
         L.orc_estimate_iterations.restype = C.c_int
         L.orc_hash64.argtypes = [C.c_void_p, C.c_uint64]
@@ -181,6 +184,18 @@ class Oracle:
         if trace:
             out["err_trace"] = tr[: it.value]
         return out
+
+    def step_rows(self, prev, out_degree, alpha, off, nbr):
+        """One reference iteration (pagerank.hpp:85-93) for the rows whose
+        in-neighbours are off/nbr, from the full previous vector.  Returns
+        (next values [rows], teleport)."""
+        prev = np.ascontiguousarray(prev, np.float64)
+        deg = np.ascontiguousarray(out_degree, np.uint32)
+        off = np.ascontiguousarray(off, np.uint64)
+        nbr = np.ascontiguousarray(nbr if len(nbr) else np.zeros(1, np.uint32), np.uint32)
+        out = np.zeros(max(len(off) - 1, 1), np.float64)
+        c0 = self.L.orc_pagerank_step_rows(prev.size, prev, deg, alpha, len(off) - 1, off, nbr, out)
+        return out[: len(off) - 1], c0
 
     def dense_pagerank(self, n, pairs, alpha, tol, norm, max_iter=500):
         pairs = np.ascontiguousarray(pairs, dtype=np.uint32)

@@ -27,7 +27,7 @@ EXPORTS = [
     "prgpu_part_step", "prgpu_part_finalize", "prgpu_part_active", "prgpu_part_local_ranks",
     "prgpu_part_local_ranks_device", "prgpu_part_set_peers", "prgpu_part_launch",
     "prgpu_ipc_export", "prgpu_ipc_open", "prgpu_ipc_close",
-    "prgpu_graph_permutation",
+    "prgpu_graph_permutation", "prgpu_graph_rows",
 ]
 
 
@@ -119,6 +119,7 @@ def lib():
             "prgpu_ipc_open": ([vp, u64, i32, C.POINTER(vp)], i32),
             "prgpu_ipc_close": ([vp, u64], i32),
             "prgpu_graph_permutation": ([vp, vp], i32),
+            "prgpu_graph_rows": ([vp, vp, C.c_uint32, vp, vp, C.c_uint64, vp], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

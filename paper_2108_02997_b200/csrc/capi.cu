@@ -47,6 +47,7 @@ int read_any_active(prgpu_session*);
 void part_plan_copy(prgpu_session*, prgpu_partition*);
 void part_set_stream(prgpu_session*, void*);
 void graph_permutation(const prgpu_graph*, uint32_t*);
+uint64_t graph_rows(const prgpu_graph*, const uint32_t*, uint32_t, uint64_t*, uint32_t*, uint64_t, cudaStream_t);
 void session_destroy(prgpu_session*);
 using SessionPtr = std::unique_ptr<prgpu_session, void (*)(prgpu_session*)>;
 double session_run(prgpu_session*);
@@ -167,6 +168,18 @@ int prgpu_graph_download(const prgpu_graph* g, uint64_t* off, uint32_t* nbr, uin
         prgpu::Stream st;
         prgpu::AllocScope scope(st);
         prgpu::graph_download(g, off, nbr, deg, dang, st);
+    });
+}
+
+int prgpu_graph_rows(const prgpu_graph* g, const uint32_t* rows, uint32_t nrows, uint64_t* off,
+                     uint32_t* nbr, uint64_t cap, uint64_t* total) {
+    return guarded([&] {
+        if (!g || (nrows && (!rows || !off))) prgpu::fail(PRGPU_EINVAL, "null argument");
+        prgpu::DeviceGuard dg(g->device);
+        prgpu::Stream st;
+        prgpu::AllocScope scope(st);
+        const uint64_t t = prgpu::graph_rows(g, rows, nrows, off, nbr, cap, st);
+        if (total) *total = t;
     });
 }
 

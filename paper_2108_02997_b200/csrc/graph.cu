@@ -348,6 +348,29 @@ __global__ void engine_to_orig_keys(const uint64_t* __restrict__ row_off,
     }
 }
 
+// in-degrees of requested original rows (graph_rows)
+__global__ void rows_deg(const uint64_t* __restrict__ row_off, const uint32_t* __restrict__ new_of_old,
+                         const uint32_t* __restrict__ rows, uint32_t nrows, uint64_t* __restrict__ cnt) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += gridDim.x * blockDim.x) {
+        const uint32_t r = new_of_old[rows[i]];
+        cnt[i] = row_off[r + 1] - row_off[r];
+    }
+}
+
+// in-neighbours (original ids, engine order) of requested rows: one warp per row
+__global__ void rows_fill(const uint64_t* __restrict__ row_off, const uint32_t* __restrict__ col,
+                          const uint32_t* __restrict__ row_of_src, const uint32_t* __restrict__ old_of_new,
+                          const uint32_t* __restrict__ new_of_old, const uint32_t* __restrict__ rows,
+                          uint32_t nrows, const uint64_t* __restrict__ out_off, uint32_t* __restrict__ out) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nrows;
+         i += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t r = new_of_old[rows[i]];
+        const uint64_t lo = row_off[r], d = row_off[r + 1] - lo;
+        for (uint64_t j = lane; j < d; j += 32) out[out_off[i] + j] = old_of_new[row_of_src[col[lo + j]]];
+    }
+}
+
 __global__ void in_deg_orig(const uint64_t* __restrict__ row_off,
                             const uint32_t* __restrict__ new_of_old, uint32_t n,
                             uint64_t* __restrict__ out) {
@@ -869,6 +892,37 @@ void graph_download(const prgpu_graph* g, uint64_t* h_off, uint32_t* h_nbr, uint
         PRGPU_CUDA(cudaMemcpyAsync(h_nbr, nb.p, e * 4, cudaMemcpyDeviceToHost, st));
         PRGPU_CUDA(cudaStreamSynchronize(st));
     }
+}
+
+// In-neighbours of selected original rows in the reference layout (ascending
+// per row): off[nrows+1] always filled; nbr (capacity cap) filled when it fits.
+// Test tooling for graphs too large to download whole (C5).
+uint64_t graph_rows(const prgpu_graph* g, const uint32_t* h_rows, uint32_t nrows, uint64_t* h_off,
+                    uint32_t* h_nbr, uint64_t cap, cudaStream_t st) {
+    for (uint32_t i = 0; i < nrows; ++i)
+        if (h_rows[i] >= g->n) fail(PRGPU_EINVAL, "graph_rows: row >= vertex_count");
+    h_off[0] = 0;
+    if (nrows == 0) return 0;
+    DevBuf<uint32_t> rows(nrows);
+    DevBuf<uint64_t> cnt((size_t)nrows + 1);
+    PRGPU_CUDA(cudaMemcpyAsync(rows.p, h_rows, (size_t)nrows * 4, cudaMemcpyHostToDevice, st));
+    rows_deg<<<grid_for(nrows), kThreads, 0, st>>>(g->row_off.p, g->new_of_old.p, rows.p, nrows, cnt.p);
+    PRGPU_LAUNCHED("rows_deg");
+    PRGPU_CUDA(cudaMemcpyAsync(h_off + 1, cnt.p, (size_t)nrows * 8, cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    for (uint32_t i = 0; i < nrows; ++i) h_off[i + 1] += h_off[i];
+    const uint64_t total = h_off[nrows];
+    if (!h_nbr || total > cap || total == 0) return total;
+    PRGPU_CUDA(cudaMemcpyAsync(cnt.p, h_off, ((size_t)nrows + 1) * 8, cudaMemcpyHostToDevice, st));
+    DevBuf<uint32_t> out(total);
+    rows_fill<<<grid_for((uint64_t)nrows * 32), kThreads, 0, st>>>(g->row_off.p, g->col.p, g->row_of_src.p,
+                                                                    g->old_of_new.p, g->new_of_old.p, rows.p,
+                                                                    nrows, cnt.p, out.p);
+    PRGPU_LAUNCHED("rows_fill");
+    PRGPU_CUDA(cudaMemcpyAsync(h_nbr, out.p, total * 4, cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    for (uint32_t i = 0; i < nrows; ++i) std::sort(h_nbr + h_off[i], h_nbr + h_off[i + 1]);
+    return total;
 }
 
 } // namespace prgpu

@@ -158,6 +158,28 @@ class CsrGraph:
         off = self.in_offsets
         return self.in_neighbors[int(off[v]):int(off[v + 1])]
 
+    def out_degree_only(self) -> np.ndarray:
+        """out_degree[n] without downloading the edge arrays."""
+        if self._host is not None:
+            return self._host[2]
+        deg = np.zeros(self.vertex_count, np.uint32)
+        check(lib().prgpu_graph_download(self._h, None, None, deg.ctypes.data, None), "download")
+        return deg
+
+    def rows(self, rows):
+        """(off[len(rows)+1], nbr): the in-neighbours of the given vertices,
+        ascending per row as in in_neighbors, without downloading the whole
+        graph (prgpu_graph_rows)."""
+        r = np.ascontiguousarray(rows, np.uint32)
+        off = np.zeros(len(r) + 1, np.uint64)
+        total = C.c_uint64()
+        check(lib().prgpu_graph_rows(self._h, r.ctypes.data, len(r), off.ctypes.data, None, 0,
+                                     C.byref(total)), "graph rows")
+        nbr = np.zeros(max(int(total.value), 1), np.uint32)
+        check(lib().prgpu_graph_rows(self._h, r.ctypes.data, len(r), off.ctypes.data, nbr.ctypes.data,
+                                     len(nbr), C.byref(total)), "graph rows")
+        return off, nbr[:int(total.value)]
+
 
 def _new_graph(fn, *args, device: Optional[int] = None) -> CsrGraph:
     dev = _lib.default_device() if device is None else device

@@ -158,3 +158,26 @@ def test_restatement_matches_reference_live(oracle, ref):
         assert oracle.error_norm(norm, rs[0], rs[1]) == ref.error_norm(norm, rs[0], rs[1])
     oracle.free_csr(ho)
     ref.free_csr(hr)
+
+
+def test_step_rows_is_one_reference_iteration(oracle):
+    """orc_pagerank_step_rows (the C5 one-step checker) reproduces iteration t
+    of the full restatement bit for bit from iteration t-1, on every row and on
+    a row subset (reference layout, ascending neighbours)."""
+    n, pairs = oracle.rmat(14, 16, 0.57, 0.19, 0.19, 9)
+    g = oracle.build_csr(n, pairs)
+    h = oracle.build_csr_handle(n, pairs)
+    for alpha in (0.5, 0.85, 1.0):
+        for t in (1, 2, 5):
+            prev = oracle.pagerank(h, alpha, 1e-30, "l1", max_iter=t - 1)["ranks"] if t > 1 \
+                else np.full(n, 1.0 / n)
+            nxt = oracle.pagerank(h, alpha, 1e-30, "l1", max_iter=t)["ranks"]
+            got, c0 = oracle.step_rows(prev, g.out_degree, alpha, g.in_offsets, g.in_neighbors)
+            assert np.array_equal(got, nxt), (alpha, t)
+            rows = np.arange(0, n, 37, dtype=np.uint32)
+            off = np.zeros(len(rows) + 1, np.uint64)
+            off[1:] = np.cumsum(g.in_offsets[rows + 1] - g.in_offsets[rows])
+            nbr = np.concatenate([g.in_neighbors[g.in_offsets[v]:g.in_offsets[v + 1]] for v in rows])
+            sub, _ = oracle.step_rows(prev, g.out_degree, alpha, off, nbr)
+            assert np.array_equal(sub, nxt[rows])
+    oracle.free_csr(h)

@@ -298,3 +298,19 @@ def test_batched_lane_modes_vs_oracle(prl, oracle, K):
         assert iterations_match(got.iterations, want["iterations"], want["err_trace"], tols[k]), k
         assert np.max(np.abs(got.ranks - want["ranks"])) <= RANK_TOL, k
     oracle.free_csr(h)
+
+
+def test_graph_rows_matches_download(prl):
+    """prgpu_graph_rows (row-sample download for graphs too large to pull back
+    whole) agrees with the full reference-layout download."""
+    g = prl.generate_rmat(14, 16, 0.57, 0.19, 0.19, 31)
+    n = g.vertex_count
+    rows = np.array([0, 5, n - 1] + list(range(100, n, 97)), np.uint32)
+    off, nbr = g.rows(rows)
+    full_off, full_nbr = g.in_offsets, g.in_neighbors
+    want = [full_nbr[full_off[v]:full_off[v + 1]] for v in rows]
+    assert np.array_equal(np.diff(off), [len(w) for w in want])
+    assert np.array_equal(nbr, np.concatenate(want))
+    assert np.array_equal(g.out_degree_only(), g.out_degree)
+    with pytest.raises(ValueError):
+        g.rows([n])
