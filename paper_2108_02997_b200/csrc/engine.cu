@@ -217,6 +217,12 @@ inline int variant() {
     return v ? std::atoi(v) : 0;
 }
 
+// per-mode instance alternatives (tuning only)
+inline int k_variant(const char* name) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : 0;
+}
+
 // `all_q`: the run needs every partial (all norms / the reference trace);
 // otherwise only L1 + dangling (the damping sweep's stopping rule).
 template <int LG, int W, int WIN, int QJ, int MINB, int QM, int KS, int PATHS = 3>
@@ -233,12 +239,13 @@ LaneCfg wide_cfg(bool all_q) {
 
 // Defaults measured on B200 (scripts/gpu_variants*.sh).
 // Wide lanes: two doubles per thread (one 16-byte load per edge), LG = KS/2
-// threads per edge, rows padded to whole 32-byte sectors.
+// threads per edge, rows padded to whole 32-byte sectors; up to four lanes,
+// one double per thread (LG = KS).
 template <int PATHS>
 LaneCfg lane_cfg_t(int K, bool all_q) {
     if (K == 1) return mk_cfg<1, 1, 256, 2, 3, kQmAll, 0, PATHS>();
-    if (K == 2) return wide_cfg<1, 2, 64, 4, 2, PATHS>(all_q);
-    if (K <= 4) return wide_cfg<2, 2, 128, 4, 4, PATHS>(all_q);
+    if (K == 2) return wide_cfg<2, 1, 64, 4, 2, PATHS>(all_q);
+    if (K <= 4) return wide_cfg<4, 1, 128, 4, 4, PATHS>(all_q);
     if (K <= 8) return wide_cfg<4, 2, 128, 4, 8, PATHS>(all_q);
     if (K <= 12) return wide_cfg<8, 2, 128, 4, 12, PATHS>(all_q);
     return wide_cfg<8, 2, 128, 4, 16, PATHS>(all_q);
@@ -263,21 +270,35 @@ inline LaneCfg lane_cfg(int K, bool all_q) {
     return lane_cfg_t<3>(K, all_q);
 }
 
-// Lane-width modes of a K > 1 run (Params::mode_id): the same row stride KS,
-// window and task tables, a lane group of kp/2 threads.  Returns false when
-// (KS, kp) has no instance.
 // Lane-width modes of a K > 1 run (Params::mode_id): the same window and task
-// tables, a lane group of kp/2 threads; a narrow mode's contribution rows hold
+// tables (an instance's WIN must be >= the run's: its shared-memory stage is
+// sized by it); a narrow mode's contribution rows hold
 // just its kp lanes (KS = kp), the widest mode's the run's full stride.
 // Returns false when (KS, kp) has no instance.
+// k1_minb4: a K = 1 run split into its two kernels (win 256), bit PATHS-1
+// set: that kernel at 4 CTAs/SM instead of 3.
 template <int PATHS>
-bool mode_cfg(int KS, int kp, bool all_q, LaneCfg& out) {
+bool mode_cfg(int KS, int kp, int win, bool all_q, LaneCfg& out, int k1_minb4 = 0) {
+    if (win == 256 && KS == 1 && kp == 1) {
+        if ((k1_minb4 >> (PATHS - 1)) & 1) out = mk_cfg<1, 1, 256, 2, 4, kQmAll, 1, PATHS>();
+        else out = mk_cfg<1, 1, 256, 2, 3, kQmAll, 1, PATHS>();
+        return true;
+    }
     switch (KS * 100 + kp) {
     case 101:
         out = all_q ? mk_cfg<1, 1, 128, 2, 3, kQmAll, 1, PATHS>() : mk_cfg<1, 1, 128, 2, 3, kQmL1, 1, PATHS>();
         return true;
-    case 202: out = wide_cfg<1, 2, 128, 4, 2, PATHS>(all_q); return true;
-    case 404: out = wide_cfg<2, 2, 128, 4, 4, PATHS>(all_q); return true;
+    // two- and four-lane modes: one 8-byte lane per thread (LG = kp), measured
+    // -9% per C5 sweep against two lanes per thread (PRGPU_K4CFG=1 /
+    // PRGPU_K2CFG=1 select the two-lane-per-thread instances: tuning only)
+    case 202:
+        if (k_variant("PRGPU_K2CFG") == 1) { out = wide_cfg<1, 2, 128, 4, 2, PATHS>(all_q); return true; }
+        out = wide_cfg<2, 1, 128, 4, 2, PATHS>(all_q);
+        return true;
+    case 404:
+        if (k_variant("PRGPU_K4CFG") == 1) { out = wide_cfg<2, 2, 128, 4, 4, PATHS>(all_q); return true; }
+        out = wide_cfg<4, 1, 128, 4, 4, PATHS>(all_q);
+        return true;
     case 808: out = wide_cfg<4, 2, 128, 4, 8, PATHS>(all_q); return true;
     case 1216: out = wide_cfg<8, 2, 128, 4, 12, PATHS>(all_q); return true;
     case 1616: out = wide_cfg<8, 2, 128, 4, 16, PATHS>(all_q); return true;
@@ -735,19 +756,30 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     // pair per lane-width mode (narrowest first): a hub-chunk kernel that only
     // leaves CTA partials and a packed + empty kernel that finalizes; once the
     // live lanes fit a narrower mode the wide pairs exit at once.  Multi-GPU
-    // partitions and K = 1 run the one base kernel.
+    // partitions run the one base kernel; K = 1 see below.
     std::vector<std::pair<int, std::pair<LaneCfg, LaneCfg>>> modes; // kp, (chunk, packed)
     {
         const char* sp = std::getenv("PRGPU_SPLIT");   // =0: base kernel only (tuning)
         const char* mm = std::getenv("PRGPU_MODES");   // =0: widest mode only (tuning)
-        const bool modal = nranks == 0 && s->K > 1 && !(sp && std::atoi(sp) == 0) && variant() == 0;
+        // K = 1 splits into the hub-chunk and packed kernels on large graphs
+        // (measured C4 -4%) and on graphs without hub rows, where the packed
+        // kernel then runs at 4 CTAs/SM (C3 -19%); on C2's graph (-2.5%) and
+        // small graphs (launch-bound) the one kernel wins.  PRGPU_K1SPLIT=0/1
+        // and PRGPU_K1MINB (bit 0 hub, bit 1 packed kernel) override (tuning).
+        const char* ks1 = std::getenv("PRGPU_K1SPLIT");
+        const bool k1auto = P.n_chunk == 0 ? g->e >= (1ull << 24) : g->e >= (1ull << 29);
+        const bool k1split = s->K == 1 && (ks1 ? std::atoi(ks1) == 1 : k1auto);
+        const char* km = std::getenv("PRGPU_K1MINB");
+        const int k1_minb4 = km ? std::atoi(km) : (P.n_chunk == 0 ? 2 : 0);
+        const bool modal = nranks == 0 && (s->K > 1 || k1split) && !(sp && std::atoi(sp) == 0) && variant() == 0;
         if (modal) {
             const int wide = s->cfg.KP(); // (measured: 12 lanes as 4 threads x 3 lost 30%)
             for (int kp = 1; kp <= wide; kp *= 2) {
                 if (kp < wide && mm && std::atoi(mm) == 0) continue;
                 LaneCfg a, b;
                 const int ks = kp == wide ? s->cfg.KS : kp;
-                if (mode_cfg<1>(ks, kp, s->all_q, a) && mode_cfg<2>(ks, kp, s->all_q, b))
+                if (mode_cfg<1>(ks, kp, s->cfg.WIN, s->all_q, a, k1_minb4) &&
+                    mode_cfg<2>(ks, kp, s->cfg.WIN, s->all_q, b, k1_minb4))
                     modes.push_back({kp, {a, b}});
             }
             if (modes.empty() || modes.back().first != wide) modes.clear(); // no instances: base kernel
