@@ -428,9 +428,19 @@ def run_partitioned(args, cfg):
     else:
         g = prl.generate_grid(cfg["side"], 0.6, 0.01, SEED, device=local)
     n, e = g.vertex_count, g.edge_count()
+    # the fused exchange stores into the peers' memory: every pair of local
+    # GPUs must have peer access, agreed on by all ranks; else NCCL calls
+    exchange, fallback = args.exchange, None
+    if exchange == "peer" and world > 1:
+        ok = all(torch.cuda.can_device_access_peer(local, j) for j in range(world) if j != local)
+        flag = torch.tensor([1 if ok else 0], device=f"cuda:{local}")
+        tdist.all_reduce(flag, op=tdist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            exchange, fallback = "nccl", "no peer access between every pair of GPUs: NCCL exchange"
+    args.exchange = exchange
     run = lambda: distributed.run_distributed(g, cfg["alphas"], cfg["tol"],  # noqa: E731
                                               prl.NormKind(cfg["norm"]), 500, cfg.get("stop_mask", 0),
-                                              exchange=args.exchange)
+                                              exchange=exchange)
     for _ in range(args.warmup):
         r = run()
     iters = r.iterations
@@ -500,7 +510,7 @@ def run_partitioned(args, cfg):
                            "fused peer-memory exchange (NVLink stores from the pull kernel, CUDA graph loop)"
                            if args.exchange == "peer" else "NCCL exchange per iteration"),
                        "timed_scope": "iteration loop incl. exchange, CUDA events, max over ranks",
-                       "wall_s": wall},
+                       "exchange_fallback": fallback, "wall_s": wall},
             "gpu_launches": args.steps * r.run_iterations * 2,
             "clocks": clk.summary(),
             "roofline": roof,

@@ -27,7 +27,9 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <filesystem>
+#include <iterator>
 #include <fstream>
 #include <functional>
 #include <istream>
@@ -163,99 +165,31 @@ private:
 };
 
 namespace detail {
-inline std::string_view trim(std::string_view s) {
-    while (!s.empty() && (s.back() == '\r' || s.back() == ' ' || s.back() == '\t')) s.remove_suffix(1);
-    while (!s.empty() && (s.front() == ' ' || s.front() == '\t')) s.remove_prefix(1);
-    return s;
-}
-inline std::vector<std::string_view> fields(std::string_view line) {
-    std::vector<std::string_view> out;
-    std::size_t i = 0;
-    while (i < line.size()) {
-        while (i < line.size() && (line[i] == ' ' || line[i] == '\t')) ++i;
-        const std::size_t b = i;
-        while (i < line.size() && line[i] != ' ' && line[i] != '\t') ++i;
-        if (i > b) out.push_back(line.substr(b, i - b));
-    }
-    return out;
-}
-inline std::string lower(std::string_view s) {
-    std::string o(s);
-    for (char& c : o) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
-    return o;
-}
-template <typename T>
-bool to_num(std::string_view tok, T& out) {
-    auto [p, ec] = std::from_chars(tok.data(), tok.data() + tok.size(), out);
-    return ec == std::errc{} && p == tok.data() + tok.size();
+// pairs from prgpu_mtx_parse / prgpu_mtx_load into an EdgeList
+inline EdgeList take_pairs(std::uint32_t n, std::uint32_t* pairs, std::uint64_t m) {
+    EdgeList el;
+    el.vertex_count = n;
+    el.edges.resize(m);
+    static_assert(sizeof(std::pair<std::uint32_t, std::uint32_t>) == 8);
+    if (m) std::memcpy(el.edges.data(), pairs, m * 8);
+    prgpu_pairs_free(pairs);
+    return el;
 }
 } // namespace detail
 
-/// MatrixMarket coordinate parser (host text I/O; graph.hpp:111-199 semantics).
+/// graph.hpp:111-199: the library's multi-threaded MatrixMarket parser
+/// (prgpu_mtx_parse), same language, same MtxParseError lines and messages.
 inline EdgeList parse_matrix_market(std::istream& in) {
-    std::string line;
-    std::size_t ln = 0;
-    if (!std::getline(in, line)) throw MtxParseError(1, "empty input, no banner");
-    ++ln;
-    const auto b = detail::fields(detail::trim(line));
-    if (b.size() != 5 || b[0] != "%%MatrixMarket") throw MtxParseError(ln, "malformed MatrixMarket banner");
-    const std::string obj = detail::lower(b[1]), fmt = detail::lower(b[2]), fld = detail::lower(b[3]),
-                      sym = detail::lower(b[4]);
-    if (obj != "matrix") throw MtxParseError(ln, "unsupported object '" + obj + "' (want matrix)");
-    if (fmt != "coordinate") throw MtxParseError(ln, "unsupported format '" + fmt + "' (want coordinate)");
-    if (fld != "pattern" && fld != "real" && fld != "integer")
-        throw MtxParseError(ln, "unsupported field '" + fld + "' (want pattern, real or integer)");
-    if (sym != "general" && sym != "symmetric")
-        throw MtxParseError(ln, "unsupported symmetry '" + sym + "' (want general or symmetric)");
-    const bool symmetric = sym == "symmetric", weighted = fld != "pattern";
-    std::uint64_t rows = 0, cols = 0, entries = 0;
-    for (;;) {
-        if (!std::getline(in, line)) throw MtxParseError(ln + 1, "unexpected end of file before size line");
-        ++ln;
-        const auto body = detail::trim(line);
-        if (body.empty() || body.front() == '%') continue;
-        const auto f = detail::fields(body);
-        if (f.size() != 3 || !detail::to_num(f[0], rows) || !detail::to_num(f[1], cols) ||
-            !detail::to_num(f[2], entries))
-            throw MtxParseError(ln, "size line must be three integers (rows cols entries)");
-        break;
+    const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    std::uint32_t n = 0, *pairs = nullptr;
+    std::uint64_t m = 0, line = 0;
+    const int st = prgpu_mtx_parse(text.data(), text.size(), 0, &n, &pairs, &m, &line);
+    if (st == PRGPU_EPARSE) {
+        const std::string msg = prgpu_last_error(), prefix = "line " + std::to_string(line) + ": ";
+        throw MtxParseError(line, msg.rfind(prefix, 0) == 0 ? msg.substr(prefix.size()) : msg);
     }
-    const std::uint64_t n = std::max(rows, cols);
-    if (n == 0) throw MtxParseError(ln, "graph has no vertices");
-    if (n > UINT32_MAX) throw MtxParseError(ln, "vertex count exceeds 2^32-1");
-    EdgeList el;
-    el.vertex_count = static_cast<std::uint32_t>(n);
-    el.edges.reserve(symmetric ? 2 * entries : entries);
-    std::uint64_t seen = 0;
-    while (seen < entries) {
-        if (!std::getline(in, line))
-            throw MtxParseError(ln + 1, "unexpected end of file: got " + std::to_string(seen) + " of " +
-                                            std::to_string(entries) + " entries");
-        ++ln;
-        const auto body = detail::trim(line);
-        if (body.empty() || body.front() == '%') continue;
-        const auto f = detail::fields(body);
-        const std::size_t expect = weighted ? 3 : 2;
-        if (f.size() != expect)
-            throw MtxParseError(ln, "expected " + std::to_string(expect) + " fields, got " +
-                                        std::to_string(f.size()));
-        std::uint64_t r = 0, c = 0;
-        if (!detail::to_num(f[0], r) || !detail::to_num(f[1], c))
-            throw MtxParseError(ln, "entry indices must be integers");
-        if (r < 1 || r > rows || c < 1 || c > cols)
-            throw MtxParseError(ln, "entry (" + std::to_string(r) + ", " + std::to_string(c) +
-                                        ") out of range for " + std::to_string(rows) + " x " +
-                                        std::to_string(cols));
-        if (weighted) {
-            double w = 0;
-            if (!detail::to_num(f[2], w)) throw MtxParseError(ln, "entry weight is not a number");
-        }
-        const auto s = static_cast<std::uint32_t>(r - 1), d = static_cast<std::uint32_t>(c - 1);
-        el.edges.emplace_back(s, d);
-        if (symmetric && s != d) el.edges.emplace_back(d, s);
-        ++seen;
-    }
-    return el;
+    detail::check(st, "parse_matrix_market");
+    return detail::take_pairs(n, pairs, m);
 }
 
 namespace detail {
@@ -288,18 +222,25 @@ inline CsrGraph build_csr(EdgeList el) {
     return detail::download(g);
 }
 
+/// graph.hpp:238-247: file parsed in place (mmap) by all host threads;
+/// errors name the file (std::runtime_error).
 inline EdgeList load_matrix_market(const std::filesystem::path& path) {
-    std::ifstream in(path);
-    if (!in) throw std::runtime_error("cannot open graph file: " + path.string());
-    try {
-        return parse_matrix_market(in);
-    } catch (const MtxParseError& e) {
-        throw std::runtime_error(path.string() + ": " + e.what());
-    }
+    std::uint32_t n = 0, *pairs = nullptr;
+    std::uint64_t m = 0, line = 0;
+    const int st = prgpu_mtx_load(path.string().c_str(), 0, &n, &pairs, &m, &line);
+    if (st == PRGPU_EPARSE || st == PRGPU_EIO) throw std::runtime_error(prgpu_last_error());
+    detail::check(st, "load_matrix_market");
+    return detail::take_pairs(n, pairs, m);
 }
 
+/// graph.hpp:249-251: parallel parse, build_csr on the device.
 inline CsrGraph load_csr_graph(const std::filesystem::path& path) {
-    return build_csr(load_matrix_market(path));
+    prgpu_graph* g = nullptr;
+    std::uint64_t line = 0;
+    const int st = prgpu_graph_load_mtx(path.string().c_str(), 0, detail::default_device(), &g, &line);
+    if (st == PRGPU_EPARSE || st == PRGPU_EIO) throw std::runtime_error(prgpu_last_error());
+    detail::check(st, "load_csr_graph");
+    return detail::download(g);
 }
 
 // ---------------------------------------------------------------------------

@@ -37,6 +37,8 @@ extern "C" {
 #define PRGPU_ECUDA 2  /* CUDA runtime or kernel failure                       */
 #define PRGPU_ENCCL 3  /* NCCL failure (multi-GPU)                             */
 #define PRGPU_ENOMEM 4 /* device allocation failed                             */
+#define PRGPU_EPARSE 5 /* MatrixMarket syntax error: MtxParseError(line)       */
+#define PRGPU_EIO 6    /* a file cannot be opened / read: std::runtime_error    */
 
 /* ---- norms (norms.hpp:18 NormKind) -------------------------------------- */
 #define PRGPU_NORM_L1 0
@@ -94,6 +96,23 @@ PRGPU_API int prgpu_graph_download(const prgpu_graph* g, uint64_t* in_offsets, u
  * scale-28 config); no reference counterpart (test/diagnostic call). */
 PRGPU_API int prgpu_graph_rows(const prgpu_graph* g, const uint32_t* rows, uint32_t nrows, uint64_t* off,
                      uint32_t* nbr, uint64_t cap, uint64_t* total);
+/* ---- MatrixMarket ingest (replaces parse_matrix_market / load_matrix_market /
+ * load_csr_graph, graph.hpp:111-199,238-251) -------------------------------
+ * Same language and errors as the reference (banner, size line, entries,
+ * symmetric expansion, weights validated and discarded, first error in file
+ * order with its 1-based line), parsed by `threads` host threads (<= 0: all
+ * cores).  On a syntax error: PRGPU_EPARSE, *err_line = the line, and
+ * prgpu_last_error() = "line L: what" ("<path>: line L: what" for files);
+ * a file that cannot be opened: PRGPU_EIO, "cannot open graph file: <path>".
+ * pairs: malloc'd (source, target) u32 pairs, release with prgpu_pairs_free. */
+PRGPU_API int prgpu_mtx_parse(const char* text, uint64_t len, int threads, uint32_t* n, uint32_t** pairs,
+                    uint64_t* m, uint64_t* err_line);
+PRGPU_API int prgpu_mtx_load(const char* path, int threads, uint32_t* n, uint32_t** pairs, uint64_t* m,
+                   uint64_t* err_line);
+PRGPU_API void prgpu_pairs_free(uint32_t* pairs);
+/* load_csr_graph(path): parse in parallel, then build_csr on the device. */
+PRGPU_API int prgpu_graph_load_mtx(const char* path, int threads, int device, prgpu_graph** out,
+                         uint64_t* err_line);
 PRGPU_API void prgpu_graph_free(prgpu_graph* g);
 
 /* ---- engine (replaces pagerank, pagerank.hpp:70-108) --------------------

@@ -310,6 +310,33 @@ class Ref:
             return self.L.ref_build_csr(n, pairs, 0)
         return self.L.ref_build_csr(n, pairs, pairs.size // 2)
 
+    def parse_mtx(self, text: bytes):
+        """parse_matrix_market (graph.hpp:111-199): (n, pairs[m,2]) or raises
+        ValueError((line, what))."""
+        L = self.L
+        L.ref_parse_mtx.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64), C.c_char_p, C.c_int]
+        L.ref_parse_mtx.restype = C.c_void_p
+        line = C.c_uint64()
+        msg = C.create_string_buffer(512)
+        h = L.ref_parse_mtx(text, len(text), C.byref(line), msg, 512)
+        if not h:
+            raise ValueError((int(line.value), msg.value.decode()))
+        n, pairs = self._take(h)
+        return n, np.asarray(pairs, np.uint32).reshape(-1, 2)
+
+    def load_mtx(self, path: str):
+        """load_matrix_market (graph.hpp:238-247): (n, pairs) or raises
+        RuntimeError(what)."""
+        L = self.L
+        L.ref_load_mtx.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+        L.ref_load_mtx.restype = C.c_void_p
+        msg = C.create_string_buffer(4096)
+        h = L.ref_load_mtx(path.encode(), msg, 4096)
+        if not h:
+            raise RuntimeError(msg.value.decode())
+        n, pairs = self._take(h)
+        return n, np.asarray(pairs, np.uint32).reshape(-1, 2)
+
     def free_csr(self, h):
         self.L.ref_csr_free(h)
 

@@ -11,10 +11,14 @@
 //   estimate_iterations pagerank.hpp:113-123
 //   random_digraph / regular_ring / scale_free_web  tests/support/graph_gen.hpp:21-85
 //   dense_pagerank   tests/support/dense_oracle.hpp:24-62
+//   parse_matrix_market / load_matrix_market  graph.hpp:111-199,238-247
 // Used to pin the oracle/oracle.c restatement, to write tests/golden/, and as
 // the CPU baseline ("kind": "reference") in bench.py.
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <sstream>
+#include <string>
 #include <random>
 #include <span>
 #include <stdexcept>
@@ -161,5 +165,30 @@ void* ref_csr_from_arrays(uint32_t n, const uint64_t* off, const uint32_t* nbr,
     for (uint32_t v = 0; v < n; ++v)
         if (g->out_degree[v] == 0) g->dangling.push_back(v); // graph.hpp:230-231
     return g;
+}
+}
+
+extern "C" {
+// parse_matrix_market (graph.hpp:111-199) on an in-memory stream: the
+// EdgeList (free with ref_edges_free), or null with the MtxParseError's line
+// and what() in err_line / msg.
+void* ref_parse_mtx(const char* text, uint64_t len, uint64_t* err_line, char* msg, int cap) {
+    std::istringstream in(std::string(text, len));
+    try {
+        return new EdgeList(parse_matrix_market(in));
+    } catch (const MtxParseError& e) {
+        *err_line = e.line();
+        std::snprintf(msg, (size_t)cap, "%s", e.what());
+        return nullptr;
+    }
+}
+// load_matrix_market (graph.hpp:238-247): errors as runtime_error what()
+void* ref_load_mtx(const char* path, char* msg, int cap) {
+    try {
+        return new EdgeList(load_matrix_market(path));
+    } catch (const std::exception& e) {
+        std::snprintf(msg, (size_t)cap, "%s", e.what());
+        return nullptr;
+    }
 }
 }

@@ -13,6 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PRGPU_LIB") or os.path.join(HERE, "libprgpu.so")  # override: tuning builds
 
 PRGPU_OK, PRGPU_EINVAL, PRGPU_ECUDA, PRGPU_ENCCL, PRGPU_ENOMEM = 0, 1, 2, 3, 4
+PRGPU_EPARSE, PRGPU_EIO = 5, 6
 MAX_LANES = 16
 
 # Every symbol include/prgpu.h declares (checked by tests/test_abi.py).
@@ -28,6 +29,7 @@ EXPORTS = [
     "prgpu_part_local_ranks_device", "prgpu_part_set_peers", "prgpu_part_launch",
     "prgpu_ipc_export", "prgpu_ipc_open", "prgpu_ipc_close",
     "prgpu_graph_permutation", "prgpu_graph_rows",
+    "prgpu_mtx_parse", "prgpu_mtx_load", "prgpu_pairs_free", "prgpu_graph_load_mtx",
 ]
 
 
@@ -120,6 +122,10 @@ def lib():
             "prgpu_ipc_close": ([vp, u64], i32),
             "prgpu_graph_permutation": ([vp, vp], i32),
             "prgpu_graph_rows": ([vp, vp, C.c_uint32, vp, vp, C.c_uint64, vp], i32),
+            "prgpu_mtx_parse": ([C.c_char_p, C.c_uint64, i32, vp, vp, vp, vp], i32),
+            "prgpu_mtx_load": ([C.c_char_p, i32, vp, vp, vp, vp], i32),
+            "prgpu_pairs_free": ([vp], None),
+            "prgpu_graph_load_mtx": ([C.c_char_p, i32, i32, vp, vp], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

@@ -7,6 +7,12 @@
 #include <string>
 
 #include "common.cuh"
+#include "mtx.h"
+
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 namespace prgpu {
 std::atomic<uint64_t> g_launches{0};
@@ -47,6 +53,7 @@ int read_any_active(prgpu_session*);
 void part_plan_copy(prgpu_session*, prgpu_partition*);
 void part_set_stream(prgpu_session*, void*);
 void graph_permutation(const prgpu_graph*, uint32_t*);
+
 uint64_t graph_rows(const prgpu_graph*, const uint32_t*, uint32_t, uint64_t*, uint32_t*, uint64_t, cudaStream_t);
 void session_destroy(prgpu_session*);
 using SessionPtr = std::unique_ptr<prgpu_session, void (*)(prgpu_session*)>;
@@ -180,6 +187,86 @@ int prgpu_graph_rows(const prgpu_graph* g, const uint32_t* rows, uint32_t nrows,
         prgpu::AllocScope scope(st);
         const uint64_t t = prgpu::graph_rows(g, rows, nrows, off, nbr, cap, st);
         if (total) *total = t;
+    });
+}
+
+// ---- MatrixMarket ingest (graph.hpp:111-199, 238-251) ----------------------------
+namespace {
+// the file's bytes, mapped read-only (empty files are an empty view)
+struct Mapped {
+    const char* p = nullptr;
+    uint64_t len = 0;
+    int fd = -1;
+    explicit Mapped(const char* path) {
+        fd = ::open(path, O_RDONLY);
+        if (fd < 0) prgpu::fail(PRGPU_EIO, std::string("cannot open graph file: ") + path);
+        struct stat st {};
+        if (::fstat(fd, &st) != 0) prgpu::fail(PRGPU_EIO, std::string("cannot open graph file: ") + path);
+        len = (uint64_t)st.st_size;
+        if (len) {
+            void* m = ::mmap(nullptr, len, PROT_READ, MAP_PRIVATE, fd, 0);
+            if (m == MAP_FAILED) prgpu::fail(PRGPU_EIO, std::string("cannot read graph file: ") + path);
+            ::madvise(m, len, MADV_SEQUENTIAL);
+            p = static_cast<const char*>(m);
+        }
+    }
+    ~Mapped() {
+        if (p) ::munmap(const_cast<char*>(p), len);
+        if (fd >= 0) ::close(fd);
+    }
+};
+
+// parse errors: PRGPU_EPARSE, message "line L: what" (MtxParseError::what),
+// prefixed with "<path>: " for files (load_matrix_market, graph.hpp:243-246)
+prgpu::MtxResult parse_or_fail(const char* text, uint64_t len, int threads, const char* path,
+                               uint64_t* err_line) {
+    prgpu::MtxResult r = prgpu::mtx_parse(text, len, threads);
+    if (r.err_line || !r.err_what.empty()) {
+        if (err_line) *err_line = r.err_line;
+        std::string msg = "line " + std::to_string(r.err_line) + ": " + r.err_what;
+        if (path) msg = std::string(path) + ": " + msg;
+        std::free(r.pairs);
+        prgpu::fail(r.err_line ? PRGPU_EPARSE : PRGPU_ENOMEM, msg);
+    }
+    return r;
+}
+} // namespace
+
+int prgpu_mtx_parse(const char* text, uint64_t len, int threads, uint32_t* n, uint32_t** pairs, uint64_t* m,
+                    uint64_t* err_line) {
+    return guarded([&] {
+        if ((!text && len) || !n || !pairs || !m) prgpu::fail(PRGPU_EINVAL, "null argument");
+        if (err_line) *err_line = 0;
+        prgpu::MtxResult r = parse_or_fail(text, len, threads, nullptr, err_line);
+        *n = r.n;
+        *m = r.m;
+        *pairs = r.pairs;
+    });
+}
+
+int prgpu_mtx_load(const char* path, int threads, uint32_t* n, uint32_t** pairs, uint64_t* m,
+                   uint64_t* err_line) {
+    return guarded([&] {
+        if (!path || !n || !pairs || !m) prgpu::fail(PRGPU_EINVAL, "null argument");
+        if (err_line) *err_line = 0;
+        Mapped f(path);
+        prgpu::MtxResult r = parse_or_fail(f.p, f.len, threads, path, err_line);
+        *n = r.n;
+        *m = r.m;
+        *pairs = r.pairs;
+    });
+}
+
+void prgpu_pairs_free(uint32_t* pairs) { std::free(pairs); }
+
+int prgpu_graph_load_mtx(const char* path, int threads, int device, prgpu_graph** out, uint64_t* err_line) {
+    if (!path) { t_last_error = "null path"; return PRGPU_EINVAL; }
+    if (err_line) *err_line = 0;
+    return make_graph(device, out, [&](cudaStream_t st) {
+        Mapped f(path);
+        prgpu::MtxResult r = parse_or_fail(f.p, f.len, threads, path, err_line);
+        std::unique_ptr<uint32_t, void (*)(void*)> keep(r.pairs, std::free);
+        return prgpu::graph_build_host(r.n, r.pairs, r.m, device, st);
     });
 }
 

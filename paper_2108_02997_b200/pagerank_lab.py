@@ -224,109 +224,64 @@ def generate_grid(side: int, p: float = 0.6, longrange_frac: float = 0.01, seed:
                       device=device)
 
 
-# ---- MatrixMarket (host text I/O; graph.hpp:111-199, out of the accelerated scope) ----
+# ---- MatrixMarket (graph.hpp:111-199, 238-251): the library's parallel parser ----
 
-def _parse_int(tok: str) -> Optional[int]:
-    if not tok or not all(ch.isdigit() for ch in tok):
-        return None
-    return int(tok)
-
-
-def _parse_number(tok: str) -> bool:
+def _mtx_pairs(call) -> EdgeList:
+    """Runs prgpu_mtx_parse / prgpu_mtx_load (`call` gets the output refs) and
+    turns the result into an EdgeList; PRGPU_EPARSE comes back as
+    (line, message)."""
+    n, m, line = C.c_uint32(), C.c_uint64(), C.c_uint64()
+    pairs = C.POINTER(C.c_uint32)()
+    st = call(C.byref(n), C.byref(pairs), C.byref(m), C.byref(line))
+    if st != _lib.PRGPU_OK:
+        msg = lib().prgpu_last_error().decode(errors="replace")
+        return st, int(line.value), msg
     try:
-        float(tok)
-    except ValueError:
-        return False
-    return tok.lower() not in ("nan", "inf", "-inf", "+inf", "infinity") or True
+        arr = np.ctypeslib.as_array(pairs, shape=(2 * int(m.value),)).copy() if m.value else \
+            np.zeros(0, np.uint32)
+    finally:
+        lib().prgpu_pairs_free(pairs)
+    return EdgeList(int(n.value), arr.reshape(-1, 2))
 
 
-def parse_matrix_market(text: str) -> EdgeList:
-    """graph.hpp:111-199: coordinate pattern|real|integer, general|symmetric."""
-    lines = text.split("\n")
-    if text == "" or not lines:
-        raise MtxParseError(1, "empty input, no banner")
-    banner = lines[0].strip(" \t\r").split()
-    if len(banner) != 5 or banner[0] != "%%MatrixMarket":
-        raise MtxParseError(1, "malformed MatrixMarket banner")
-    obj, fmt, fld, sym = (t.lower() for t in banner[1:])
-    if obj != "matrix":
-        raise MtxParseError(1, f"unsupported object '{obj}' (want matrix)")
-    if fmt != "coordinate":
-        raise MtxParseError(1, f"unsupported format '{fmt}' (want coordinate)")
-    if fld not in ("pattern", "real", "integer"):
-        raise MtxParseError(1, f"unsupported field '{fld}' (want pattern, real or integer)")
-    if sym not in ("general", "symmetric"):
-        raise MtxParseError(1, f"unsupported symmetry '{sym}' (want general or symmetric)")
-    symmetric, has_weight = sym == "symmetric", fld != "pattern"
-    i = 1
-    # an input ending in "\n" yields a trailing "" that is not a line
-    nlines = len(lines) - 1 if lines and lines[-1] == "" else len(lines)
-    while True:
-        if i >= nlines:
-            raise MtxParseError(i + 1, "unexpected end of file before size line")
-        body = lines[i].strip(" \t\r")
-        i += 1
-        if not body or body.startswith("%"):
-            continue
-        f = body.split()
-        vals = [_parse_int(t) for t in f] if len(f) == 3 else None
-        if vals is None or any(v is None for v in vals):
-            raise MtxParseError(i, "size line must be three integers (rows cols entries)")
-        rows, cols, entries = vals
-        break
-    n = max(rows, cols)
-    if n == 0:
-        raise MtxParseError(i, "graph has no vertices")
-    if n > 0xFFFFFFFF:
-        raise MtxParseError(i, "vertex count exceeds 2^32-1")
-    out = []
-    seen = 0
-    while seen < entries:
-        if i >= nlines:
-            raise MtxParseError(i + 1, f"unexpected end of file: got {seen} of {entries} entries")
-        body = lines[i].strip(" \t\r")
-        i += 1
-        if not body or body.startswith("%"):
-            continue
-        f = body.split()
-        expected = 3 if has_weight else 2
-        if len(f) != expected:
-            raise MtxParseError(i, f"expected {expected} fields, got {len(f)}")
-        row, col = _parse_int(f[0]), _parse_int(f[1])
-        if row is None or col is None:
-            raise MtxParseError(i, "entry indices must be integers")
-        if row < 1 or row > rows or col < 1 or col > cols:
-            raise MtxParseError(i, f"entry ({row}, {col}) out of range for {rows} x {cols}")
-        if has_weight:
-            try:
-                float(f[2])
-            except ValueError:
-                raise MtxParseError(i, "entry weight is not a number") from None
-        src, dst = row - 1, col - 1
-        out.append((src, dst))
-        if symmetric and src != dst:
-            out.append((dst, src))
-        seen += 1
-    return EdgeList(n, np.array(out, np.uint32).reshape(-1, 2))
+def parse_matrix_market(text) -> EdgeList:
+    """graph.hpp:111-199: coordinate pattern|real|integer, general|symmetric;
+    MtxParseError(line) on malformed input.  Parsed by the library's
+    multi-threaded host parser (prgpu_mtx_parse)."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    r = _mtx_pairs(lambda *out: lib().prgpu_mtx_parse(data, len(data), 0, *out))
+    if isinstance(r, EdgeList):
+        return r
+    st, line, msg = r
+    if st == _lib.PRGPU_EPARSE:
+        prefix = f"line {line}: "
+        raise MtxParseError(line, msg[len(prefix):] if msg.startswith(prefix) else msg)
+    _lib.check(st, "parse_matrix_market")
 
 
 def load_matrix_market(path) -> EdgeList:
-    """graph.hpp:238-247 — errors name the file."""
+    """graph.hpp:238-247 — errors name the file (std::runtime_error)."""
     path = os.fspath(path)
-    try:
-        with open(path) as f:
-            text = f.read()
-    except OSError:
-        raise RuntimeError(f"cannot open graph file: {path}") from None
-    try:
-        return parse_matrix_market(text)
-    except MtxParseError as e:
-        raise RuntimeError(f"{path}: {e}") from None
+    r = _mtx_pairs(lambda *out: lib().prgpu_mtx_load(path.encode(), 0, *out))
+    if isinstance(r, EdgeList):
+        return r
+    st, _, msg = r
+    if st in (_lib.PRGPU_EPARSE, _lib.PRGPU_EIO):
+        raise RuntimeError(msg)
+    _lib.check(st, "load_matrix_market")
 
 
 def load_csr_graph(path, device: Optional[int] = None) -> CsrGraph:
-    """graph.hpp:249-251."""
-    return build_csr(load_matrix_market(path), device=device)
+    """graph.hpp:249-251: parallel parse, then build_csr on the device
+    (prgpu_graph_load_mtx)."""
+    path = os.fspath(path)
+    dev = _lib.default_device() if device is None else device
+    h = C.c_void_p()
+    st = lib().prgpu_graph_load_mtx(path.encode(), 0, dev, C.byref(h), None)
+    if st in (_lib.PRGPU_EPARSE, _lib.PRGPU_EIO):
+        raise RuntimeError(lib().prgpu_last_error().decode(errors="replace"))
+    check(st, "load_csr_graph")
+    return CsrGraph(h, dev)
 
 
 # ---------------------------------------------------------------------------

@@ -314,3 +314,25 @@ def test_graph_rows_matches_download(prl):
     assert np.array_equal(g.out_degree_only(), g.out_degree)
     with pytest.raises(ValueError):
         g.rows([n])
+
+
+def test_load_csr_graph_mtx(prl, ref, tmp_path):
+    """load_csr_graph (graph.hpp:249-251): parallel MatrixMarket parse +
+    device build_csr, CSR identical to the reference's on a symmetric,
+    weighted file with comments."""
+    rng = np.random.default_rng(7)
+    n, m = 3000, 20000
+    r, c = rng.integers(1, n + 1, m), rng.integers(1, n + 1, m)
+    path = tmp_path / "g.mtx"
+    with open(path, "w") as f:
+        f.write("%%MatrixMarket matrix coordinate real symmetric\n% test\n")
+        f.write(f"{n} {n} {m}\n")
+        for i in range(m):
+            f.write(f"{r[i]} {c[i]} {rng.random():.6f}\n")
+    g = prl.load_csr_graph(path)
+    rn, rp = ref.load_mtx(str(path))
+    want = ref.build_csr(rn, rp.reshape(-1))
+    for key in ("in_offsets", "in_neighbors", "out_degree", "dangling"):
+        assert np.array_equal(getattr(g, key), getattr(want, key)), key
+    with pytest.raises(RuntimeError, match="cannot open graph file"):
+        prl.load_csr_graph(tmp_path / "none.mtx")
