@@ -474,6 +474,10 @@ def run_partitioned(args, cfg):
         off = torch.from_numpy(g.in_offsets).pin_memory()
         nbr = torch.from_numpy(g.in_neighbors).pin_memory()
         deg = torch.from_numpy(g.out_degree).pin_memory()
+        del g  # the e2e steps build their own device graph (C5: two would not fit)
+        import gc
+        gc.collect()
+        torch.cuda.synchronize(local)
 
         def e2e_step():
             h = C.c_void_p()

@@ -771,11 +771,13 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         const bool k1split = s->K == 1 && (ks1 ? std::atoi(ks1) == 1 : k1auto);
         const char* km = std::getenv("PRGPU_K1MINB");
         const int k1_minb4 = km ? std::atoi(km) : (P.n_chunk == 0 ? 2 : 0);
-        const bool modal = nranks == 0 && (s->K > 1 || k1split) && !(sp && std::atoi(sp) == 0) && variant() == 0;
+        // partitions (nranks > 0) split too, but keep the widest mode only:
+        // narrower modes would need the peers' mode buffers mapped as well
+        const bool modal = (s->K > 1 || k1split) && !(sp && std::atoi(sp) == 0) && variant() == 0;
         if (modal) {
             const int wide = s->cfg.KP(); // (measured: 12 lanes as 4 threads x 3 lost 30%)
             for (int kp = 1; kp <= wide; kp *= 2) {
-                if (kp < wide && mm && std::atoi(mm) == 0) continue;
+                if (kp < wide && ((mm && std::atoi(mm) == 0) || nranks > 0)) continue;
                 LaneCfg a, b;
                 const int ks = kp == wide ? s->cfg.KS : kp;
                 if (mode_cfg<1>(ks, kp, s->cfg.WIN, s->all_q, a, k1_minb4) &&
@@ -819,13 +821,17 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         s->launches.push_back({s->cfg.fn, P, smem, false});
         part_cols = (size_t)kNQ * KP * P.gtot;
     } else {
-        const uint32_t T1 = P.n_chunk, T3 = P.task_end;
+        // this rank's tasks [task_begin, task_end): its hub chunks go to the
+        // first kernel, its packed + empty tasks to the second
+        const uint32_t T1 = P.n_chunk;
+        const uint32_t a0 = std::min(P.task_begin, T1), a1 = std::min(P.task_end, T1);
+        const uint32_t b0 = std::max(P.task_begin, T1), b1 = std::max(P.task_end, b0);
         for (int m = 0; m < (int)modes.size(); ++m) {
             const LaneCfg& A = modes[m].second.first;
             const LaneCfg& B = modes[m].second.second;
             size_t sa = 0, sb = 0;
-            const uint32_t GA = T1 ? grid_for_cfg(A, T1, sa) : 0;
-            const uint32_t GB = grid_for_cfg(B, T3 - T1, sb);
+            const uint32_t GA = a1 > a0 ? grid_for_cfg(A, a1 - a0, sa) : 0;
+            const uint32_t GB = grid_for_cfg(B, std::max(1u, b1 - b0), sb);
             Params PM = P;
             PM.mode_id = m;
             PM.cbase = P.mode_cbase[m];
@@ -839,15 +845,15 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
             PA.mode_id = PB.mode_id = m;
             PA.gtot = PB.gtot = GA + GB;
             if (GA) {
-                PA.task_begin = 0;
-                PA.task_end = T1;
+                PA.task_begin = a0;
+                PA.task_end = a1;
                 PA.G = GA;
                 PA.pcol0 = 0;
                 PA.no_finalize = 1;
                 s->launches.push_back({A.fn, PA, sa, false});
             }
-            PB.task_begin = T1;
-            PB.task_end = T3;
+            PB.task_begin = b0;
+            PB.task_end = b1;
             PB.G = GB;
             PB.pcol0 = GA;
             s->launches.push_back({B.fn, PB, sb, false});
@@ -967,6 +973,8 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
         l.P.pcol0 = keep.pcol0;
         l.P.task_begin = keep.task_begin;
         l.P.task_end = keep.task_end;
+        l.P.no_finalize = keep.no_finalize; // split: hub-chunk kernel, then packed + finalize
+        l.P.mode_id = keep.mode_id;
     }
     if (s->exec) { cudaGraphExecDestroy(s->exec); s->exec = nullptr; }
     if (s->graph) { cudaGraphDestroy(s->graph); s->graph = nullptr; }

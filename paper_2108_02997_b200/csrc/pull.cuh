@@ -985,11 +985,10 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
         P.partials[(size_t)t * P.gtot + P.pcol0 + blockIdx.x] = v;
     }
 
-    if (P.no_finalize) return; // first kernel of a split iteration
-
     // ---- last CTA: reduce partials, convergence, next teleport --------------------------
     if (P.fused) __threadfence_system(); // this CTA's peer stores before its ticket
     else __threadfence();
+    if (P.no_finalize) return; // first kernel of a split iteration
     __syncthreads();
     if (tid == 0) s_flag = (atomicAdd(&P.gs->counter, 1u) == P.G - 1);
     __syncthreads();
