@@ -619,6 +619,16 @@ struct Warp {
         // row bounds relative to e0 (a run holds < 2*WIN edges: 32-bit is enough)
         const uint32_t mylo = (lane < R) ? (uint32_t)(ld_stream_u64(P.row_off + r0 + lane, sp) - e0) : 0;
         const uint32_t myhi = (lane < R) ? (uint32_t)(ld_stream_u64(P.row_off + r0 + lane + 1, sp) - e0) : 0;
+        // the epilogue's row info and previous rank of row r0 + lane, in flight
+        // during the gathers (handed to the reducing lane by a shuffle)
+        uint2 my_ri = make_uint2(0, 0);
+        double my_prev = 0.0;
+        if constexpr (KP == 1) {
+            if (lane < R) {
+                my_ri = ld_stream_u2(P.rowinfo + r0 + lane, sp);
+                if (!(P.skip_mask & 16)) my_prev = __ldcs(rp + (size_t)(r0 + lane) * P.ks);
+            }
+        }
         // cb is the 16-byte aligned colidx base; valid positions [off0, ne).
         const uint32_t* __restrict__ cb = P.col + (e0 & ~3ull);
         const uint32_t off0 = (uint32_t)(e0 & 3ull);
@@ -674,7 +684,14 @@ struct Warp {
             for (int off = LG; off < LG * gs; off <<= 1)
 #pragma unroll
                 for (int w = 0; w < W; ++w) acc[w] += __shfl_xor_sync(0xffffffffu, acc[w], off);
-            if (i < R && sub == 0) epilogue(r0 + i, slice, acc);
+            if constexpr (KP == 1) {
+                const uint2 ri = make_uint2(__shfl_sync(0xffffffffu, my_ri.x, src),
+                                            __shfl_sync(0xffffffffu, my_ri.y, src));
+                const double o[1] = {__shfl_sync(0xffffffffu, my_prev, src)};
+                if (i < R && sub == 0) epilogue_with<false>(r0 + i, slice, acc, ri, o);
+            } else {
+                if (i < R && sub == 0) epilogue(r0 + i, slice, acc);
+            }
         }
         __syncwarp();
     }
