@@ -336,3 +336,42 @@ def test_load_csr_graph_mtx(prl, ref, tmp_path):
         assert np.array_equal(getattr(g, key), getattr(want, key)), key
     with pytest.raises(RuntimeError, match="cannot open graph file"):
         prl.load_csr_graph(tmp_path / "none.mtx")
+
+
+def test_concurrent_pagerank_on_shared_graph(prl):
+    """SPEC.md:194 / sweep.hpp:209-225: pagerank is reentrant on a shared,
+    immutable graph.  Host threads (ctypes drops the GIL) solve different
+    configs on one graph at once, plus builds of other graphs; every result
+    equals the same call made alone, bit for bit."""
+    import threading
+    g = prl.generate_rmat(16, 16, 0.57, 0.19, 0.19, 2108)
+    cfgs = [prl.PageRankConfig(a, t, nm) for a in (0.6, 0.85, 0.95)
+            for t, nm in ((1e-6, prl.NormKind.L1), (1e-9, prl.NormKind.L2), (1e-8, prl.NormKind.LInf))]
+    alone = [prl.pagerank(g, c) for c in cfgs]
+    out = [None] * len(cfgs)
+    built = [None] * 4
+    errors = []
+
+    def solve(i):
+        try:
+            out[i] = prl.pagerank(g, cfgs[i])
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    def build(i):
+        try:
+            built[i] = prl.generate_rmat(12, 16, 0.57, 0.19, 0.19, 100 + i).edge_count()
+        except Exception as e:
+            errors.append(e)
+
+    ts = [threading.Thread(target=solve, args=(i,)) for i in range(len(cfgs))]
+    ts += [threading.Thread(target=build, args=(i,)) for i in range(len(built))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for a, b in zip(alone, out):
+        assert a.iterations == b.iterations and np.array_equal(a.ranks, b.ranks)
+    for i in range(len(built)):
+        assert built[i] == prl.generate_rmat(12, 16, 0.57, 0.19, 0.19, 100 + i).edge_count()
