@@ -363,6 +363,7 @@ struct prgpu_session {
     int part_rank = 0, nranks = 1, host_iter = 0;
     std::vector<prgpu_partition> parts;
     DevBuf<double> rank_partials;
+    DevBuf<unsigned int> need; // fused exchange: [ceil(nsrc/4)] one byte per source, bit q = rank q gathers it
     cudaStream_t ext_stream = nullptr;
     double* ext_contrib_base = nullptr; // caller-provided contribution buffer (partition sessions)
     cudaStream_t cur() const { return ext_stream ? ext_stream : (cudaStream_t)stream; }
@@ -942,6 +943,23 @@ void part_plan_copy(prgpu_session* s, prgpu_partition* parts) {
 
 void part_set_stream(prgpu_session* s, void* stream) { s->ext_stream = (cudaStream_t)stream; }
 
+// need[src] bit q: some row of rank q has source src as an in-neighbour (one
+// warp per row; rows of rank q are [bound[q], bound[q+1]))
+__global__ void need_kernel(const uint64_t* __restrict__ row_off, const uint32_t* __restrict__ col,
+                            uint32_t rows, const uint32_t* __restrict__ bound, int nranks,
+                            unsigned int* __restrict__ need) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += (gridDim.x * blockDim.x) >> 5) {
+        int q = 0;
+        while (q + 1 < nranks && r >= bound[q + 1]) ++q;
+        const uint32_t bit = 1u << q;
+        for (uint64_t j = row_off[r] + lane; j < row_off[r + 1]; j += 32) {
+            const uint32_t src = col[j];
+            atomicOr(need + (src >> 2), bit << (8 * (src & 3)));
+        }
+    }
+}
+
 // Fused exchange over peer memory (Params::fused): the peers' buffers as
 // device pointers valid in this process (CUDA IPC or same-device buffers),
 // and the iteration loop as a CUDA graph WHILE { pull ; finalize } that runs
@@ -965,6 +983,27 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
         P.peer_arrive[q] = peer_arrive[q];
     }
     P.arrive = arrive;
+    // only the peers that gather a source receive its row (PRGPU_NEED=0: all)
+    P.need = nullptr;
+    const char* nv = std::getenv("PRGPU_NEED");
+    if (npeers > 0 && !(nv && std::atoi(nv) == 0)) {
+        const uint32_t nsrc = std::max<uint32_t>(s->g->nsrc, 1);
+        s->need.alloc((nsrc + 3) / 4);
+        PRGPU_CUDA(cudaMemsetAsync(s->need.p, 0, (size_t)(nsrc + 3) / 4 * 4, s->stream));
+        std::vector<uint32_t> hb(s->nranks + 1);
+        for (int q = 0; q < s->nranks; ++q) hb[q] = s->parts[q].row_begin;
+        hb[s->nranks] = s->parts[s->nranks - 1].row_end;
+        DevBuf<uint32_t> bound(hb.size());
+        PRGPU_CUDA(cudaMemcpyAsync(bound.p, hb.data(), hb.size() * 4, cudaMemcpyHostToDevice, s->stream));
+        const uint32_t rows = s->P.empty_begin; // rows with in-edges
+        if (rows) {
+            need_kernel<<<(unsigned)std::min<uint64_t>(((uint64_t)rows * 32 + kNT - 1) / kNT, 148ull * 64), kNT, 0,
+                          s->stream>>>(s->g->row_off.p, s->g->col.p, rows, bound.p, s->nranks, s->need.p);
+            PRGPU_LAUNCHED("need");
+        }
+        PRGPU_CUDA(cudaStreamSynchronize(s->stream));
+        P.need = reinterpret_cast<const uint8_t*>(s->need.p);
+    }
     for (auto& l : s->launches) {
         Params keep = l.P;
         l.P = P;

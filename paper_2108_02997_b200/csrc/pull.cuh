@@ -162,6 +162,7 @@ struct Params {
     double* peer_rp[kMaxPeers];
     unsigned int* peer_arrive[kMaxPeers];
     unsigned int* arrive; // this rank's arrival counter (peers add to it)
+    const uint8_t* need;  // [src] bit r: rank r gathers the source (null: every peer)
 };
 
 // ---- L2 residency control -------------------------------------------------------
@@ -391,9 +392,11 @@ struct Warp {
         } else {
             store_w<W>(dst, cv);
         }
-        if (P.fused) { // the same row into every peer's buffer (NVLink stores)
+        if (P.fused) { // the same row into the peers that gather it (NVLink stores)
             const size_t off = (size_t)(dst - P.cbase);
-            for (int q = 0; q < P.npeers; ++q) store_w<W>(P.peer_cbase[q] + off, cv);
+            const uint32_t m = P.need ? P.need[src] : 0xffu;
+            for (int q = 0; q < P.npeers; ++q)
+                if ((m >> (q < (int)P.part_rank ? q : q + 1)) & 1u) store_w<W>(P.peer_cbase[q] + off, cv);
         }
     }
 
