@@ -1,0 +1,6 @@
+# round-1 evidence refresh: bench lines for every config, C2 launch lists + ncu of the widest kernels
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -n 2 gpurun_out/pytest_gpu.log
+for c in c1 c3 c4 c5; do timeout 900 python bench.py --config $c --steps 5 --warmup 3 --no-e2e > gpurun_out/bench_$c.log 2>&1; echo "bench $c rc=$?"; done
+bash scripts/gpu_bench_r1.sh
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/ref.log 2>&1; echo "ref rc=$?"
