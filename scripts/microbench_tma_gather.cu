@@ -58,6 +58,27 @@ __global__ void __launch_bounds__(256) ldg_rows(const double* __restrict__ t, co
     if (acc == 12345.0) out[0] = acc;
 }
 
+// 96-byte rows with lane groups of 8 (6 active, 4 rows per warp instruction:
+// the pull kernel's K = 11 layout) against ldg_rows<96> (groups of 6, 5 rows)
+__global__ void __launch_bounds__(256) ldg_rows96_lg8(const double* __restrict__ t, const uint32_t* __restrict__ idx,
+                                                      uint64_t m, double* out) {
+    const int lane = threadIdx.x & 31, slot = lane / 8, slice = lane % 8;
+    const uint64_t warps = (uint64_t)gridDim.x * blockDim.x / 32;
+    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
+    double acc = 0;
+    for (uint64_t e = w * 4 + slot; e + 7 * warps * 4 < m; e += 8 * warps * 4) {
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint64_t r = idx[e + u * warps * 4];
+            v[u] = slice < 6 ? __ldg(reinterpret_cast<const double2*>(t + r * 12 + slice * 2)) : make_double2(0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y;
+    }
+    if (acc == 12345.0) out[0] = acc;
+}
+
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // TMA gather4: each warp owns D stages of 4 rows; lane 0 issues, all lanes consume
@@ -138,6 +159,23 @@ int main() {
             }
             printf("L2 sweep: unif table %4zu MB rows %2d B: %.3f ms  %.1f Grows/s\n", mb, rb, ms, m / ms / 1e6);
         }
+    if (getenv("LG_ONLY")) {
+        for (int skew = 0; skew < 2; ++skew)
+            for (size_t mb : {48, 96, 194, 512}) {
+                const uint64_t rows = (mb << 20) / 96;
+                fill_idx<<<1024, 256>>>(idx, m, rows, skew);
+                float a6 = 0, a8 = 0;
+                for (int rep = 0; rep < 3; ++rep) {
+                    cudaEventRecord(a); ldg_rows<96><<<nsm * 8, 256>>>(t, idx, m, out); cudaEventRecord(b);
+                    cudaEventSynchronize(b); cudaEventElapsedTime(&a6, a, b);
+                    cudaEventRecord(a); ldg_rows96_lg8<<<nsm * 8, 256>>>(t, idx, m, out); cudaEventRecord(b);
+                    cudaEventSynchronize(b); cudaEventElapsedTime(&a8, a, b);
+                }
+                printf("%s 96 B rows table %4zu MB: groups of 6 (5 rows/warp) %.1f G rows/s | groups of 8 (4 rows/warp) %.1f G rows/s\n",
+                       skew ? "skew" : "unif", mb, m / a6 / 1e6, m / a8 / 1e6);
+            }
+        return 0;
+    }
     if (getenv("SWEEP_ONLY")) return 0;
     // hot/cold split: a fraction `hf` of the gathers hits the hottest `hot_mb`
     // of a `tab_mb` table (96-byte rows, like C2); mixed in one stream, or
