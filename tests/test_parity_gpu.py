@@ -375,3 +375,40 @@ def test_concurrent_pagerank_on_shared_graph(prl):
         assert a.iterations == b.iterations and np.array_equal(a.ranks, b.ranks)
     for i in range(len(built)):
         assert built[i] == prl.generate_rmat(12, 16, 0.57, 0.19, 0.19, 100 + i).edge_count()
+
+
+def test_acceptance_sensitivity_and_damping_trend(prl, oracle, small_golden):
+    """acceptance.cpp:261-329 through the product API on the 10k scale-free
+    fixture (seed 2021): at alpha .95 over the tolerance grid extended to
+    1e-16, L1 hits the sensitivity limit and no later than L2 / LInf, and
+    each norm's failing tail is exactly its non-converged cells; the
+    iteration ratios 0.95/0.85 in [2, 4] and 0.75/0.85 in [0.4, 0.8] equal
+    the reference's iteration counts."""
+    sf = small_golden["known"]["scale_free_10k"]
+    rng = oracle.mt19937(2021)
+    n, pairs = oracle.scale_free_web(rng, 10000, 4, 0.08)
+    g = prl.build_csr(edge_list(prl, n, pairs))
+    grid = list(prl.default_tolerance_grid()) + [5e-11, 1e-11, 5e-12, 1e-12, 5e-13, 1e-13,
+                                                 5e-14, 1e-14, 5e-15, 1e-15, 5e-16, 1e-16]
+    recs = []
+    for norm in prl.all_norms:
+        for tol in grid:
+            r = prl.pagerank(g, prl.PageRankConfig(0.95, tol, norm))
+            recs.append(prl.SweepRecord("scale_free_10k", n, g.edge_count(), 0.95, tol, norm,
+                                        r.iterations, r.converged))
+    first = {int(f.norm): f.first_failing_tolerance for f in prl.detect_sensitivity(recs)}
+    l1, l2, linf = (first[int(k)] for k in (prl.NormKind.L1, prl.NormKind.L2, prl.NormKind.LInf))
+    assert l1 is not None
+    if l2 is not None:
+        assert l1 >= l2
+    if linf is not None:
+        assert l1 >= linf
+    for rec in recs:
+        f = first[int(rec.norm)]
+        in_tail = f is not None and rec.tolerance <= f
+        assert rec.converged == (not in_tail), (rec.norm, rec.tolerance)
+    its = {a: prl.pagerank(g, prl.PageRankConfig(a, 1e-6, prl.NormKind.L1)).iterations
+           for a in (0.75, 0.85, 0.95)}
+    for a, it in its.items():
+        assert it == sf["damping"][f"{a:.2f}"], (a, it)
+    assert 2.0 <= its[0.95] / its[0.85] <= 4.0 and 0.4 <= its[0.75] / its[0.85] <= 0.8
