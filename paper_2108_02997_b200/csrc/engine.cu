@@ -342,6 +342,11 @@ struct prgpu_session {
     };
     std::vector<Launch> launches;
     int mode0 = 0;   // lane-width mode of the first iteration
+    // partition sessions: the lane-mode launch list the fused exchange switches
+    // to (prgpu_part_set_peers); the NCCL exchange keeps the widest mode only
+    std::vector<Launch> modal_launches;
+    Params modal_P{};
+    int modal_mode0 = 0;
     bool all_q = true; // every partial quantity tracked (not only the L1 stopping rule)
     Params P{};
     Stream stream;
@@ -616,6 +621,17 @@ void plan_partition(prgpu_session* s, int nranks) {
     }
 }
 
+// Contribution buffer of a partition session (doubles): both parities of the
+// run's rows, then of every narrower lane mode a K > 1 run can switch to (the
+// fused exchange maps the whole allocation into the peers once).
+uint64_t part_contrib_doubles(const prgpu_graph* g, const LaneCfg& c, int K) {
+    const uint64_t nsrc = std::max<uint64_t>(g->nsrc, 1);
+    uint64_t lanes = (uint64_t)c.KS;
+    if (K > 1)
+        for (int kp = 1; kp < c.KP(); kp *= 2) lanes += (uint64_t)kp;
+    return 2 * nsrc * lanes;
+}
+
 prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_graph, int rank = 0,
                               int nranks = 0, double* ext_contrib = nullptr, double* ext_rp = nullptr) {
     validate_params(p);
@@ -642,8 +658,8 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     s->rank.alloc(2 * (size_t)KS * n);
     double* cbase = ext_contrib;
     s->ext_contrib_base = ext_contrib;
-    if (!cbase) {
-        s->contrib.alloc(2 * nsrc * KS);
+    if (!cbase) { // partitions: room for the narrow lane modes' buffers too (part_contrib_doubles)
+        s->contrib.alloc(nranks >= 1 ? part_contrib_doubles(g, s->cfg, K) : 2 * nsrc * KS);
         cbase = s->contrib.p;
     }
     PRGPU_CUDA(cudaMemsetAsync(cbase, 0, 2 * nsrc * KS * sizeof(double), st));
@@ -760,7 +776,8 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     // leaves CTA partials and a packed + empty kernel that finalizes; once the
     // live lanes fit a narrower mode the wide pairs exit at once.  Multi-GPU
     // partitions run the one base kernel; K = 1 see below.
-    std::vector<std::pair<int, std::pair<LaneCfg, LaneCfg>>> modes; // kp, (chunk, packed)
+    using ModeList = std::vector<std::pair<int, std::pair<LaneCfg, LaneCfg>>>; // kp, (chunk, packed)
+    ModeList modes;
     {
         const char* sp = std::getenv("PRGPU_SPLIT");   // =0: base kernel only (tuning)
         const char* mm = std::getenv("PRGPU_MODES");   // =0: widest mode only (tuning)
@@ -774,13 +791,11 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         const bool k1split = s->K == 1 && (ks1 ? std::atoi(ks1) == 1 : k1auto);
         const char* km = std::getenv("PRGPU_K1MINB");
         const int k1_minb4 = km ? std::atoi(km) : (P.n_chunk == 0 ? 2 : 0);
-        // partitions (nranks > 0) split too, but keep the widest mode only:
-        // narrower modes would need the peers' mode buffers mapped as well
         const bool modal = (s->K > 1 || k1split) && !(sp && std::atoi(sp) == 0) && variant() == 0;
         if (modal) {
             const int wide = s->cfg.KP(); // (measured: 12 lanes as 4 threads x 3 lost 30%)
             for (int kp = 1; kp <= wide; kp *= 2) {
-                if (kp < wide && ((mm && std::atoi(mm) == 0) || nranks > 0)) continue;
+                if (kp < wide && mm && std::atoi(mm) == 0) continue;
                 LaneCfg a, b;
                 const int ks = kp == wide ? s->cfg.KS : kp;
                 if (mode_cfg<1>(ks, kp, s->cfg.WIN, s->all_q, a, k1_minb4) &&
@@ -790,59 +805,82 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
             if (modes.empty() || modes.back().first != wide) modes.clear(); // no instances: base kernel
         }
     }
-    P.nmodes = modes.empty() ? 1 : (int)modes.size();
-    for (int m = 0; m < kMaxModes; ++m)
-        P.mode_kp[m] = modes.empty() ? KP : (m < (int)modes.size() ? modes[m].first : KP);
-    s->mode0 = 0;
-    for (int m = P.nmodes - 1; m >= 0; --m)
-        if (P.mode_kp[m] > K - 1) s->mode0 = m; // narrowest mode covering every lane
-    P.no_finalize = 0;
-    // contribution buffers per mode: the widest mode uses the run's buffers
-    for (int m = 0; m < kMaxModes; ++m) {
-        P.mode_cbase[m] = P.cbase;
-        P.mode_cold_off[m][0] = P.cold_off[0];
-        P.mode_cold_off[m][1] = P.cold_off[1];
-        P.mode_ks[m] = s->cfg.KS;
-    }
+    P.part_kp = (uint32_t)KP;
+    // contribution buffers of the narrow modes: after the run's own buffers
+    // in the same allocation for partitions (one IPC mapping covers them all),
+    // separate buffers otherwise
+    double* narrow_base = cbase + 2 * nsrc * KS;
+    std::vector<double*> narrow_cbase;
     for (int m = 0; m + 1 < (int)modes.size(); ++m) {
         const int kp = modes[m].first;
-        s->mode_contrib[m].alloc(2 * nsrc * kp);
-        PRGPU_CUDA(cudaMemsetAsync(s->mode_contrib[m].p, 0, 2 * nsrc * kp * sizeof(double), st));
-        P.mode_cbase[m] = s->mode_contrib[m].p;
-        P.mode_cold_off[m][0] = 0;
-        P.mode_cold_off[m][1] = nsrc;
-        P.mode_ks[m] = kp;
+        double* b = nullptr;
+        if (nranks >= 1) {
+            b = narrow_base;
+            narrow_base += 2 * nsrc * kp;
+        } else {
+            s->mode_contrib[m].alloc(2 * nsrc * kp);
+            b = s->mode_contrib[m].p;
+        }
+        PRGPU_CUDA(cudaMemsetAsync(b, 0, 2 * nsrc * kp * sizeof(double), st));
+        narrow_cbase.push_back(b);
     }
-    size_t part_cols = 0; // partials: max over modes of kNQ * kp * columns
-    s->launches.clear();
-    if (modes.empty()) {
-        size_t smem = 0;
-        P.G = grid_for_cfg(s->cfg, (uint64_t)P.task_end - P.task_begin, smem);
-        P.gtot = P.G;
-        P.pcol0 = 0;
-        P.mode_id = 0;
-        s->launches.push_back({s->cfg.fn, P, smem, false});
-        part_cols = (size_t)kNQ * KP * P.gtot;
-    } else {
+    // one iteration's launches for a list of modes (narrowest first); fills the
+    // mode table of `Q` and returns the widest partial-column need
+    auto build_launches = [&](const ModeList& ml, Params& Q, std::vector<prgpu_session::Launch>& out,
+                              int& mode0) -> size_t {
+        Q.nmodes = ml.empty() ? 1 : (int)ml.size();
+        for (int m = 0; m < kMaxModes; ++m)
+            Q.mode_kp[m] = ml.empty() ? KP : (m < (int)ml.size() ? ml[m].first : KP);
+        mode0 = 0;
+        for (int m = Q.nmodes - 1; m >= 0; --m)
+            if (Q.mode_kp[m] > K - 1) mode0 = m; // narrowest mode covering every lane
+        Q.no_finalize = 0;
+        // contribution buffers per mode: the widest mode uses the run's buffers
+        for (int m = 0; m < kMaxModes; ++m) {
+            Q.mode_cbase[m] = Q.cbase;
+            Q.mode_cold_off[m][0] = Q.cold_off[0];
+            Q.mode_cold_off[m][1] = Q.cold_off[1];
+            Q.mode_ks[m] = s->cfg.KS;
+        }
+        for (int m = 0; m + 1 < (int)ml.size(); ++m) {
+            const int kp = ml[m].first;
+            int j = 0; // its buffer among the run's narrow modes
+            while (j + 1 < (int)modes.size() && modes[j].first != kp) ++j;
+            Q.mode_cbase[m] = narrow_cbase[j];
+            Q.mode_cold_off[m][0] = 0;
+            Q.mode_cold_off[m][1] = nsrc;
+            Q.mode_ks[m] = kp;
+        }
+        size_t cols = 0; // partials: max over modes of kNQ * kp * columns
+        out.clear();
+        if (ml.empty()) {
+            size_t smem = 0;
+            Q.G = grid_for_cfg(s->cfg, (uint64_t)Q.task_end - Q.task_begin, smem);
+            Q.gtot = Q.G;
+            Q.pcol0 = 0;
+            Q.mode_id = 0;
+            out.push_back({s->cfg.fn, Q, smem, false});
+            return (size_t)kNQ * KP * Q.gtot;
+        }
         // this rank's tasks [task_begin, task_end): its hub chunks go to the
         // first kernel, its packed + empty tasks to the second
-        const uint32_t T1 = P.n_chunk;
-        const uint32_t a0 = std::min(P.task_begin, T1), a1 = std::min(P.task_end, T1);
-        const uint32_t b0 = std::max(P.task_begin, T1), b1 = std::max(P.task_end, b0);
-        for (int m = 0; m < (int)modes.size(); ++m) {
-            const LaneCfg& A = modes[m].second.first;
-            const LaneCfg& B = modes[m].second.second;
+        const uint32_t T1 = Q.n_chunk;
+        const uint32_t a0 = std::min(Q.task_begin, T1), a1 = std::min(Q.task_end, T1);
+        const uint32_t b0 = std::max(Q.task_begin, T1), b1 = std::max(Q.task_end, b0);
+        for (int m = 0; m < (int)ml.size(); ++m) {
+            const LaneCfg& A = ml[m].second.first;
+            const LaneCfg& B = ml[m].second.second;
             size_t sa = 0, sb = 0;
             const uint32_t GA = a1 > a0 ? grid_for_cfg(A, a1 - a0, sa) : 0;
             const uint32_t GB = grid_for_cfg(B, std::max(1u, b1 - b0), sb);
-            Params PM = P;
+            Params PM = Q;
             PM.mode_id = m;
-            PM.cbase = P.mode_cbase[m];
-            PM.cold_off[0] = P.mode_cold_off[m][0];
-            PM.cold_off[1] = P.mode_cold_off[m][1];
-            if (m + 1 < (int)modes.size()) { // narrow mode: repack on entry
+            PM.cbase = Q.mode_cbase[m];
+            PM.cold_off[0] = Q.mode_cold_off[m][0];
+            PM.cold_off[1] = Q.mode_cold_off[m][1];
+            if (m + 1 < (int)ml.size()) { // narrow mode: repack on entry
                 PM.G = (uint32_t)dev_sms * 8;
-                s->launches.push_back({nullptr, PM, 0, true});
+                out.push_back({nullptr, PM, 0, true});
             }
             Params PA = PM, PB = PM;
             PA.mode_id = PB.mode_id = m;
@@ -853,19 +891,31 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
                 PA.G = GA;
                 PA.pcol0 = 0;
                 PA.no_finalize = 1;
-                s->launches.push_back({A.fn, PA, sa, false});
+                out.push_back({A.fn, PA, sa, false});
             }
             PB.task_begin = b0;
             PB.task_end = b1;
             PB.G = GB;
             PB.pcol0 = GA;
-            s->launches.push_back({B.fn, PB, sb, false});
-            part_cols = std::max(part_cols, (size_t)kNQ * modes[m].first * (GA + GB));
+            out.push_back({B.fn, PB, sb, false});
+            cols = std::max(cols, (size_t)kNQ * ml[m].first * (GA + GB));
         }
+        return cols;
+    };
+    size_t part_cols = 0;
+    if (nranks >= 1 && modes.size() > 1) {
+        // partitions: the full mode list for the fused exchange, kept aside;
+        // the widest mode alone is what runs until prgpu_part_set_peers
+        s->modal_P = P;
+        part_cols = build_launches(modes, s->modal_P, s->modal_launches, s->modal_mode0);
+        modes.erase(modes.begin(), modes.end() - 1);
     }
+    part_cols = std::max(part_cols, build_launches(modes, P, s->launches, s->mode0));
     s->partials.alloc(part_cols);
     P.partials = s->partials.p;
+    s->modal_P.partials = s->partials.p;
     for (auto& l : s->launches) l.P.partials = s->partials.p;
+    for (auto& l : s->modal_launches) l.P.partials = s->partials.p;
     P.G = s->launches.back().P.G;
     P.gtot = s->launches.back().P.gtot;
 
@@ -974,16 +1024,30 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
         fail(PRGPU_EINVAL, "set_peers: npeers must be nranks - 1 (<= " + std::to_string(kMaxPeers) + ")");
     if (!arrive) fail(PRGPU_EINVAL, "set_peers: null arrival counter");
     if (!s->ext_contrib_base) fail(PRGPU_EINVAL, "set_peers: the session needs caller-provided buffers");
+    // the fused exchange runs the lane-width modes (their buffers live in the
+    // same caller allocation, mapped by the peers at the same offsets);
+    // PRGPU_PART_MODES=0 keeps the widest mode only (tuning)
+    const char* pm = std::getenv("PRGPU_PART_MODES");
+    if (!s->modal_launches.empty() && !(pm && std::atoi(pm) == 0)) {
+        Params& M = s->modal_P;
+        Params& P0 = s->P;
+        P0.nmodes = M.nmodes;
+        for (int m = 0; m < kMaxModes; ++m) {
+            P0.mode_kp[m] = M.mode_kp[m];
+            P0.mode_cbase[m] = M.mode_cbase[m];
+            P0.mode_cold_off[m][0] = M.mode_cold_off[m][0];
+            P0.mode_cold_off[m][1] = M.mode_cold_off[m][1];
+            P0.mode_ks[m] = M.mode_ks[m];
+        }
+        s->launches = s->modal_launches;
+        s->mode0 = s->modal_mode0;
+        s->modal_launches.clear();
+    }
     Params& P = s->P;
     P.fused = 1;
     P.npeers = npeers;
-    for (int q = 0; q < npeers; ++q) {
+    for (int q = 0; q < npeers; ++q)
         if (!peer_contrib[q] || !peer_rp[q] || !peer_arrive[q]) fail(PRGPU_EINVAL, "set_peers: null peer pointer");
-        // peers' buffers share this rank's layout: same base offsets
-        P.peer_cbase[q] = peer_contrib[q] + (P.cbase - s->ext_contrib_base);
-        P.peer_rp[q] = peer_rp[q];
-        P.peer_arrive[q] = peer_arrive[q];
-    }
     P.arrive = arrive;
     // only the peers that gather a source receive its row (PRGPU_NEED=0: all)
     P.need = nullptr;
@@ -1006,6 +1070,8 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
         PRGPU_CUDA(cudaStreamSynchronize(s->stream));
         P.need = reinterpret_cast<const uint8_t*>(s->need.p);
     }
+    // every launch: the shared fields, its own grid / tasks / mode buffers, and
+    // the peers' copy of its buffers (same offset in the peers' allocation)
     for (auto& l : s->launches) {
         Params keep = l.P;
         l.P = P;
@@ -1016,9 +1082,23 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
         l.P.task_end = keep.task_end;
         l.P.no_finalize = keep.no_finalize; // split: hub-chunk kernel, then packed + finalize
         l.P.mode_id = keep.mode_id;
+        l.P.cbase = keep.cbase;
+        l.P.cold_off[0] = keep.cold_off[0];
+        l.P.cold_off[1] = keep.cold_off[1];
+        for (int q = 0; q < npeers; ++q) {
+            l.P.peer_cbase[q] = peer_contrib[q] + (l.P.cbase - s->ext_contrib_base);
+            l.P.peer_rp[q] = peer_rp[q];
+            l.P.peer_arrive[q] = peer_arrive[q];
+        }
+    }
+    for (int q = 0; q < npeers; ++q) {
+        P.peer_cbase[q] = peer_contrib[q] + (P.cbase - s->ext_contrib_base);
+        P.peer_rp[q] = peer_rp[q];
+        P.peer_arrive[q] = peer_arrive[q];
     }
     if (s->exec) { cudaGraphExecDestroy(s->exec); s->exec = nullptr; }
     if (s->graph) { cudaGraphDestroy(s->graph); s->graph = nullptr; }
+    // WHILE { per mode an IF node (narrowest first) around its kernels ; finalize }
     PRGPU_CUDA(cudaGraphCreate(&s->graph, 0));
     cudaGraphConditionalHandle h;
     PRGPU_CUDA(cudaGraphConditionalHandleCreate(&h, s->graph, 1, cudaGraphCondAssignDefault));
@@ -1030,26 +1110,53 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
     cudaGraphNode_t cnode;
     PRGPU_CUDA(cudaGraphAddNode(&cnode, s->graph, nullptr, 0, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    cudaGraphNode_t prev = nullptr;
+    const int nm = P.nmodes;
+    cudaGraphConditionalHandle mh[kMaxModes] = {};
+    cudaGraph_t mbody[kMaxModes] = {};
+    cudaGraphNode_t last = nullptr; // the node the finalize kernel follows
+    if (nm > 1) {
+        for (int m = 0; m < nm; ++m) {
+            PRGPU_CUDA(cudaGraphConditionalHandleCreate(&mh[m], body, m == s->mode0 ? 1u : 0u,
+                                                        cudaGraphCondAssignDefault));
+            cudaGraphNodeParams ip = {};
+            ip.type = cudaGraphNodeTypeConditional;
+            ip.conditional.handle = mh[m];
+            ip.conditional.type = cudaGraphCondTypeIf;
+            ip.conditional.size = 1;
+            cudaGraphNode_t inode;
+            PRGPU_CUDA(cudaGraphAddNode(&inode, body, last ? &last : nullptr, last ? 1 : 0, &ip));
+            mbody[m] = ip.conditional.phGraph_out[0];
+            last = inode;
+        }
+    }
+    uint32_t nsrc32 = std::max<uint32_t>(s->g->nsrc, 1);
+    cudaGraphNode_t prev[kMaxModes] = {};
     for (const auto& l : s->launches) {
         Params PG = l.P;
         PG.use_cond = 1;
         PG.cond = h;
+        PG.use_mode_cond = 0; // the finalize kernel arms the next mode
+        const int m = nm > 1 ? PG.mode_id : 0;
+        cudaGraph_t tgt = nm > 1 ? mbody[m] : body;
+        cudaGraphNode_t* dep = nm > 1 ? (prev[m] ? &prev[m] : nullptr) : (last ? &last : nullptr);
         cudaKernelNodeParams kp = {};
-        kp.func = (void*)l.fn;
+        kp.func = l.repack ? (void*)repack_kernel : (void*)l.fn;
         kp.gridDim = dim3(PG.G);
         kp.blockDim = dim3(kNT);
         kp.sharedMemBytes = (unsigned)l.smem;
-        void* args[] = {&PG};
+        void* args[] = {&PG, &nsrc32};
         kp.kernelParams = args;
         cudaGraphNode_t node;
-        PRGPU_CUDA(cudaGraphAddKernelNode(&node, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
-        prev = node;
+        PRGPU_CUDA(cudaGraphAddKernelNode(&node, tgt, dep, dep ? 1 : 0, &kp));
+        if (nm > 1) prev[m] = node;
+        else last = node;
     }
     {
         Params PF = P;
         PF.use_cond = 1;
         PF.cond = h;
+        PF.use_mode_cond = nm > 1;
+        for (int m = 0; m < kMaxModes; ++m) PF.mode_cond[m] = mh[m];
         cudaKernelNodeParams kp = {};
         kp.func = (void*)s->cfg.fin;
         kp.gridDim = dim3(1);
@@ -1057,7 +1164,7 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
         void* args[] = {&PF};
         kp.kernelParams = args;
         cudaGraphNode_t node;
-        PRGPU_CUDA(cudaGraphAddKernelNode(&node, body, &prev, 1, &kp));
+        PRGPU_CUDA(cudaGraphAddKernelNode(&node, body, last ? &last : nullptr, last ? 1 : 0, &kp));
     }
     PRGPU_CUDA(cudaGraphInstantiate(&s->exec, s->graph, 0));
     s->use_graph = true;
@@ -1082,7 +1189,7 @@ void part_sizes(prgpu_graph* g, const prgpu_params* p, int nranks, uint64_t* con
     const uint32_t mask = p->stop_mask ? p->stop_mask : (1u << p->norm);
     const bool l1_only = mask == 1u && p->norm == PRGPU_NORM_L1 && !p->ref_ranks;
     const LaneCfg c = lane_cfg(p->lanes, !l1_only);
-    *contrib = 2ull * std::max<uint64_t>(g->nsrc, 1) * c.KS;
+    *contrib = part_contrib_doubles(g, c, p->lanes);
     *partials = (uint64_t)nranks * kNQ * c.KP();
 }
 

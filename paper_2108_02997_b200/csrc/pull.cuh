@@ -163,6 +163,7 @@ struct Params {
     unsigned int* peer_arrive[kMaxPeers];
     unsigned int* arrive; // this rank's arrival counter (peers add to it)
     const uint8_t* need;  // [src] bit r: rank r gathers the source (null: every peer)
+    uint32_t part_kp;     // lane stride of rank_partials (the run's widest mode)
 };
 
 // ---- L2 residency control -------------------------------------------------------
@@ -855,9 +856,10 @@ struct Warp {
 
 // Per-lane convergence and the next teleport from the reduced partials
 // (pagerank.hpp:87, :95-99); thread k < K handles lane k, thread 0 the loop flag.
+// `layout`: the lane-width mode whose contribution buffers this iteration wrote
 template <int KP, int QM>
 __device__ void finalize_lanes(const Params& P, const double* s_tot, const double* s_c0,
-                               const int* s_active, int iter) {
+                               const int* s_active, int iter, int layout) {
     const int tid = threadIdx.x;
     if (tid < (int)P.K && tid < KP && s_active[tid]) { // lanes >= KP are frozen in this mode
         const int k = tid;
@@ -916,7 +918,7 @@ __device__ void finalize_lanes(const Params& P, const double* s_tot, const doubl
         P.gs->mode = mode;
         if (P.use_cond && P.use_mode_cond)
             for (int m = 0; m < P.nmodes; ++m) cudaGraphSetConditional(P.mode_cond[m], m == mode ? 1u : 0u);
-        if (!P.no_finalize) P.gs->layout = P.mode_id; // this iteration wrote our buffer
+        P.gs->layout = layout; // this iteration wrote that mode's buffers
         P.gs->iter = iter + 1;
         P.gs->any_active = any;
         P.gs->counter = 0;
@@ -1044,11 +1046,14 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     }
     __syncthreads();
     if (P.part_mode) { // multi-GPU: publish this rank's vector; finalize runs after the exchange
-        const size_t slot = ((P.fused ? (size_t)(s_iter & 1) * P.nranks : 0) + P.part_rank) * kNQ * KP;
+        // in the run's layout [q][part_kp] (a narrow mode fills its first KP lanes)
+        const uint32_t pkp = P.part_kp;
+        const size_t slot = ((P.fused ? (size_t)(s_iter & 1) * P.nranks : 0) + P.part_rank) * kNQ * pkp;
         for (int t = tid; t < kNQ * KP; t += kNT) {
-            P.rank_partials[slot + t] = s_tot[t];
+            const size_t at = slot + (size_t)(t / KP) * pkp + t % KP;
+            P.rank_partials[at] = s_tot[t];
             if (P.fused)
-                for (int q = 0; q < P.npeers; ++q) P.peer_rp[q][slot + t] = s_tot[t];
+                for (int q = 0; q < P.npeers; ++q) P.peer_rp[q][at] = s_tot[t];
         }
         __syncthreads();
         if (tid == 0) {
@@ -1061,7 +1066,7 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
         }
         return;
     }
-    finalize_lanes<KP, QM>(P, s_tot, s_c0, s_active, s_iter);
+    finalize_lanes<KP, QM>(P, s_tot, s_c0, s_active, s_iter, P.mode_id);
 }
 
 // Mode change (Params::mode_id): copy the current contributions (parity of
@@ -1104,8 +1109,11 @@ __global__ void __launch_bounds__(kNT) part_finalize_kernel(const Params P) {
         s_c0[tid] = real ? P.lanes[tid].c0 : 0.0;
         s_active[tid] = real ? P.lanes[tid].active : 0;
     }
-    __shared__ int s_go;
-    if (tid == 0) s_go = P.gs->any_active;
+    __shared__ int s_go, s_mode;
+    if (tid == 0) {
+        s_go = P.gs->any_active;
+        s_mode = P.gs->mode; // the mode this iteration ran in (finalize picks the next)
+    }
     __syncthreads();
     if (!s_go) return; // speculative launch after convergence
     if (P.fused && tid == 0) {
@@ -1134,7 +1142,7 @@ __global__ void __launch_bounds__(kNT) part_finalize_kernel(const Params P) {
         s_tot[t] = v;
     }
     __syncthreads();
-    finalize_lanes<KP, QM>(P, s_tot, s_c0, s_active, s_iter);
+    finalize_lanes<KP, QM>(P, s_tot, s_c0, s_active, s_iter, s_mode);
 }
 
 } // namespace prgpu
