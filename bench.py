@@ -504,6 +504,14 @@ def run_partitioned(args, cfg):
     roof = {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s", "frac": per_gpu / peak,
             "traffic": None, "peak_source": peak_kind,
             "kernel": "pull kernels + exchange, whole loop (per GPU, aggregate bytes / N)"}
+    # NVLink: contribution rows each rank stores into its peers (fused exchange,
+    # needed-only), per iteration with every lane live; max over ranks
+    sent = torch.tensor([float(getattr(r, "sent_bytes", 0))], device=f"cuda:{local}", dtype=torch.float64)
+    tdist.all_reduce(sent, op=tdist.ReduceOp.MAX)
+    t_iter_s = ms_per_step / 1e3 / max(1, int(r.run_iterations))
+    exchange = {"kind": args.exchange, "bytes_per_iteration_all_lanes": float(sent.item()),
+                "per_gpu_gbs_at_mean_iteration": float(sent.item()) / t_iter_s / 1e9,
+                "link_peak_gbs": 900.0} if args.exchange == "peer" else {"kind": args.exchange}
     # e2e through the public API at N GPUs: every rank uploads the reference-layout
     # CSR from pinned host memory, runs the partitioned solve, the ranks are
     # gathered to the host (distributed.run_distributed(want_ranks=True))
@@ -558,6 +566,7 @@ def run_partitioned(args, cfg):
             "gpu_launches": args.steps * r.run_iterations * 2,
             "clocks": clk.summary(),
             "roofline": roof,
+            "exchange": exchange,
             "cpu_baseline": None,
             "e2e": e2e,
         }

@@ -228,6 +228,9 @@ PRGPU_API int prgpu_part_set_peers(prgpu_session* s, int npeers, double* const* 
                                    double* const* peer_partials, unsigned int* const* peer_arrive,
                                    unsigned int* arrive);
 PRGPU_API int prgpu_part_launch(prgpu_session* s);
+/* Fused exchange volume: contribution rows this rank stores into its peers
+ * per iteration while every lane is live (rows of *row_doubles doubles). */
+PRGPU_API int prgpu_part_sent_rows(prgpu_session* s, uint64_t* rows, uint32_t* row_doubles);
 /* CUDA IPC for the fused exchange's buffers (any pointer inside a device
  * allocation): export a 64-byte handle + offset; open it in another process
  * of the same node (peer access enabled); close with the pointer open gave. */

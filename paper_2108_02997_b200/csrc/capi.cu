@@ -53,6 +53,7 @@ int read_any_active(prgpu_session*);
 void part_plan_copy(prgpu_session*, prgpu_partition*);
 void part_set_stream(prgpu_session*, void*);
 void graph_permutation(const prgpu_graph*, uint32_t*);
+void part_sent_rows(prgpu_session*, uint64_t*, uint32_t*);
 
 uint64_t graph_rows(const prgpu_graph*, const uint32_t*, uint32_t, uint64_t*, uint32_t*, uint64_t, cudaStream_t);
 void session_destroy(prgpu_session*);
@@ -440,6 +441,13 @@ int prgpu_part_set_peers(prgpu_session* s, int npeers, double* const* peer_contr
         if (!s || (npeers > 0 && (!peer_contrib || !peer_partials || !peer_arrive)))
             prgpu::fail(PRGPU_EINVAL, "null argument");
         prgpu::part_set_peers(s, npeers, peer_contrib, peer_partials, peer_arrive, arrive);
+    });
+}
+
+int prgpu_part_sent_rows(prgpu_session* s, uint64_t* rows, uint32_t* row_doubles) {
+    return guarded([&] {
+        if (!s || !rows || !row_doubles) prgpu::fail(PRGPU_EINVAL, "null argument");
+        prgpu::part_sent_rows(s, rows, row_doubles);
     });
 }
 

@@ -368,6 +368,7 @@ struct prgpu_session {
     int part_rank = 0, nranks = 1, host_iter = 0;
     std::vector<prgpu_partition> parts;
     DevBuf<double> rank_partials;
+    uint64_t sent_rows = 0;    // fused exchange: contribution rows stored into peers per iteration
     DevBuf<unsigned int> need; // fused exchange: [ceil(nsrc/4)] one byte per source, bit q = rank q gathers it
     cudaStream_t ext_stream = nullptr;
     double* ext_contrib_base = nullptr; // caller-provided contribution buffer (partition sessions)
@@ -1012,6 +1013,20 @@ __global__ void need_kernel(const uint64_t* __restrict__ row_off, const uint32_t
     }
 }
 
+// rows this rank stores into peers per iteration (widest mode): for each
+// source of its rows, the peers that gather it (all peers without a mask)
+__global__ void sent_rows_kernel(const uint2* __restrict__ rowinfo, uint32_t row_begin, uint32_t row_end,
+                                 const uint8_t* __restrict__ need, uint32_t others, int npeers,
+                                 unsigned long long* __restrict__ out) {
+    unsigned long long c = 0;
+    for (uint32_t r = row_begin + blockIdx.x * blockDim.x + threadIdx.x; r < row_end; r += gridDim.x * blockDim.x) {
+        const uint2 ri = rowinfo[r];
+        if (ri.x) c += need ? (unsigned long long)__popc(need[ri.y] & others) : (unsigned long long)npeers;
+    }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 // Fused exchange over peer memory (Params::fused): the peers' buffers as
 // device pointers valid in this process (CUDA IPC or same-device buffers),
 // and the iteration loop as a CUDA graph WHILE { pull ; finalize } that runs
@@ -1096,6 +1111,20 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
         P.peer_rp[q] = peer_rp[q];
         P.peer_arrive[q] = peer_arrive[q];
     }
+    {
+        const prgpu_partition& me = s->parts[s->part_rank];
+        const uint32_t others = ((1u << s->nranks) - 1u) & ~(1u << s->part_rank);
+        DevBuf<unsigned long long> cnt(1);
+        PRGPU_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), s->stream));
+        if (me.row_end > me.row_begin)
+            sent_rows_kernel<<<blocks_for(me.row_end - me.row_begin), kNT, 0, s->stream>>>(
+                s->g->rowinfo.p, me.row_begin, me.row_end, P.need, others, npeers, cnt.p);
+        PRGPU_LAUNCHED("sent_rows");
+        unsigned long long c = 0;
+        PRGPU_CUDA(cudaMemcpyAsync(&c, cnt.p, sizeof(c), cudaMemcpyDeviceToHost, s->stream));
+        PRGPU_CUDA(cudaStreamSynchronize(s->stream));
+        s->sent_rows = c;
+    }
     if (s->exec) { cudaGraphExecDestroy(s->exec); s->exec = nullptr; }
     if (s->graph) { cudaGraphDestroy(s->graph); s->graph = nullptr; }
     // WHILE { per mode an IF node (narrowest first) around its kernels ; finalize }
@@ -1168,6 +1197,12 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
     }
     PRGPU_CUDA(cudaGraphInstantiate(&s->exec, s->graph, 0));
     s->use_graph = true;
+}
+
+void part_sent_rows(prgpu_session* s, uint64_t* rows, uint32_t* row_doubles) {
+    if (s->parts.empty()) fail(PRGPU_EINVAL, "not a partition session");
+    *rows = s->sent_rows;
+    *row_doubles = (uint32_t)s->cfg.KS;
 }
 
 // the whole fused partitioned loop, enqueued on the session's stream

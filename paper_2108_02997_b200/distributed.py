@@ -37,6 +37,7 @@ class PartResult:
     ranks: Optional[np.ndarray]  # [K, n] original vertex ids (when gathered)
     run_iterations: int
     loop_ms: float
+    sent_bytes: int = 0        # fused exchange: bytes this rank stores into peers per all-lanes iteration
 
 
 class _Part:
@@ -101,6 +102,12 @@ class _Part:
 
     def launch(self):
         check(lib().prgpu_part_launch(self._s), "part launch")
+
+    def sent_bytes(self) -> int:
+        """Bytes this rank stores into its peers per all-lanes iteration (fused)."""
+        rows, rd = C.c_uint64(), C.c_uint32()
+        check(lib().prgpu_part_sent_rows(self._s, C.byref(rows), C.byref(rd)), "sent rows")
+        return int(rows.value) * int(rd.value) * 8
 
     def step(self) -> int:
         par = C.c_int()
@@ -211,6 +218,8 @@ def _emulate_on(parts, alphas, max_iterations, want_ranks, g, fused=False, graph
         res.ranks = _assemble(g, chunks, K)
     res.iterations[:] = _lane_iterations(parts[0])
     res.run_iterations = int(res.iterations.max())
+    if fused:
+        res.sent_bytes = max(p.sent_bytes() for p in parts)
     for p in parts:
         p.close()
     return res
@@ -299,7 +308,7 @@ def _run_peer_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ran
         K = len(alphas)
         lane_its = _lane_iterations(part)
         res = PartResult(iterations=lane_its, ranks=None, run_iterations=int(lane_its.max()),
-                         loop_ms=start.elapsed_time(stop))
+                         loop_ms=start.elapsed_time(stop), sent_bytes=part.sent_bytes())
         if world > 1:
             dist.barrier()  # no peer still stores into our buffers
         if want_ranks:

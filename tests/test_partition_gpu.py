@@ -73,6 +73,22 @@ def test_fused_peer_exchange_emulated(prl, nranks, alphas):
         assert np.max(np.abs(got.ranks[k] - want.results[k].ranks)) <= 1e-13
 
 
+def test_fused_exchange_sends_only_needed_rows(prl, monkeypatch):
+    """Needed-only exchange: each rank stores fewer rows than 'every source row
+    to every peer' (PRGPU_NEED=0), with identical results; one rank sends
+    nothing."""
+    from paper_2108_02997_b200 import distributed
+    g = prl.generate_rmat(14, 16, 0.57, 0.19, 0.19, 2108)
+    alphas = [0.5, 0.85, 1.0]
+    assert distributed.emulate(g, alphas, 1, 1e-9, fused=True).sent_bytes == 0
+    need = distributed.emulate(g, alphas, 3, 1e-9, fused=True)
+    monkeypatch.setenv("PRGPU_NEED", "0")
+    every = distributed.emulate(g, alphas, 3, 1e-9, fused=True)
+    assert 0 < need.sent_bytes < every.sent_bytes
+    assert np.array_equal(need.iterations, every.iterations)
+    assert np.array_equal(need.ranks, every.ranks)
+
+
 def test_fused_peer_graph_loop_single_rank(prl):
     """One rank, the whole loop as the CUDA graph prgpu_part_launch enqueues
     (the finalize kernel's arrival wait included)."""
