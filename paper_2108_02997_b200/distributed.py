@@ -280,20 +280,38 @@ def _run_peer_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ran
     import torch.distributed as dist
     part = _Part(g, alphas, tolerance, norm, max_iterations, stop_mask, rank, world, g.device, fused=True)
     part.set_stream()
-    mine = [_ipc_export(t.data_ptr()) for t in (part.contrib, part.partials, part.arrive)] if world > 1 else []
+    opened = []  # (ptr, offset) to close
+    peers = ([], [], [])
+    ok = True
+    try:
+        mine = [_ipc_export(t.data_ptr()) for t in (part.contrib, part.partials, part.arrive)] if world > 1 else []
+    except Exception:
+        ok, mine = False, []
     table = [None] * world
     if world > 1:
         dist.all_gather_object(table, mine)
-    opened = []  # (ptr, offset) to close
-    peers = ([], [], [])
-    for r in range(world):
-        if r == rank:
-            continue
-        for j in range(3):
-            hnd, off = table[r][j]
-            ptr = _ipc_open(hnd, off, g.device)
-            opened.append((ptr, off))
-            peers[j].append(ptr)
+        ok = ok and all(t for t in table)
+        for r in range(world):
+            if r == rank or not ok:
+                continue
+            for j in range(3):
+                try:
+                    hnd, off = table[r][j]
+                    ptr = _ipc_open(hnd, off, g.device)
+                except Exception:
+                    ok = False
+                    break
+                opened.append((ptr, off))
+                peers[j].append(ptr)
+        # every rank mapped every peer, or all fall back to the NCCL exchange
+        flag = torch.tensor([1 if ok else 0], device=part.contrib.device, dtype=torch.int32)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            for ptr, off in opened:
+                lib().prgpu_ipc_close(C.c_void_p(ptr), off)
+            part.close()
+            return _run_distributed_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ranks,
+                                       rank, world)
     try:
         part.set_peers(*peers)
         part.init()
