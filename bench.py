@@ -637,7 +637,7 @@ def measure_e2e(args, cfg, g, prl, torch, dev, lane_its):
         del dbuf
     except Exception:
         pass
-    if os.environ.get("PRGPU_TIMING_LOG"):
+    if os.environ.get("PRGPU_TIMING_LOG") or os.environ.get("PRGPU_E2E_SPLIT"):
         for a_, b_, c_ in split:
             print(f"e2e split: from_csr {a_ * 1e3:.1f} ms, pagerank {b_ * 1e3:.1f} ms, free {c_ * 1e3:.1f} ms",
                   file=sys.stderr)
