@@ -412,3 +412,64 @@ def test_acceptance_sensitivity_and_damping_trend(prl, oracle, small_golden):
     for a, it in its.items():
         assert it == sf["damping"][f"{a:.2f}"], (a, it)
     assert 2.0 <= its[0.95] / its[0.85] <= 4.0 and 0.4 <= its[0.75] / its[0.85] <= 0.8
+
+
+def _structural_graphs():
+    """Shapes that stress the task decomposition: one huge hub row (chunk
+    hand-off), one huge source, chains, isolated vertices, no edges, dense
+    rows, rows exactly at the chunk/packed thresholds, self-loops."""
+    rng = np.random.default_rng(99)
+    out = {}
+    n = 300_001
+    src = np.arange(1, n, dtype=np.uint32)
+    out["big_star_in"] = (n, np.concatenate([np.stack([src, np.zeros_like(src)], 1), [[0, 1]]]))
+    out["big_star_out"] = (n, np.stack([np.zeros_like(src), src], 1))
+    m = 100_000
+    a = np.arange(m - 1, dtype=np.uint32)
+    out["chain"] = (m, np.stack([a, a + 1], 1))
+    out["one_edge"] = (1000, np.array([[5, 7]], np.uint32))
+    out["no_edges"] = (10, np.zeros((0, 2), np.uint32))
+    k = 50
+    ii, jj = np.meshgrid(np.arange(k), np.arange(k))
+    msk = ii != jj
+    out["complete_50"] = (k, np.stack([ii[msk], jj[msk]], 1).astype(np.uint32))
+    # target t gets exactly d in-edges from distinct sources, d at the thresholds
+    degs = [1, 8, 9, 32, 33, 128, 129, 256, 257, 512, 513, 2048, 2049, 4096, 4097, 8193]
+    nn = 20_000
+    pairs = []
+    for t, d in enumerate(degs):
+        s = rng.choice(np.arange(len(degs), nn), size=d, replace=False)
+        pairs.append(np.stack([s, np.full(d, t)], 1))
+    extra = rng.integers(0, nn, size=(40_000, 2))
+    out["thresholds"] = (nn, np.concatenate(pairs + [extra]).astype(np.uint32))
+    nl = 5000
+    loops = np.arange(nl, dtype=np.uint32)
+    out["self_loops"] = (nl, np.concatenate([np.stack([loops, loops], 1),
+                                             rng.integers(0, nl, size=(20_000, 2)).astype(np.uint32)]))
+    return out
+
+
+@pytest.mark.parametrize("name", ["big_star_in", "big_star_out", "chain", "one_edge", "no_edges",
+                                  "complete_50", "thresholds", "self_loops"])
+def test_structural_edge_cases_vs_oracle(prl, oracle, name):
+    n, pairs = _structural_graphs()[name]
+    flat = np.ascontiguousarray(pairs, np.uint32).reshape(-1)
+    g = prl.build_csr(edge_list(prl, n, flat))
+    want_g = oracle.build_csr(n, flat)
+    assert np.array_equal(g.in_offsets, want_g.in_offsets) and np.array_equal(g.in_neighbors, want_g.in_neighbors)
+    h = oracle.build_csr_handle(n, flat)
+    try:
+        for norm in NORMS:  # K = 1, every norm
+            want = oracle.pagerank(h, 0.85, 1e-10, norm, 500, trace=True)
+            got = prl.pagerank(g, prl.PageRankConfig(0.85, 1e-10, nk(prl, norm), 500))
+            assert iterations_match(got.iterations, want["iterations"], want["err_trace"], 1e-10), (norm,)
+            assert np.max(np.abs(got.ranks - want["ranks"])) <= RANK_TOL, norm
+        alphas = [0.5, 0.85, 1.0]  # batched lanes (lane-width modes switch as they stop)
+        br = prl.pagerank_batched(g, alphas, 1e-9, prl.NormKind.L1, 300)
+        for k, a in enumerate(alphas):
+            want = oracle.pagerank(h, a, 1e-9, "l1", 300, trace=True)
+            r = br.results[k]
+            assert iterations_match(r.iterations, want["iterations"], want["err_trace"], 1e-9), (a,)
+            assert np.max(np.abs(r.ranks - want["ranks"])) <= RANK_TOL, a
+    finally:
+        oracle.free_csr(h)
