@@ -64,3 +64,20 @@ def test_c5_rmat28_k3_one_step_oracle(prl, oracle):
         assert abs(err - full.results[k].final_err) <= 1e-9 * err, (a, err, full.results[k].final_err)
         assert full.trace[t - 2, k, 1] >= TOL * (1 + 1e-3), (a, full.trace[t - 2, k, 1])
         del capped, prev
+
+
+def test_c5_two_rank_fused_partition_matches_single_gpu(prl):
+    """The multi-GPU path at the largest config: two ranks of the 1D
+    partition, fused peer exchange with lane modes and needed-only rows,
+    emulated on one GPU (the ranks run one after another, stores land in each
+    other's buffers), against the single-GPU run: same iterations per lane,
+    ranks within 1e-13 (only the rank-order reduction of the partials
+    differs)."""
+    from paper_2108_02997_b200 import distributed
+    g = prl.generate_rmat(28, 16, 0.57, 0.19, 0.19, 2108)
+    single = prl.pagerank_batched(g, ALPHAS, TOL, prl.NormKind.L2, 500)
+    two = distributed.emulate(g, ALPHAS, 2, TOL, prl.NormKind.L2, 500, want_ranks=True, fused=True)
+    assert two.sent_bytes > 0
+    for k in range(len(ALPHAS)):
+        assert two.iterations[k] == single.results[k].iterations, k
+        assert float(np.max(np.abs(two.ranks[k] - single.results[k].ranks))) <= 1e-13, k
