@@ -211,12 +211,6 @@ struct LaneCfg {
     }
 };
 
-// PRGPU_VARIANT (env, tuning only) selects alternative instantiations.
-inline int variant() {
-    const char* v = std::getenv("PRGPU_VARIANT");
-    return v ? std::atoi(v) : 0;
-}
-
 // per-mode instance alternatives (tuning only)
 inline int k_variant(const char* name) {
     const char* v = std::getenv(name);
@@ -237,7 +231,7 @@ LaneCfg wide_cfg(bool all_q) {
                  : mk_cfg<LG, W, WIN, 0, MINB, kQmL1, KS, PATHS>();
 }
 
-// Defaults measured on B200 (scripts/gpu_variants*.sh).
+// Defaults measured on B200 (scripts/experiments/gpu_variants*.sh).
 // Wide lanes: two doubles per thread (one 16-byte load per edge), LG = KS/2
 // threads per edge, rows padded to whole 32-byte sectors; up to four lanes,
 // one double per thread (LG = KS).
@@ -251,24 +245,8 @@ LaneCfg lane_cfg_t(int K, bool all_q) {
     return wide_cfg<8, 2, 128, 4, 16, PATHS>(all_q);
 }
 
-// One kernel per iteration (PATHS = 3); PRGPU_VARIANT selects the
-// alternatives that lost (tuning only).
-inline LaneCfg lane_cfg(int K, bool all_q) {
-    const int var = variant();
-    if (K == 1) {
-        switch (var) {
-        case 1: return mk_cfg<1, 1, 256, 4, 2, kQmAll, 0>();
-        case 2: return mk_cfg<1, 1, 256, 4, 3, kQmAll, 0>();
-        case 3: return mk_cfg<1, 1, 256, 2, 4, kQmAll, 0>();
-        default: break;
-        }
-    } else if (K > 8 && K <= 12) {
-        if (var == 1) return wide_cfg<8, 2, 64, 4, 12>(all_q);
-        if (var == 2) return wide_cfg<8, 2, 128, 3, 12>(all_q);
-        if (var == 3) return wide_cfg<8, 2, 64, 3, 12>(all_q);
-    }
-    return lane_cfg_t<3>(K, all_q);
-}
+// The run's base configuration: one kernel per iteration (PATHS = 3).
+inline LaneCfg lane_cfg(int K, bool all_q) { return lane_cfg_t<3>(K, all_q); }
 
 // Lane-width modes of a K > 1 run (Params::mode_id): the same window and task
 // tables (an instance's WIN must be >= the run's: its shared-memory stage is
@@ -792,7 +770,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         const bool k1split = s->K == 1 && (ks1 ? std::atoi(ks1) == 1 : k1auto);
         const char* km = std::getenv("PRGPU_K1MINB");
         const int k1_minb4 = km ? std::atoi(km) : (P.n_chunk == 0 ? 2 : 0);
-        const bool modal = (s->K > 1 || k1split) && !(sp && std::atoi(sp) == 0) && variant() == 0;
+        const bool modal = (s->K > 1 || k1split) && !(sp && std::atoi(sp) == 0);
         if (modal) {
             const int wide = s->cfg.KP(); // (measured: 12 lanes as 4 threads x 3 lost 30%)
             for (int kp = 1; kp <= wide; kp *= 2) {
