@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <memory>
+#include <mutex>
 #include <vector>
 #include <chrono>
 #include <thread>
@@ -305,6 +306,41 @@ inline unsigned blocks_for(uint64_t n) {
 
 using namespace prgpu;
 
+namespace prgpu {
+// Host-mapped int slots (the per-lane stop iterations a session's finalizer
+// writes for the host): cudaHostAlloc / cudaFreeHost cost ~1 ms each and may
+// synchronise, so slots come from a process-wide pool of portable mapped
+// blocks (under UVA the device address equals the host address).
+constexpr int kSlotInts = 64; // >= PRGPU_MAX_LANES
+struct MappedSlots {
+    std::mutex mu;
+    std::vector<int*> free;
+};
+inline MappedSlots& mapped_slots() {
+    static MappedSlots m;
+    return m;
+}
+inline int* mapped_slot_get() {
+    MappedSlots& M = mapped_slots();
+    std::lock_guard<std::mutex> lk(M.mu);
+    if (M.free.empty()) {
+        constexpr int kSlots = 256;
+        int* base = nullptr;
+        PRGPU_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&base), (size_t)kSlots * kSlotInts * sizeof(int),
+                                 cudaHostAllocMapped | cudaHostAllocPortable));
+        for (int i = kSlots - 1; i >= 0; --i) M.free.push_back(base + (size_t)i * kSlotInts);
+    }
+    int* h = M.free.back();
+    M.free.pop_back();
+    return h;
+}
+inline void mapped_slot_put(int* h) {
+    MappedSlots& M = mapped_slots();
+    std::lock_guard<std::mutex> lk(M.mu);
+    M.free.push_back(h);
+}
+} // namespace prgpu
+
 struct prgpu_session {
     prgpu_graph* g = nullptr;
     int K = 1, KP = 1, max_iter = 500;
@@ -358,7 +394,7 @@ struct prgpu_session {
     std::unique_ptr<Stream> aux;
 
     ~prgpu_session() {
-        if (host_frozen) cudaFreeHost(host_frozen);
+        if (host_frozen) prgpu::mapped_slot_put(host_frozen);
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
         if (e0) cudaEventDestroy(e0);
@@ -698,7 +734,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     P.npeers = 0;
     P.arrive = nullptr;
     if (nranks == 0) {
-        PRGPU_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->host_frozen), K * sizeof(int), cudaHostAllocMapped));
+        s->host_frozen = mapped_slot_get();
         std::fill(s->host_frozen, s->host_frozen + K, 0);
         PRGPU_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&s->dev_frozen), s->host_frozen, 0));
         P.frozen_at = s->dev_frozen;
@@ -716,7 +752,9 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     P.cbase = cbase;
     P.cold_off[0] = 0;
     P.cold_off[1] = nsrc;
+    ph.mark("params");
     build_tasks(s.get());
+    ph.mark("tasks");
     if (nranks >= 1) { // partition session (nranks == 0: the fused single-GPU run)
         if (rank < 0 || rank >= nranks) fail(PRGPU_EINVAL, "partition: rank out of range");
         plan_partition(s.get(), nranks);
@@ -881,6 +919,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         }
         return cols;
     };
+    ph.mark("modes");
     size_t part_cols = 0;
     if (nranks >= 1 && modes.size() > 1) {
         // partitions: the full mode list for the fused exchange, kept aside;
