@@ -52,7 +52,7 @@ namespace pagerank_lab::cuda {
 // ---------------------------------------------------------------------------
 // errors
 // ---------------------------------------------------------------------------
-namespace detail {
+namespace b200_detail {
 inline void check(int status, const char* what) {
     if (status == PRGPU_OK) return;
     std::string msg = std::string(what) + ": " + prgpu_last_error();
@@ -65,7 +65,7 @@ inline int default_device() {
     if (const char* v = std::getenv("LOCAL_RANK")) return std::atoi(v);
     return 0;
 }
-} // namespace detail
+} // namespace b200_detail
 
 // ---------------------------------------------------------------------------
 // norms.hpp:18-78
@@ -100,8 +100,8 @@ inline double error_norm(NormKind kind, std::span<const double> r, std::span<con
                                     " vs " + std::to_string(s.size()) + ")");
     if (r.empty()) throw std::invalid_argument("error_norm: empty vectors");
     double out = 0;
-    detail::check(prgpu_error_norm(static_cast<int>(kind), r.data(), s.data(), r.size(),
-                                   detail::default_device(), &out),
+    b200_detail::check(prgpu_error_norm(static_cast<int>(kind), r.data(), s.data(), r.size(),
+                                   b200_detail::default_device(), &out),
                   "error_norm");
     return out;
 }
@@ -146,8 +146,8 @@ struct CsrGraph {
         if (!state_->graph) {
             if (vertex_count == 0) throw std::invalid_argument("pagerank: graph has no vertices");
             prgpu_graph* g = nullptr;
-            detail::check(prgpu_graph_from_csr(vertex_count, in_offsets.data(), in_neighbors.data(),
-                                               out_degree.data(), detail::default_device(), &g),
+            b200_detail::check(prgpu_graph_from_csr(vertex_count, in_offsets.data(), in_neighbors.data(),
+                                               out_degree.data(), b200_detail::default_device(), &g),
                           "graph_from_csr");
             state_->graph.reset(g, prgpu_graph_free);
         }
@@ -164,18 +164,18 @@ private:
     std::shared_ptr<State> state_ = std::make_shared<State>();
 };
 
-namespace detail {
+namespace b200_detail {
 // pairs from prgpu_mtx_parse / prgpu_mtx_load into an EdgeList
 inline EdgeList take_pairs(std::uint32_t n, std::uint32_t* pairs, std::uint64_t m) {
     EdgeList el;
     el.vertex_count = n;
     el.edges.resize(m);
     static_assert(sizeof(std::pair<std::uint32_t, std::uint32_t>) == 8);
-    if (m) std::memcpy(el.edges.data(), pairs, m * 8);
+    if (m) std::memcpy(static_cast<void*>(el.edges.data()), pairs, m * 8);
     prgpu_pairs_free(pairs);
     return el;
 }
-} // namespace detail
+} // namespace b200_detail
 
 /// graph.hpp:111-199: the library's multi-threaded MatrixMarket parser
 /// (prgpu_mtx_parse), same language, same MtxParseError lines and messages.
@@ -188,11 +188,11 @@ inline EdgeList parse_matrix_market(std::istream& in) {
         const std::string msg = prgpu_last_error(), prefix = "line " + std::to_string(line) + ": ";
         throw MtxParseError(line, msg.rfind(prefix, 0) == 0 ? msg.substr(prefix.size()) : msg);
     }
-    detail::check(st, "parse_matrix_market");
-    return detail::take_pairs(n, pairs, m);
+    b200_detail::check(st, "parse_matrix_market");
+    return b200_detail::take_pairs(n, pairs, m);
 }
 
-namespace detail {
+namespace b200_detail {
 inline CsrGraph download(prgpu_graph* g) {
     prgpu_graph_info info{};
     check(prgpu_graph_get_info(g, &info), "graph info");
@@ -208,7 +208,7 @@ inline CsrGraph download(prgpu_graph* g) {
     out.attach(g);
     return out;
 }
-} // namespace detail
+} // namespace b200_detail
 
 /// graph.hpp:204-234 on the device.  The returned host arrays are identical
 /// to the reference build_csr's; the device copy is kept for pagerank().
@@ -216,10 +216,10 @@ inline CsrGraph build_csr(EdgeList el) {
     if (el.vertex_count == 0) throw std::invalid_argument("build_csr: vertex_count must be >= 1");
     static_assert(sizeof(std::pair<std::uint32_t, std::uint32_t>) == 8);
     prgpu_graph* g = nullptr;
-    detail::check(prgpu_graph_build(el.vertex_count, reinterpret_cast<const std::uint32_t*>(el.edges.data()),
-                                    el.edges.size(), detail::default_device(), &g),
+    b200_detail::check(prgpu_graph_build(el.vertex_count, reinterpret_cast<const std::uint32_t*>(el.edges.data()),
+                                    el.edges.size(), b200_detail::default_device(), &g),
                   "build_csr");
-    return detail::download(g);
+    return b200_detail::download(g);
 }
 
 /// graph.hpp:238-247: file parsed in place (mmap) by all host threads;
@@ -229,18 +229,18 @@ inline EdgeList load_matrix_market(const std::filesystem::path& path) {
     std::uint64_t m = 0, line = 0;
     const int st = prgpu_mtx_load(path.string().c_str(), 0, &n, &pairs, &m, &line);
     if (st == PRGPU_EPARSE || st == PRGPU_EIO) throw std::runtime_error(prgpu_last_error());
-    detail::check(st, "load_matrix_market");
-    return detail::take_pairs(n, pairs, m);
+    b200_detail::check(st, "load_matrix_market");
+    return b200_detail::take_pairs(n, pairs, m);
 }
 
 /// graph.hpp:249-251: parallel parse, build_csr on the device.
 inline CsrGraph load_csr_graph(const std::filesystem::path& path) {
     prgpu_graph* g = nullptr;
     std::uint64_t line = 0;
-    const int st = prgpu_graph_load_mtx(path.string().c_str(), 0, detail::default_device(), &g, &line);
+    const int st = prgpu_graph_load_mtx(path.string().c_str(), 0, b200_detail::default_device(), &g, &line);
     if (st == PRGPU_EPARSE || st == PRGPU_EIO) throw std::runtime_error(prgpu_last_error());
-    detail::check(st, "load_csr_graph");
-    return detail::download(g);
+    b200_detail::check(st, "load_csr_graph");
+    return b200_detail::download(g);
 }
 
 // ---------------------------------------------------------------------------
@@ -273,12 +273,12 @@ struct PageRankResult {
 
 using IterationObserver = std::function<void(int iteration, std::span<const double> ranks, double error)>;
 
-namespace detail {
+namespace b200_detail {
 inline void observer_trampoline(int it, int, const double* ranks, std::uint64_t n, double err, void* user) {
     auto* obs = static_cast<const IterationObserver*>(user);
     (*obs)(it, std::span<const double>(ranks, n), err);
 }
-} // namespace detail
+} // namespace b200_detail
 
 /// pagerank.hpp:70-108: the pull power iteration, run to convergence on the
 /// device.  `elapsed` is the device time of the iteration loop.
@@ -303,11 +303,11 @@ inline PageRankResult pagerank(const CsrGraph& g, const PageRankConfig& cfg,
     out.iterations = &iters;
     out.converged = &conv;
     if (on_iteration)
-        detail::check(prgpu_pagerank_observed(dg, &p, &out, detail::observer_trampoline,
+        b200_detail::check(prgpu_pagerank_observed(dg, &p, &out, b200_detail::observer_trampoline,
                                               const_cast<IterationObserver*>(&on_iteration)),
                       "pagerank");
     else
-        detail::check(prgpu_pagerank(dg, &p, &out), "pagerank");
+        b200_detail::check(prgpu_pagerank(dg, &p, &out), "pagerank");
     r.iterations = iters;
     r.converged = conv != 0;
     r.elapsed = std::chrono::duration<double, std::milli>(out.loop_ms);
@@ -367,7 +367,7 @@ inline BatchedRun pagerank_batched(const CsrGraph& g, std::span<const double> al
     out.iterations = its.data();
     out.converged = conv.data();
     out.err_trace = b.trace.data();
-    detail::check(prgpu_pagerank(g.device_graph(), &p, &out), "pagerank");
+    b200_detail::check(prgpu_pagerank(g.device_graph(), &p, &out), "pagerank");
     b.run_iterations = out.run_iterations;
     b.loop_ms = out.loop_ms;
     for (int k = 0; k < K; ++k) {
@@ -474,7 +474,7 @@ inline std::vector<double> default_tolerance_grid() {
             5e-6, 1e-6, 5e-7, 1e-7, 5e-8, 1e-8, 5e-9, 1e-9, 5e-10, 1e-10};
 }
 
-namespace detail {
+namespace b200_detail {
 inline void sweep_graph(const SweepPlan& plan, const CsrGraph& g, const std::string& label,
                         std::vector<SweepRecord>& out, std::ostream* log) {
     const RankVector ref = reference_ranks(g); // untimed warm-up (sweep.hpp:160-161)
@@ -536,7 +536,7 @@ inline void sweep_graph(const SweepPlan& plan, const CsrGraph& g, const std::str
                 }
     }
 }
-} // namespace detail
+} // namespace b200_detail
 
 /// sweep.hpp:146-243.  Graphs run one after another on the GPU; records come
 /// back sorted by (graph, norm, alpha, tolerance descending).
@@ -545,7 +545,7 @@ inline std::vector<SweepRecord> run_sweep(const SweepPlan& plan, std::ostream* l
     std::vector<SweepRecord> records;
     for (const auto& path : plan.graphs) {
         const CsrGraph g = load_csr_graph(path);
-        detail::sweep_graph(plan, g, path.stem().string(), records, log);
+        b200_detail::sweep_graph(plan, g, path.stem().string(), records, log);
     }
     std::sort(records.begin(), records.end(), [](const SweepRecord& a, const SweepRecord& b) {
         if (a.graph != b.graph) return a.graph < b.graph;
