@@ -231,6 +231,12 @@ PRGPU_API int prgpu_part_launch(prgpu_session* s);
 /* Fused exchange volume: contribution rows this rank stores into its peers
  * per iteration while every lane is live (rows of *row_doubles doubles). */
 PRGPU_API int prgpu_part_sent_rows(prgpu_session* s, uint64_t* rows, uint32_t* row_doubles);
+/* A fused partition deals its work round-robin (prgpu_part_set_peers; the
+ * rank's rows are then not one range): *dealt = 1, and every lane's final
+ * value of the rows this rank owns is written at its ENGINE row into
+ * dev_out[lane * ld + row] (ld >= vertex_count; other entries untouched, so
+ * a sum over ranks of zero-initialised buffers gives the whole vector). */
+PRGPU_API int prgpu_part_owned_ranks_device(prgpu_session* s, double* dev_out, uint64_t ld, int* dealt);
 /* CUDA IPC for the fused exchange's buffers (any pointer inside a device
  * allocation): export a 64-byte handle + offset; open it in another process
  * of the same node (peer access enabled); close with the pointer open gave. */

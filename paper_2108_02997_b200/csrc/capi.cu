@@ -54,6 +54,7 @@ void part_plan_copy(prgpu_session*, prgpu_partition*);
 void part_set_stream(prgpu_session*, void*);
 void graph_permutation(const prgpu_graph*, uint32_t*);
 void part_sent_rows(prgpu_session*, uint64_t*, uint32_t*);
+void part_owned_ranks_device(prgpu_session*, double*, uint64_t, int*);
 
 uint64_t graph_rows(const prgpu_graph*, const uint32_t*, uint32_t, uint64_t*, uint32_t*, uint64_t, cudaStream_t);
 void session_destroy(prgpu_session*);
@@ -448,6 +449,13 @@ int prgpu_part_sent_rows(prgpu_session* s, uint64_t* rows, uint32_t* row_doubles
     return guarded([&] {
         if (!s || !rows || !row_doubles) prgpu::fail(PRGPU_EINVAL, "null argument");
         prgpu::part_sent_rows(s, rows, row_doubles);
+    });
+}
+
+int prgpu_part_owned_ranks_device(prgpu_session* s, double* dev_out, uint64_t ld, int* dealt) {
+    return guarded([&] {
+        if (!s || !dealt) prgpu::fail(PRGPU_EINVAL, "null argument");
+        prgpu::part_owned_ranks_device(s, dev_out, ld, dealt);
     });
 }
 

@@ -103,6 +103,21 @@ __global__ void local_ranks_kernel(Params P, LaneMap map, uint32_t row_begin, ui
     }
 }
 
+// dealt partitions: every lane's value of the rows this rank owns, at their
+// engine row in out[lane][ld] (other rows untouched)
+__global__ void owned_ranks_kernel(Params P, LaneMap map, const uint8_t* __restrict__ owner, int me,
+                                   double* __restrict__ out, uint64_t ld) {
+    const uint64_t total = (uint64_t)P.n * P.K;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = (uint32_t)(x / P.n), r = (uint32_t)(x - (uint64_t)k * P.n);
+        if (owner[r] != me) continue;
+        const LaneState& L = P.lanes[k];
+        const double v = r >= P.empty_begin ? L.c0_used : P.rank[L.iterations & 1][(size_t)r * P.ks + k];
+        out[(size_t)map.user_of[k] * ld + r] = v;
+    }
+}
+
 __global__ void scatter_ref(const double* __restrict__ in, const uint32_t* __restrict__ new_of_old,
                             double* __restrict__ out, uint32_t n) {
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n;
@@ -380,6 +395,11 @@ struct prgpu_session {
     double last_loop_ms = 0;
     // multi-GPU partition
     int part_rank = 0, nranks = 1, host_iter = 0;
+    uint32_t n_long = 0;        // rows cut into chunk tasks
+    bool dealt = false;         // fused partition: work units dealt round-robin (task lists, row owners)
+    DevBuf<uint32_t> task_list; // this rank's tasks, ascending: hub chunks, then packed + empty
+    DevBuf<uint8_t> row_owner;  // [n] rank owning each row
+    uint32_t deal_split = 0, deal_total = 0; // task_list: [0, split) hub chunks, [split, total) the rest
     std::vector<prgpu_partition> parts;
     DevBuf<double> rank_partials;
     uint64_t sent_rows = 0;    // fused exchange: contribution rows stored into peers per iteration
@@ -465,8 +485,10 @@ void build_tasks(prgpu_session* s) {
     PRGPU_LAUNCHED("count_long_rows");
     unsigned int n_long = 0;
     PRGPU_CUDA(cudaMemcpyAsync(&n_long, cnt.p, 4, cudaMemcpyDeviceToHost, st));
+    s->n_long = 0; // set once known (below)
     PRGPU_CUDA(cudaStreamSynchronize(st));
 
+    s->n_long = n_long;
     DevBuf<uint64_t> first((size_t)n_long + 1);
     chunk_counts<<<blocks_for((uint64_t)n_long + 1), kNT, 0, st>>>(g->row_off.p, n_long, emax, first.p);
     PRGPU_LAUNCHED("chunk_counts");
@@ -888,7 +910,10 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
             const LaneCfg& A = ml[m].second.first;
             const LaneCfg& B = ml[m].second.second;
             size_t sa = 0, sb = 0;
-            const uint32_t GA = a1 > a0 ? grid_for_cfg(A, a1 - a0, sa) : 0;
+            // partitions keep a hub-chunk kernel even for an empty range: a
+            // dealt plan (deal_tasks) may hand this rank hub rows later
+            const uint32_t na = a1 > a0 ? a1 - a0 : (nranks >= 1 && T1 ? std::max(1u, T1 / (uint32_t)nranks) : 0u);
+            const uint32_t GA = na ? grid_for_cfg(A, na, sa) : 0;
             const uint32_t GB = grid_for_cfg(B, std::max(1u, b1 - b0), sb);
             Params PM = Q;
             PM.mode_id = m;
@@ -1016,12 +1041,14 @@ void part_set_stream(prgpu_session* s, void* stream) { s->ext_stream = (cudaStre
 // need[src] bit q: some row of rank q has source src as an in-neighbour (one
 // warp per row; rows of rank q are [bound[q], bound[q+1]))
 __global__ void need_kernel(const uint64_t* __restrict__ row_off, const uint32_t* __restrict__ col,
-                            uint32_t rows, const uint32_t* __restrict__ bound, int nranks,
-                            unsigned int* __restrict__ need) {
+                            uint32_t rows, const uint32_t* __restrict__ bound, const uint8_t* __restrict__ owner,
+                            int nranks, unsigned int* __restrict__ need) {
     const uint32_t lane = threadIdx.x & 31;
     for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += (gridDim.x * blockDim.x) >> 5) {
         int q = 0;
-        while (q + 1 < nranks && r >= bound[q + 1]) ++q;
+        if (owner) q = owner[r];
+        else
+            while (q + 1 < nranks && r >= bound[q + 1]) ++q;
         const uint32_t bit = 1u << q;
         for (uint64_t j = row_off[r] + lane; j < row_off[r + 1]; j += 32) {
             const uint32_t src = col[j];
@@ -1030,15 +1057,80 @@ __global__ void need_kernel(const uint64_t* __restrict__ row_off, const uint32_t
     }
 }
 
+// Dealt partition (fused exchange): the work units — a hub row with all its
+// chunk tasks, a packed run, an empty-row task — go to the ranks snake-wise
+// (0..N-1, N-1..0, ...) within each kind, so every rank pulls a similar
+// share of the hottest rows and, above all, publishes a similar share of the
+// most-gathered sources (contiguous cost ranges put all hub rows, whose
+// sources every rank gathers, on the first ranks: its NVLink egress bounded
+// the iteration).  Each rank gets its ascending task list and every row's
+// owner.  Needs the split iteration (hub-chunk and packed kernels) and
+// PRGPU_DEAL != 0.
+__global__ void fill_owner(uint8_t* __restrict__ owner, uint32_t lo, uint32_t hi, uint8_t q) {
+    for (uint32_t r = lo + blockIdx.x * blockDim.x + threadIdx.x; r < hi; r += gridDim.x * blockDim.x) owner[r] = q;
+}
+
+void deal_tasks(prgpu_session* s) {
+    s->dealt = false;
+    Params& P = s->P;
+    P.task_list = nullptr;
+    P.row_owner = nullptr;
+    const char* dv = std::getenv("PRGPU_DEAL");
+    const int N = s->nranks;
+    bool split = false;
+    for (const auto& l : s->launches) split |= l.P.no_finalize != 0;
+    if (N < 2 || (dv && std::atoi(dv) == 0) || !split) return;
+    cudaStream_t st = s->stream;
+    const uint32_t n = s->g->n, nl = s->n_long, T1 = P.n_chunk, np = P.n_packed, ne = P.n_empty_tasks;
+    std::vector<uint32_t> cf((size_t)nl + 1), pr((size_t)np + 1);
+    PRGPU_CUDA(cudaMemcpyAsync(cf.data(), s->chunk_first.p, cf.size() * 4, cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaMemcpyAsync(pr.data(), s->packed_r0.p, pr.size() * 4, cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    auto snake = [N](uint32_t u) { const uint32_t r = u / N, q = u % N; return (r & 1) ? N - 1 - q : q; };
+    const int me = s->part_rank;
+    std::vector<uint32_t> list;
+    std::vector<uint8_t> owner(n, 0); // rows without a task (isolated) stay on rank 0
+    for (uint32_t u = 0; u < nl; ++u) {
+        const uint32_t q = snake(u);
+        owner[u] = (uint8_t)q;
+        if ((int)q == me)
+            for (uint32_t t = cf[u]; t < cf[u + 1]; ++t) list.push_back(t);
+    }
+    const uint32_t split_at = (uint32_t)list.size();
+    for (uint32_t k = 0; k < np; ++k) {
+        const uint32_t q = snake(k);
+        std::fill(owner.begin() + pr[k], owner.begin() + pr[k + 1], (uint8_t)q);
+        if ((int)q == me) list.push_back(T1 + k);
+    }
+    for (uint32_t e = 0; e < ne; ++e) {
+        const uint32_t q = snake(e);
+        const uint64_t lo = (uint64_t)P.empty_begin + (uint64_t)e * P.er, hi = std::min<uint64_t>(lo + P.er, n);
+        std::fill(owner.begin() + lo, owner.begin() + hi, (uint8_t)q);
+        if ((int)q == me) list.push_back(T1 + np + e);
+    }
+    s->task_list.alloc(std::max<size_t>(list.size(), 1));
+    s->row_owner.alloc(n);
+    if (!list.empty())
+        PRGPU_CUDA(cudaMemcpyAsync(s->task_list.p, list.data(), list.size() * 4, cudaMemcpyHostToDevice, st));
+    PRGPU_CUDA(cudaMemcpyAsync(s->row_owner.p, owner.data(), n, cudaMemcpyHostToDevice, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st)); // host vectors go out of scope
+    s->deal_split = split_at;
+    s->deal_total = (uint32_t)list.size();
+    P.task_list = s->task_list.p;
+    P.row_owner = s->row_owner.p;
+    s->dealt = true;
+}
+
 // rows this rank stores into peers per iteration (widest mode): for each
 // source of its rows, the peers that gather it (all peers without a mask)
 __global__ void sent_rows_kernel(const uint2* __restrict__ rowinfo, uint32_t row_begin, uint32_t row_end,
-                                 const uint8_t* __restrict__ need, uint32_t others, int npeers,
-                                 unsigned long long* __restrict__ out) {
+                                 const uint8_t* __restrict__ owner, int me, const uint8_t* __restrict__ need,
+                                 uint32_t others, int npeers, unsigned long long* __restrict__ out) {
     unsigned long long c = 0;
     for (uint32_t r = row_begin + blockIdx.x * blockDim.x + threadIdx.x; r < row_end; r += gridDim.x * blockDim.x) {
         const uint2 ri = rowinfo[r];
-        if (ri.x) c += need ? (unsigned long long)__popc(need[ri.y] & others) : (unsigned long long)npeers;
+        if (ri.x && (!owner || owner[r] == me))
+            c += need ? (unsigned long long)__popc(need[ri.y] & others) : (unsigned long long)npeers;
     }
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
@@ -1081,6 +1173,7 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
     for (int q = 0; q < npeers; ++q)
         if (!peer_contrib[q] || !peer_rp[q] || !peer_arrive[q]) fail(PRGPU_EINVAL, "set_peers: null peer pointer");
     P.arrive = arrive;
+    deal_tasks(s); // before the exchange mask: it decides which rank owns each row
     // only the peers that gather a source receive its row (PRGPU_NEED=0: all)
     P.need = nullptr;
     const char* nv = std::getenv("PRGPU_NEED");
@@ -1096,7 +1189,8 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
         const uint32_t rows = s->P.empty_begin; // rows with in-edges
         if (rows) {
             need_kernel<<<(unsigned)std::min<uint64_t>(((uint64_t)rows * 32 + kNT - 1) / kNT, 148ull * 64), kNT, 0,
-                          s->stream>>>(s->g->row_off.p, s->g->col.p, rows, bound.p, s->nranks, s->need.p);
+                          s->stream>>>(s->g->row_off.p, s->g->col.p, rows, bound.p, P.row_owner, s->nranks,
+                                       s->need.p);
             PRGPU_LAUNCHED("need");
         }
         PRGPU_CUDA(cudaStreamSynchronize(s->stream));
@@ -1114,6 +1208,11 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
         l.P.task_end = keep.task_end;
         l.P.no_finalize = keep.no_finalize; // split: hub-chunk kernel, then packed + finalize
         l.P.mode_id = keep.mode_id;
+        if (s->dealt) { // hub-chunk kernels take the list's chunk tasks, the others the rest
+            const bool hub = keep.no_finalize != 0; // the split iteration's first kernel
+            l.P.list_begin = hub ? 0u : s->deal_split;
+            l.P.list_end = hub ? s->deal_split : s->deal_total;
+        }
         l.P.cbase = keep.cbase;
         l.P.cold_off[0] = keep.cold_off[0];
         l.P.cold_off[1] = keep.cold_off[1];
@@ -1133,9 +1232,10 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
         const uint32_t others = ((1u << s->nranks) - 1u) & ~(1u << s->part_rank);
         DevBuf<unsigned long long> cnt(1);
         PRGPU_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), s->stream));
-        if (me.row_end > me.row_begin)
-            sent_rows_kernel<<<blocks_for(me.row_end - me.row_begin), kNT, 0, s->stream>>>(
-                s->g->rowinfo.p, me.row_begin, me.row_end, P.need, others, npeers, cnt.p);
+        const uint32_t rb = s->dealt ? 0u : me.row_begin, re = s->dealt ? s->g->n : me.row_end;
+        if (re > rb)
+            sent_rows_kernel<<<blocks_for(re - rb), kNT, 0, s->stream>>>(
+                s->g->rowinfo.p, rb, re, P.row_owner, s->part_rank, P.need, others, npeers, cnt.p);
         PRGPU_LAUNCHED("sent_rows");
         unsigned long long c = 0;
         PRGPU_CUDA(cudaMemcpyAsync(&c, cnt.p, sizeof(c), cudaMemcpyDeviceToHost, s->stream));
@@ -1328,6 +1428,19 @@ void part_local_ranks_device(prgpu_session* s, double* out, uint64_t ld) {
                                                                                   out, ld);
         PRGPU_LAUNCHED("local_ranks_kernel");
     }
+}
+
+void part_owned_ranks_device(prgpu_session* s, double* out, uint64_t ld, int* dealt) {
+    DeviceGuard dg(s->g->device);
+    if (s->parts.empty()) fail(PRGPU_EINVAL, "not a partition session");
+    *dealt = s->dealt ? 1 : 0;
+    if (!s->dealt || !out) return;
+    if (ld < s->g->n) fail(PRGPU_EINVAL, "owned_ranks_device: ld smaller than vertex_count");
+    LaneMap map{};
+    for (int k = 0; k < s->K; ++k) map.user_of[k] = s->user_of[k];
+    owned_ranks_kernel<<<blocks_for((uint64_t)s->g->n * s->K), kNT, 0, s->cur()>>>(s->P, map, s->row_owner.p,
+                                                                                  s->part_rank, out, ld);
+    PRGPU_LAUNCHED("owned_ranks_kernel");
 }
 
 void part_local_ranks(prgpu_session* s, int user_lane, double* out) {

@@ -164,6 +164,12 @@ struct Params {
     unsigned int* arrive; // this rank's arrival counter (peers add to it)
     const uint8_t* need;  // [src] bit r: rank r gathers the source (null: every peer)
     uint32_t part_kp;     // lane stride of rank_partials (the run's widest mode)
+    // dealt partition (fused exchange): this rank runs the tasks
+    // task_list[list_begin, list_end) instead of [task_begin, task_end), and
+    // row_owner[row] is the rank that owns (pulls and publishes) each row
+    const uint32_t* task_list;
+    uint32_t list_begin, list_end;
+    const uint8_t* row_owner;
 };
 
 // ---- L2 residency control -------------------------------------------------------
@@ -968,7 +974,10 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     double* sv = s_dyn + (size_t)warp * PER_WARP;
     const uint32_t TW = P.G * kWarps;
     const uint32_t T1 = P.n_chunk, T2 = T1 + P.n_packed;
-    for (uint32_t t = P.task_begin + blockIdx.x * kWarps + warp; t < P.task_end; t += TW) {
+    const bool listed = P.task_list != nullptr;
+    const uint32_t i0 = listed ? P.list_begin : P.task_begin, i1 = listed ? P.list_end : P.task_end;
+    for (uint32_t i = i0 + blockIdx.x * kWarps + warp; i < i1; i += TW) {
+        const uint32_t t = listed ? __ldg(P.task_list + i) : i;
         if (t < T1) {
             if constexpr ((PATHS & 1) != 0)
                 if (!(P.skip_mask & 1)) w.chunk_task(t);

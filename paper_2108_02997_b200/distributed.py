@@ -103,6 +103,19 @@ class _Part:
     def launch(self):
         check(lib().prgpu_part_launch(self._s), "part launch")
 
+    def dealt(self) -> bool:
+        """Work dealt round-robin (fused partitions): rows are not one range."""
+        d = C.c_int()
+        check(lib().prgpu_part_owned_ranks_device(self._s, None, 0, C.byref(d)), "owned ranks")
+        return bool(d.value)
+
+    def owned_ranks_into(self, out) -> None:
+        """Add this rank's rows (every lane, engine row order) into the zeroed
+        device tensor out[K][n]."""
+        d = C.c_int()
+        check(lib().prgpu_part_owned_ranks_device(self._s, C.c_void_p(out.data_ptr()), out.shape[1],
+                                                  C.byref(d)), "owned ranks")
+
     def sent_bytes(self) -> int:
         """Bytes this rank stores into its peers per all-lanes iteration (fused)."""
         rows, rd = C.c_uint64(), C.c_uint32()
@@ -214,8 +227,14 @@ def _emulate_on(parts, alphas, max_iterations, want_ranks, g, fused=False, graph
     res = PartResult(iterations=np.zeros(K, np.int32), ranks=None, run_iterations=0,
                      loop_ms=start.elapsed_time(stop))
     if want_ranks:
-        chunks = [[p.local_ranks(k) for k in range(K)] for p in parts]
-        res.ranks = _assemble(g, chunks, K)
+        if parts[0].dealt():  # disjoint owned rows summed over the ranks
+            eng = torch.zeros((K, g.vertex_count), dtype=torch.float64, device=parts[0].contrib.device)
+            for p in parts:
+                p.owned_ranks_into(eng)
+            res.ranks = _to_caller_host(eng, g, parts[0].contrib.device)
+        else:
+            chunks = [[p.local_ranks(k) for k in range(K)] for p in parts]
+            res.ranks = _assemble(g, chunks, K)
     res.iterations[:] = _lane_iterations(parts[0])
     res.run_iterations = int(res.iterations.max())
     if fused:
@@ -382,6 +401,12 @@ def _gather_ranks(part: _Part, g: CsrGraph, K: int, world: int) -> np.ndarray:
     import torch
     import torch.distributed as dist
     dev = part.contrib.device
+    if part.dealt():  # rows dealt round-robin: disjoint rows summed across ranks
+        eng = torch.zeros((K, g.vertex_count), dtype=torch.float64, device=dev)
+        part.owned_ranks_into(eng)
+        if world > 1:
+            dist.all_reduce(eng, op=dist.ReduceOp.SUM)
+        return _to_caller_host(eng, g, dev)
     rows = [q.row_end - q.row_begin for q in part.parts]
     ld = max(rows)
     local = torch.empty((K, ld), dtype=torch.float64, device=dev)
@@ -392,6 +417,12 @@ def _gather_ranks(part: _Part, g: CsrGraph, K: int, world: int) -> np.ndarray:
     else:
         gathered = local.unsqueeze(0)
     eng = torch.cat([gathered[r, :, :rows[r]] for r in range(world)], dim=1)  # [K][n], engine rows
+    return _to_caller_host(eng, g, dev)
+
+
+def _to_caller_host(eng, g: CsrGraph, dev) -> np.ndarray:
+    """[K][n] engine-row ranks -> caller vertex order, on the host."""
+    import torch
     perm = torch.from_numpy(_permutation(g).astype(np.int64)).to(dev)
     out = torch.empty_like(eng)
     out[:, perm] = eng
