@@ -117,3 +117,18 @@ def test_nccl_world_of_one_peer_exchange(prl):
             assert np.max(np.abs(got.ranks[k] - want.results[k].ranks)) <= 1e-13
     finally:
         dist.destroy_process_group()
+
+
+def test_fused_eight_ranks_eleven_lanes(prl):
+    """The widest multi-GPU case: 8 ranks (the most one NVSwitch domain holds,
+    every bit of the needed-rank mask), 11 damping lanes walking through all
+    lane-width modes, dealt work; equal to the single-GPU run."""
+    from paper_2108_02997_b200 import distributed
+    g = prl.generate_rmat(16, 16, 0.57, 0.19, 0.19, 2108)
+    alphas = [0.50, 0.55, 0.60, 0.65, 0.70, 0.75, 0.80, 0.85, 0.90, 0.95, 1.00]
+    want = prl.pagerank_batched(g, alphas, 1e-8)
+    got = distributed.emulate(g, alphas, 8, 1e-8, fused=True)
+    assert got.sent_bytes > 0
+    for k in range(len(alphas)):
+        assert got.iterations[k] == want.results[k].iterations, k
+        assert np.max(np.abs(got.ranks[k] - want.results[k].ranks)) <= 1e-13, k
