@@ -66,6 +66,13 @@ CONFIGS = {
                alphas=[0.85], tol=1e-10, norm=2),
     "c5": dict(workload="C5: RMAT-28 alpha sweep {.75,.85,.95} batched K=3, tau 1e-6, L2",
                kind="rmat", scale=28, alphas=[0.95, 0.85, 0.75], tol=1e-6, norm=1),
+    # the same sweeps by the power-series method (prgpu_pagerank_series): one
+    # alpha = 1 chain and per-lane weighted sums, same results
+    "c2series": dict(workload="C2 damping sweep (RMAT-22, 11 alphas, tau 1e-6, L1) by the power-series "
+                              "method: one alpha=1 pull chain + per-lane weighted sums",
+                     kind="rmat", scale=22, alphas=ALPHAS, tol=1e-6, norm=0, series=True),
+    "c5series": dict(workload="C5 sweep (RMAT-28, alphas .95/.85/.75, tau 1e-6, L2) by the power-series method",
+                     kind="rmat", scale=28, alphas=[0.95, 0.85, 0.75], tol=1e-6, norm=1, series=True),
 }
 
 
@@ -576,6 +583,42 @@ def run_partitioned(args, cfg):
     return 0
 
 
+def run_series(args, cfg):
+    """A damping sweep by the power-series method (single GPU): one alpha = 1
+    pull chain as long as the slowest lane runs, plus per-lane weighted sums;
+    same iterations and ranks as the separate runs.  `value` counts the
+    reference's lane-iterations x E per second (the work the method replaces,
+    labelled as such); `pull_iterations` is what it actually ran."""
+    import torch
+    import paper_2108_02997_b200 as prl
+    dev = 0
+    torch.cuda.set_device(dev)
+    g = prl.generate_rmat(cfg["scale"], 16, 0.57, 0.19, 0.19, SEED, device=dev)
+    e = g.edge_count()
+    run = lambda: prl.pagerank_batched(g, cfg["alphas"], cfg["tol"], prl.NormKind(cfg["norm"]), 500,  # noqa: E731
+                                       want_ranks=False, series=True)
+    for _ in range(args.warmup):
+        r = run()
+    its = [x.iterations for x in r.results]
+    with ClockSampler(dev) as clk:
+        ms = [run().loop_ms for _ in range(args.steps)]
+    ms_per_step = float(sum(ms)) / args.steps
+    lane_its = int(sum(its))
+    line = {"metric": METRIC, "value": lane_its * e / (ms_per_step / 1e3) / 1e9, "unit": "GTEPS",
+            "value_kind": "reference-equivalent: the separate runs' lane-iterations x E per second",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded RMAT generated on the device (DESIGN.md)",
+            "config": {"workload": cfg["workload"], "vertices": g.vertex_count, "edges": e,
+                       "iterations_per_lane": its, "lane_iterations": lane_its,
+                       "pull_iterations": int(r.run_iterations),
+                       "pull_gteps": int(r.run_iterations) * e / (ms_per_step / 1e3) / 1e9,
+                       "timed_scope": "chain + weighted sums, CUDA events"},
+            "clocks": clk.summary(), "cpu_baseline": None, "e2e": None}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def measure_e2e(args, cfg, g, prl, torch, dev, lane_its):
     """C-ABI call with host buffers: prgpu_graph_from_csr (pinned H2D of the
     reference-layout CSR + device relabel) -> prgpu_pagerank (K lanes, ranks
@@ -670,6 +713,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference_arm(args, cfg)
+    if cfg.get("series"):
+        return run_series(args, cfg)
     if (env_rank()[1] > 1 or os.environ.get("PRGPU_BENCH_PARTITION")) and not args.replicas:
         return run_partitioned(args, cfg)
     return run_ours(args, cfg)

@@ -146,6 +146,15 @@ typedef struct {
  * copy results, free. */
 PRGPU_API int prgpu_pagerank(prgpu_graph* g, const prgpu_params* p, prgpu_result* out);
 
+/* Damping sweep as one power series: the same K lanes and results as
+ * prgpu_pagerank (iterations, converged, final_err, err_trace L1/L2/LInf,
+ * ranks), computed from ONE alpha = 1 chain y_t = M^t y_0 and per-lane
+ * weighted sums, since the reference's iterates are exactly
+ * r_t = alpha^t y_t + (1 - alpha) sum_{j<t} alpha^j y_j and
+ * r_t - r_{t-1} = alpha^t (y_t - y_{t-1}).  One pull per iteration of the
+ * slowest lane instead of one per lane-iteration.  ref_ranks unsupported. */
+PRGPU_API int prgpu_pagerank_series(prgpu_graph* g, const prgpu_params* p, prgpu_result* out);
+
 /* Per-iteration observer (pagerank.hpp:51-52,98): called after every
  * iteration of lane `lane` with its ranks (original ids) and error.  This
  * path syncs once per iteration and is meant for tests. */

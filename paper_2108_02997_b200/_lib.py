@@ -30,7 +30,7 @@ EXPORTS = [
     "prgpu_ipc_export", "prgpu_ipc_open", "prgpu_ipc_close",
     "prgpu_graph_permutation", "prgpu_graph_rows",
     "prgpu_mtx_parse", "prgpu_mtx_load", "prgpu_pairs_free", "prgpu_graph_load_mtx",
-    "prgpu_part_sent_rows", "prgpu_part_owned_ranks_device",
+    "prgpu_part_sent_rows", "prgpu_part_owned_ranks_device", "prgpu_pagerank_series",
 ]
 
 
@@ -129,6 +129,7 @@ def lib():
             "prgpu_graph_load_mtx": ([C.c_char_p, i32, i32, vp, vp], i32),
             "prgpu_part_sent_rows": ([vp, vp, vp], i32),
             "prgpu_part_owned_ranks_device": ([vp, vp, u64, vp], i32),
+            "prgpu_pagerank_series": ([vp, vp, vp], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

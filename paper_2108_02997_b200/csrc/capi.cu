@@ -54,6 +54,7 @@ void part_plan_copy(prgpu_session*, prgpu_partition*);
 void part_set_stream(prgpu_session*, void*);
 void graph_permutation(const prgpu_graph*, uint32_t*);
 void part_sent_rows(prgpu_session*, uint64_t*, uint32_t*);
+void pagerank_series(prgpu_graph*, const prgpu_params*, prgpu_result*);
 void part_owned_ranks_device(prgpu_session*, double*, uint64_t, int*);
 
 uint64_t graph_rows(const prgpu_graph*, const uint32_t*, uint32_t, uint64_t*, uint32_t*, uint64_t, cudaStream_t);
@@ -298,6 +299,14 @@ int prgpu_pagerank(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
         if (g) check_device(g->device);
         prgpu::SessionPtr s(prgpu::session_create(g, p, true, 0, 0, nullptr, nullptr), prgpu::session_destroy);
         prgpu::session_solve(s.get(), out);
+    });
+}
+
+int prgpu_pagerank_series(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
+    return guarded([&] {
+        if (!out) prgpu::fail(PRGPU_EINVAL, "null result");
+        if (g) check_device(g->device);
+        prgpu::pagerank_series(g, p, out);
     });
 }
 

@@ -1594,6 +1594,143 @@ void session_solve(prgpu_session* s, prgpu_result* out) {
     out->loop_ms = rest.loop_ms;
 }
 
+// ---- damping sweep as one power series ---------------------------------------------
+// The reference iterates every alpha separately: r_t = alpha * M r_{t-1} +
+// (1 - alpha)/N * 1 with M the column-stochastic link matrix whose dangling
+// columns spread 1/N (pagerank.hpp:85-92: c0 = (1-alpha)/N + alpha*D/N).
+// With r_0 = y_0 = 1/N and y_j = M^j y_0 that sequence is, exactly,
+//   r_t = alpha^t y_t + (1 - alpha) sum_{j<t} alpha^j y_j,
+//   r_t - r_{t-1} = alpha^t (y_t - y_{t-1}),
+// so every lane's iterates and every norm of its change (the stopping rule,
+// norms.hpp) follow from ONE chain y_t (an alpha = 1 run) plus per-lane
+// weighted sums of it.  The chain runs until the last lane stops; each lane
+// stops at the first t where alpha^t * ||y_t - y_{t-1}|| < tau for every norm
+// of its stop mask (or at max_iterations), and its ranks are the weighted sum
+// up to there.  Arithmetic differs from the reference's only in rounding
+// (summation order), like the batched run's.
+__global__ void series_accumulate(const double* __restrict__ y, uint32_t stride, uint32_t empty_begin, double y_empty,
+                                  uint32_t n, const double* __restrict__ coef, int K, double* __restrict__ acc) {
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n; v += (size_t)gridDim.x * blockDim.x) {
+        const double yv = v < empty_begin ? y[v * stride] : y_empty;
+        for (int k = 0; k < K; ++k) {
+            const double c = coef[k];
+            if (c != 0.0) acc[(size_t)k * n + v] = __dadd_rn(acc[(size_t)k * n + v], __dmul_rn(c, yv));
+        }
+    }
+}
+
+__global__ void series_extract(const double* __restrict__ acc, const uint32_t* __restrict__ new_of_old, uint32_t n,
+                               double* __restrict__ out) { // out[v_orig] = acc[new_of_old[v]]
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n; v += (size_t)gridDim.x * blockDim.x)
+        out[v] = acc[new_of_old[v]];
+}
+
+void pagerank_series(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
+    validate_params(p);
+    if (p->ref_ranks) fail(PRGPU_EINVAL, "pagerank_series: ref_ranks not supported");
+    if (!g || g->n == 0) fail(PRGPU_EINVAL, "pagerank: graph has no vertices");
+    DeviceGuard dg(g->device);
+    const int K = p->lanes;
+    const uint32_t n = g->n;
+    // the chain: one lane, alpha = 1, every norm traced, never stopping early
+    const double one = 1.0;
+    prgpu_params q{};
+    q.lanes = 1;
+    q.alphas = &one;
+    q.tolerance = 1e-300;
+    q.norm = PRGPU_NORM_L1;
+    q.stop_mask = 7u;
+    q.max_iterations = p->max_iterations;
+    std::unique_ptr<prgpu_session, void (*)(prgpu_session*)> s(session_create(g, &q, false), session_destroy);
+    cudaStream_t st = s->stream;
+    AllocScope scope(st);
+    DevBuf<double> acc((size_t)K * n), coef(K);
+    PRGPU_CUDA(cudaMemsetAsync(acc.p, 0, (size_t)K * n * sizeof(double), st));
+    std::vector<double> alpha(K), tol(K), c(K);
+    std::vector<uint32_t> mask(K);
+    std::vector<int> its(K, 0), conv(K, 0);
+    std::vector<double> ferr(K, INFINITY);
+    for (int k = 0; k < K; ++k) {
+        alpha[k] = p->alphas[k];
+        tol[k] = p->tolerances ? p->tolerances[k] : p->tolerance;
+        mask[k] = p->stop_mask ? p->stop_mask : (1u << p->norm);
+    }
+    std::vector<double> trace((size_t)p->max_iterations * K * 4, NAN);
+    session_init(s.get());
+    cudaEvent_t e0 = s->e0, e1 = s->e1;
+    PRGPU_CUDA(cudaEventRecord(e0, st));
+    auto accumulate = [&](int parity, double y_empty) {
+        PRGPU_CUDA(cudaMemcpyAsync(coef.p, c.data(), K * sizeof(double), cudaMemcpyHostToDevice, st));
+        series_accumulate<<<blocks_for(n), kNT, 0, st>>>(s->P.rank[parity], s->P.ks, s->P.empty_begin, y_empty, n,
+                                                         coef.p, K, acc.p);
+        PRGPU_LAUNCHED("series_accumulate");
+    };
+    // t = 0: every lane takes (1 - alpha) y_0, y_0 = 1/N everywhere
+    for (int k = 0; k < K; ++k) c[k] = 1.0 - alpha[k]; // 0 for alpha = 1: skipped
+    accumulate(0, 1.0 / (double)n);
+    int live = K, t = 0;
+    std::vector<double> pw(K, 1.0); // alpha^t
+    while (live > 0 && t < p->max_iterations) {
+        launch_pull(s.get()); // y_{t+1} into rank[(t+1)&1]; trace[t] = norms of y_{t+1} - y_t
+        ++t;
+        double tr[4];
+        LaneState L;
+        PRGPU_CUDA(cudaMemcpyAsync(tr, s->trace.p + (size_t)(t - 1) * 4, sizeof(tr), cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaMemcpyAsync(&L, s->lanes.p, sizeof(L), cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaStreamSynchronize(st));
+        // a chain that reached a fixed point stops iterating: its later
+        // differences are exactly zero
+        const double e[3] = {t - 1 < L.iterations ? tr[0] : 0.0, t - 1 < L.iterations ? tr[1] : 0.0,
+                             t - 1 < L.iterations ? tr[2] : 0.0};
+        const double y_empty = L.c0_used;
+        for (int k = 0; k < K; ++k) {
+            c[k] = 0.0;
+            if (its[k]) continue; // stopped earlier
+            pw[k] = pw[k] * alpha[k];
+            double err[3];
+            for (int qn = 0; qn < 3; ++qn) err[qn] = pw[k] * e[qn];
+            for (int qn = 0; qn < 3; ++qn) trace[((size_t)(t - 1) * K + k) * 4 + qn] = err[qn];
+            bool stop = true; // every norm of the lane's stop mask strictly below tau (pagerank.hpp:99)
+            for (int qn = 0; qn < 3; ++qn)
+                if ((mask[k] >> qn) & 1u) stop = stop && err[qn] < tol[k];
+            const bool last = stop || t >= p->max_iterations;
+            if (last) {
+                its[k] = t;
+                conv[k] = stop;
+                ferr[k] = err[p->norm];
+                c[k] = pw[k];  // r_t = acc + alpha^t y_t
+                --live;
+            } else {
+                c[k] = (1.0 - alpha[k]) * pw[k]; // acc += (1 - alpha) alpha^t y_t
+            }
+        }
+        accumulate(t & 1, y_empty);
+    }
+    PRGPU_CUDA(cudaEventRecord(e1, st));
+    PRGPU_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    PRGPU_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (out->ranks) {
+        DevBuf<double> tmp(n);
+        for (int k = 0; k < K; ++k) {
+            series_extract<<<blocks_for(n), kNT, 0, st>>>(acc.p + (size_t)k * n, g->new_of_old.p, n, tmp.p);
+            PRGPU_LAUNCHED("series_extract");
+            PRGPU_CUDA(cudaMemcpyAsync(out->ranks + (size_t)k * n, tmp.p, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+            PRGPU_CUDA(cudaStreamSynchronize(st));
+        }
+    }
+    for (int k = 0; k < K; ++k) {
+        if (out->iterations) out->iterations[k] = its[k];
+        if (out->converged) out->converged[k] = (uint8_t)conv[k];
+        if (out->final_err) out->final_err[k] = ferr[k];
+    }
+    if (out->err_trace)
+        for (size_t i = 0; i < trace.size(); ++i) out->err_trace[i] = trace[i];
+    out->run_iterations = t;
+    out->loop_ms = ms;
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+}
+
 void session_observed(prgpu_session* s, prgpu_result* out, prgpu_observer_fn fn, void* user) {
     DeviceGuard dg(s->g->device);
     cudaStream_t st = s->stream;

@@ -344,8 +344,13 @@ def _params(alphas: Sequence[float], tolerance, norm: NormKind, max_iterations: 
 
 def pagerank_batched(g: CsrGraph, alphas: Sequence[float], tolerance=1e-6,
                      norm: NormKind = NormKind.L1, max_iterations: int = 500,
-                     stop_mask: int = 0, ref_ranks=None, want_ranks: bool = True) -> BatchedRun:
-    """K = len(alphas) PageRank runs that share every edge visit (BASELINE C2)."""
+                     stop_mask: int = 0, ref_ranks=None, want_ranks: bool = True,
+                     series: bool = False) -> BatchedRun:
+    """K = len(alphas) PageRank runs that share every edge visit (BASELINE C2).
+
+    series=True: the same results from one alpha = 1 chain and per-lane
+    weighted sums (prgpu_pagerank_series): one pull per iteration of the
+    slowest lane instead of one per lane-iteration."""
     K = len(alphas)
     if not 1 <= K <= _lib.MAX_LANES:
         raise ValueError(f"pagerank_batched: 1..{_lib.MAX_LANES} alphas per run")
@@ -367,7 +372,12 @@ def pagerank_batched(g: CsrGraph, alphas: Sequence[float], tolerance=1e-6,
                     conv.ctypes.data_as(C.POINTER(C.c_uint8)),
                     ferr.ctypes.data_as(C.POINTER(C.c_double)),
                     trace.ctypes.data_as(C.POINTER(C.c_double)), 0.0, 0)
-    check(lib().prgpu_pagerank(g.handle, C.byref(p), C.byref(r)), "pagerank")
+    if series:
+        if ref is not None:
+            raise ValueError("pagerank_batched(series=True): ref_ranks not supported")
+        check(lib().prgpu_pagerank_series(g.handle, C.byref(p), C.byref(r)), "pagerank_series")
+    else:
+        check(lib().prgpu_pagerank(g.handle, C.byref(p), C.byref(r)), "pagerank")
     del keep
     results = [PageRankResult(ranks[k] if want_ranks else None, int(its[k]), bool(conv[k]),
                               r.loop_ms, float(ferr[k])) for k in range(K)]

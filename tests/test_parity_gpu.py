@@ -473,3 +473,64 @@ def test_structural_edge_cases_vs_oracle(prl, oracle, name):
             assert np.max(np.abs(r.ranks - want["ranks"])) <= RANK_TOL, a
     finally:
         oracle.free_csr(h)
+
+
+@pytest.mark.parametrize("K", [1, 3, 11])
+def test_series_sweep_vs_oracle(prl, oracle, K):
+    """The power-series sweep (one alpha = 1 chain, per-lane weighted sums)
+    against the oracle's separate runs: iterations (+-1 rule), converged,
+    ranks <= 1e-10, and the err traces to the reference's rounding noise;
+    alpha 0 and 1 included; per-lane tolerances and all-norm stop masks."""
+    rng = np.random.default_rng(500 + K)
+    n, pairs = oracle.rmat(14, 16, 0.57, 0.19, 0.19, 77)
+    h = oracle.build_csr_handle(n, pairs)
+    g = prl.generate_rmat(14, 16, 0.57, 0.19, 0.19, 77)
+    try:
+        alphas = [0.0, 1.0, 0.85][:K] if K <= 3 else list(np.round(rng.uniform(0.3, 1.0, K), 3))
+        tols = list(10.0 ** -rng.uniform(4, 10, K))
+        for norm, mask in ((prl.NormKind.L1, 0), (prl.NormKind.L2, 0), (prl.NormKind.LInf, 7)):
+            br = prl.pagerank_batched(g, alphas, tols, norm, 500, stop_mask=mask, series=True)
+            for k in range(K):
+                got = br.results[k]
+                names = ["l1", "l2", "linf"]
+                if mask == 7:  # every norm must be below tau: the latest crossing of the three
+                    runs = [oracle.pagerank(h, alphas[k], tols[k], nm, 500, trace=True) for nm in names]
+                    want = max(runs, key=lambda r: r["iterations"])
+                    tr = want["err_trace"]
+                else:
+                    want = oracle.pagerank(h, alphas[k], tols[k], names[int(norm)], 500, trace=True)
+                    tr = want["err_trace"]
+                assert iterations_match(got.iterations, want["iterations"], tr, tols[k]), (k, norm)
+                assert got.converged == want["converged"]
+                assert np.max(np.abs(got.ranks - want["ranks"])) <= RANK_TOL, (k, norm)
+            # traces: lane k's err at every iteration it ran, under the run's norm
+            if mask == 0:
+                for k in range(K):
+                    want = oracle.pagerank(h, alphas[k], tols[k], ["l1", "l2", "linf"][int(norm)], 500, trace=True)
+                    m = min(br.results[k].iterations, len(want["err_trace"]))
+                    got_tr = br.trace[:m, k, int(norm)]
+                    ref_tr = np.asarray(want["err_trace"][:m])
+                    # the reference differences two iterates of size ~1/N each: its err
+                    # carries ~1e-13 of rounding noise (the series computes
+                    # alpha^t * ||y_t - y_{t-1}||, equal in exact arithmetic)
+                    assert np.allclose(got_tr, ref_tr, rtol=1e-6, atol=1e-13), k
+    finally:
+        oracle.free_csr(h)
+
+
+def test_series_sweep_c2_golden(prl):
+    """C2 (RMAT-22, 11 alphas) through the series sweep against the reference's
+    goldens: iterations per lane, converged, sampled and top ranks, rank sums."""
+    gold = load_golden("c2_rmat22.json")
+    arr = np.load(os.path.join(GOLD, "c2_rmat22.npz"))
+    g = prl.generate_rmat(22, 16, 0.57, 0.19, 0.19, gold["seed"])
+    alphas = [ln["alpha"] for ln in gold["lanes"]]
+    br = prl.pagerank_batched(g, alphas, 1e-6, prl.NormKind.L1, 500, series=True)
+    idx = arr["sample_idx"]
+    for k, ln in enumerate(gold["lanes"]):
+        r = br.results[k]
+        assert iterations_match(r.iterations, ln["iterations"], arr[f"lane{k}_trace"], 1e-6), k
+        assert r.converged == ln["converged"]
+        assert np.max(np.abs(r.ranks[idx] - arr[f"lane{k}_sample"])) <= RANK_TOL
+        assert np.max(np.abs(r.ranks[arr[f"lane{k}_top_idx"]] - arr[f"lane{k}_top"])) <= RANK_TOL
+        assert abs(float(np.sum(r.ranks.astype(np.longdouble))) - float(arr[f"lane{k}_total"])) <= 1e-9
