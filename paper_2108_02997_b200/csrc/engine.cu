@@ -1608,10 +1608,40 @@ void session_solve(prgpu_session* s, prgpu_result* out) {
 // of its stop mask (or at max_iterations), and its ranks are the weighted sum
 // up to there.  Arithmetic differs from the reference's only in rounding
 // (summation order), like the batched run's.
-__global__ void series_accumulate(const double* __restrict__ y, uint32_t stride, uint32_t empty_begin, double y_empty,
-                                  uint32_t n, const double* __restrict__ coef, int K, double* __restrict__ acc) {
+// y_t kept (rows with in-edges, in blocks of kHistBlock vectors; rows without
+// hold the scalar c0 of step t) and every lane's ranks formed once at the
+// end, in engine row order (coalesced), all lanes per pass: acc_k = sum_j
+// w[k][j] * y_j in the order j = 0..T_k, w = (1-alpha) alpha^j for j < T_k and
+// alpha^T_k at j = T_k (0 beyond).  hist[j] points at y_j.
+constexpr int kHistBlock = 16;
+__global__ void series_combine(const double* const* __restrict__ hist, const double* __restrict__ yempty,
+                               const double* __restrict__ w /*[K][T+1]*/, int T, int K, uint32_t rows, uint32_t n,
+                               double* __restrict__ acc /*[K][n] engine rows*/) {
+    for (size_t r = blockIdx.x * (size_t)blockDim.x + threadIdx.x; r < n; r += (size_t)gridDim.x * blockDim.x) {
+        double a[PRGPU_MAX_LANES];
+#pragma unroll
+        for (int k = 0; k < PRGPU_MAX_LANES; ++k) a[k] = 0.0;
+        for (int j = 0; j <= T; ++j) {
+            const double y = r < rows ? hist[j][r] : yempty[j];
+#pragma unroll
+            for (int k = 0; k < PRGPU_MAX_LANES; ++k) {
+                if (k >= K) break;
+                const double c = w[(size_t)k * (T + 1) + j];
+                if (c != 0.0) a[k] = __dadd_rn(a[k], __dmul_rn(c, y));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PRGPU_MAX_LANES; ++k)
+            if (k < K) acc[(size_t)k * n + r] = a[k];
+    }
+}
+
+// large graphs (history would not stay in the memory pool): the weighted
+// sums accumulated as the chain runs, acc_k += coef_k * y_t (coef 0: lane done)
+__global__ void series_accumulate(const double* __restrict__ y, uint32_t rows, double y_empty, uint32_t n,
+                                  const double* __restrict__ coef, int K, double* __restrict__ acc) {
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n; v += (size_t)gridDim.x * blockDim.x) {
-        const double yv = v < empty_begin ? y[v * stride] : y_empty;
+        const double yv = v < rows ? y[v] : y_empty;
         for (int k = 0; k < K; ++k) {
             const double c = coef[k];
             if (c != 0.0) acc[(size_t)k * n + v] = __dadd_rn(acc[(size_t)k * n + v], __dmul_rn(c, yv));
@@ -1619,7 +1649,7 @@ __global__ void series_accumulate(const double* __restrict__ y, uint32_t stride,
     }
 }
 
-__global__ void series_extract(const double* __restrict__ acc, const uint32_t* __restrict__ new_of_old, uint32_t n,
+__global__ void series_permute(const double* __restrict__ acc, const uint32_t* __restrict__ new_of_old, uint32_t n,
                                double* __restrict__ out) { // out[v_orig] = acc[new_of_old[v]]
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n; v += (size_t)gridDim.x * blockDim.x)
         out[v] = acc[new_of_old[v]];
@@ -1644,9 +1674,8 @@ void pagerank_series(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
     std::unique_ptr<prgpu_session, void (*)(prgpu_session*)> s(session_create(g, &q, false), session_destroy);
     cudaStream_t st = s->stream;
     AllocScope scope(st);
-    DevBuf<double> acc((size_t)K * n), coef(K);
-    PRGPU_CUDA(cudaMemsetAsync(acc.p, 0, (size_t)K * n * sizeof(double), st));
-    std::vector<double> alpha(K), tol(K), c(K);
+    const uint32_t rows = s->P.empty_begin; // rows the chain stores (the rest hold c0)
+    std::vector<double> alpha(K), tol(K);
     std::vector<uint32_t> mask(K);
     std::vector<int> its(K, 0), conv(K, 0);
     std::vector<double> ferr(K, INFINITY);
@@ -1656,18 +1685,49 @@ void pagerank_series(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
         mask[k] = p->stop_mask ? p->stop_mask : (1u << p->norm);
     }
     std::vector<double> trace((size_t)p->max_iterations * K * 4, NAN);
+    std::vector<DevBuf<double>> blocks; // y_0, y_1, ... (rows with in-edges), kHistBlock per block
+    std::vector<const double*> hist;
+    std::vector<double> yempty;
+    const size_t hrows = std::max<uint32_t>(rows, 1);
+    // keep the chain (one combine at the end) while a block of it is small;
+    // on large graphs accumulate every lane as the chain runs instead
+    const char* sk = std::getenv("PRGPU_SERIES_KEEP"); // =0/1 forces the variant (tests)
+    const bool keep_chain = sk ? std::atoi(sk) != 0 : hrows * kHistBlock * sizeof(double) <= (2ull << 30);
+    DevBuf<double> acc((size_t)K * n), coef(K);
+    std::vector<double> c(K, 0.0), pw_run(K, 1.0);
+    std::vector<int> done_at(K, 0);
+    if (!keep_chain) PRGPU_CUDA(cudaMemsetAsync(acc.p, 0, (size_t)K * n * sizeof(double), st));
+    auto keep = [&](int parity, double y_empty) {
+        if (!keep_chain) return;
+        const size_t j = hist.size();
+        if (j % kHistBlock == 0) blocks.emplace_back(hrows * kHistBlock);
+        double* dst = blocks.back().p + (j % kHistBlock) * hrows;
+        if (rows)
+            PRGPU_CUDA(cudaMemcpyAsync(dst, s->P.rank[parity], (size_t)rows * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, st)); // K = 1: rank rows are contiguous
+        hist.push_back(dst);
+        yempty.push_back(y_empty);
+    };
+    // the in-loop variant: after step t every live lane adds (1 - alpha) alpha^t y_t,
+    // a lane stopping at t adds alpha^t y_t and is done
+    auto accumulate = [&](int parity, double y_empty, int step) {
+        if (keep_chain) return;
+        for (int k = 0; k < K; ++k) {
+            c[k] = 0.0;
+            if (done_at[k] && done_at[k] < step) continue;
+            c[k] = (done_at[k] == step && step > 0) ? pw_run[k] : (1.0 - alpha[k]) * pw_run[k];
+        }
+        PRGPU_CUDA(cudaMemcpyAsync(coef.p, c.data(), K * sizeof(double), cudaMemcpyHostToDevice, st));
+        series_accumulate<<<blocks_for(n), kNT, 0, st>>>(s->P.rank[parity], rows, y_empty, n, coef.p, K, acc.p);
+        PRGPU_LAUNCHED("series_accumulate");
+        PRGPU_CUDA(cudaStreamSynchronize(st)); // c is reused next step
+        for (int k = 0; k < K; ++k) pw_run[k] = pw_run[k] * alpha[k];
+    };
     session_init(s.get());
     cudaEvent_t e0 = s->e0, e1 = s->e1;
     PRGPU_CUDA(cudaEventRecord(e0, st));
-    auto accumulate = [&](int parity, double y_empty) {
-        PRGPU_CUDA(cudaMemcpyAsync(coef.p, c.data(), K * sizeof(double), cudaMemcpyHostToDevice, st));
-        series_accumulate<<<blocks_for(n), kNT, 0, st>>>(s->P.rank[parity], s->P.ks, s->P.empty_begin, y_empty, n,
-                                                         coef.p, K, acc.p);
-        PRGPU_LAUNCHED("series_accumulate");
-    };
-    // t = 0: every lane takes (1 - alpha) y_0, y_0 = 1/N everywhere
-    for (int k = 0; k < K; ++k) c[k] = 1.0 - alpha[k]; // 0 for alpha = 1: skipped
-    accumulate(0, 1.0 / (double)n);
+    keep(0, 1.0 / (double)n); // y_0 = 1/N everywhere
+    accumulate(0, 1.0 / (double)n, 0);
     int live = K, t = 0;
     std::vector<double> pw(K, 1.0); // alpha^t
     while (live > 0 && t < p->max_iterations) {
@@ -1677,14 +1737,14 @@ void pagerank_series(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
         LaneState L;
         PRGPU_CUDA(cudaMemcpyAsync(tr, s->trace.p + (size_t)(t - 1) * 4, sizeof(tr), cudaMemcpyDeviceToHost, st));
         PRGPU_CUDA(cudaMemcpyAsync(&L, s->lanes.p, sizeof(L), cudaMemcpyDeviceToHost, st));
+        keep(t & 1, 0.0);
         PRGPU_CUDA(cudaStreamSynchronize(st));
+        if (keep_chain) yempty.back() = L.c0_used;
         // a chain that reached a fixed point stops iterating: its later
         // differences are exactly zero
-        const double e[3] = {t - 1 < L.iterations ? tr[0] : 0.0, t - 1 < L.iterations ? tr[1] : 0.0,
-                             t - 1 < L.iterations ? tr[2] : 0.0};
-        const double y_empty = L.c0_used;
+        const bool ran = t - 1 < L.iterations;
+        const double e[3] = {ran ? tr[0] : 0.0, ran ? tr[1] : 0.0, ran ? tr[2] : 0.0};
         for (int k = 0; k < K; ++k) {
-            c[k] = 0.0;
             if (its[k]) continue; // stopped earlier
             pw[k] = pw[k] * alpha[k];
             double err[3];
@@ -1693,32 +1753,50 @@ void pagerank_series(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
             bool stop = true; // every norm of the lane's stop mask strictly below tau (pagerank.hpp:99)
             for (int qn = 0; qn < 3; ++qn)
                 if ((mask[k] >> qn) & 1u) stop = stop && err[qn] < tol[k];
-            const bool last = stop || t >= p->max_iterations;
-            if (last) {
+            if (stop || t >= p->max_iterations) {
                 its[k] = t;
                 conv[k] = stop;
                 ferr[k] = err[p->norm];
-                c[k] = pw[k];  // r_t = acc + alpha^t y_t
+                done_at[k] = t;
                 --live;
-            } else {
-                c[k] = (1.0 - alpha[k]) * pw[k]; // acc += (1 - alpha) alpha^t y_t
             }
         }
-        accumulate(t & 1, y_empty);
+        accumulate(t & 1, L.c0_used, t);
+    }
+    // weights: (1-alpha) alpha^j for j < T_k, alpha^T_k at T_k
+    const int T = t;
+    std::vector<double> w((size_t)K * (T + 1), 0.0);
+    for (int k = 0; k < K; ++k) {
+        double a = 1.0;
+        for (int j = 0; j <= its[k]; ++j) {
+            w[(size_t)k * (T + 1) + j] = j < its[k] ? (1.0 - alpha[k]) * a : a;
+            a = a * alpha[k];
+        }
+    }
+    DevBuf<double> res((size_t)K * n);
+    if (keep_chain) {
+        DevBuf<const double*> d_hist(hist.size());
+        DevBuf<double> d_w(w.size()), d_ye(yempty.size());
+        PRGPU_CUDA(cudaMemcpyAsync(d_hist.p, hist.data(), hist.size() * sizeof(const double*),
+                                   cudaMemcpyHostToDevice, st));
+        PRGPU_CUDA(cudaMemcpyAsync(d_w.p, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+        PRGPU_CUDA(cudaMemcpyAsync(d_ye.p, yempty.data(), yempty.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+        series_combine<<<blocks_for(n), kNT, 0, st>>>(d_hist.p, d_ye.p, d_w.p, T, K, rows, n, acc.p);
+        PRGPU_LAUNCHED("series_combine");
+        PRGPU_CUDA(cudaStreamSynchronize(st)); // host staging vectors
+    }
+    for (int k = 0; k < K; ++k) {
+        series_permute<<<blocks_for(n), kNT, 0, st>>>(acc.p + (size_t)k * n, g->new_of_old.p, n,
+                                                      res.p + (size_t)k * n);
+        PRGPU_LAUNCHED("series_permute");
     }
     PRGPU_CUDA(cudaEventRecord(e1, st));
     PRGPU_CUDA(cudaEventSynchronize(e1));
     float ms = 0;
     PRGPU_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    if (out->ranks) {
-        DevBuf<double> tmp(n);
-        for (int k = 0; k < K; ++k) {
-            series_extract<<<blocks_for(n), kNT, 0, st>>>(acc.p + (size_t)k * n, g->new_of_old.p, n, tmp.p);
-            PRGPU_LAUNCHED("series_extract");
-            PRGPU_CUDA(cudaMemcpyAsync(out->ranks + (size_t)k * n, tmp.p, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
-            PRGPU_CUDA(cudaStreamSynchronize(st));
-        }
-    }
+    if (out->ranks)
+        PRGPU_CUDA(cudaMemcpyAsync(out->ranks, res.p, (size_t)K * n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st)); // ptrs, w, yempty are host vectors
     for (int k = 0; k < K; ++k) {
         if (out->iterations) out->iterations[k] = its[k];
         if (out->converged) out->converged[k] = (uint8_t)conv[k];
