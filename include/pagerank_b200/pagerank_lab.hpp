@@ -346,7 +346,10 @@ struct BatchedRun {
 
 inline BatchedRun pagerank_batched(const CsrGraph& g, std::span<const double> alphas, double tolerance,
                                    NormKind norm, int max_iterations, std::uint32_t stop_mask = 0,
-                                   const RankVector* ref = nullptr, bool want_ranks = true) {
+                                   const RankVector* ref = nullptr, bool want_ranks = true,
+                                   bool series = false) {
+    // series: the same results from one alpha = 1 chain and per-lane weighted
+    // sums (prgpu_pagerank_series; no ref trace)
     const int K = static_cast<int>(alphas.size());
     if (K < 1 || K > PRGPU_MAX_LANES) throw std::invalid_argument("pagerank_batched: 1..16 alphas");
     prgpu_params p{};
@@ -367,7 +370,10 @@ inline BatchedRun pagerank_batched(const CsrGraph& g, std::span<const double> al
     out.iterations = its.data();
     out.converged = conv.data();
     out.err_trace = b.trace.data();
-    b200_detail::check(prgpu_pagerank(g.device_graph(), &p, &out), "pagerank");
+    if (series && ref) throw std::invalid_argument("pagerank_batched: series runs take no reference ranks");
+    b200_detail::check(series ? prgpu_pagerank_series(g.device_graph(), &p, &out)
+                              : prgpu_pagerank(g.device_graph(), &p, &out),
+                       "pagerank");
     b.run_iterations = out.run_iterations;
     b.loop_ms = out.loop_ms;
     for (int k = 0; k < K; ++k) {
