@@ -185,5 +185,5 @@ struct prgpu_graph {
     prgpu::DevBuf<uint32_t> old_of_new; // [n]
     uint32_t hub_end = 0, warp_end = 0, nonempty_end = 0;
     bool locality = false; // rows in the caller's order within classes (low-degree graphs)
-    uint32_t sort_end[3] = {0, 0, 0}; // rows with in-degree > 512, > 128, > 8
+    uint32_t sort_end[6] = {0, 0, 0, 0, 0, 0}; // rows with in-degree > 512, 256, 128, 64, 32, 8
 };

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <memory>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -247,8 +248,8 @@ __device__ __forceinline__ void block_add(T v, unsigned long long* dst) {
 // bins over rows sorted by in-degree descending: counts of rows above thresholds
 // counts[0..2]: rows with in-degree > 4096, > 32, > 0; counts[4..6]: > 512, > 128, > 8
 __global__ void bin_counts(const uint64_t* __restrict__ row_off, uint32_t n,
-                           unsigned long long* __restrict__ counts /*7*/) {
-    unsigned long long c0 = 0, c1 = 0, c2 = 0, c4 = 0, c5 = 0, c6 = 0;
+                           unsigned long long* __restrict__ counts /*9*/) {
+    unsigned long long c0 = 0, c1 = 0, c2 = 0, c4 = 0, c5 = 0, c6 = 0, c7 = 0, c8 = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t d = row_off[i + 1] - row_off[i];
@@ -256,8 +257,10 @@ __global__ void bin_counts(const uint64_t* __restrict__ row_off, uint32_t n,
         c1 += d > kWarpMinDegree;
         c2 += d > 0;
         c4 += d > 512;
-        c5 += d > 128;
-        c6 += d > 8;
+        c5 += d > 256;
+        c6 += d > 128;
+        c7 += d > 64;
+        c8 += d > 8;
     }
     block_add(c0, &counts[0]);
     block_add(c1, &counts[1]);
@@ -265,6 +268,8 @@ __global__ void bin_counts(const uint64_t* __restrict__ row_off, uint32_t n,
     block_add(c4, &counts[4]);
     block_add(c5, &counts[5]);
     block_add(c6, &counts[6]);
+    block_add(c7, &counts[7]);
+    block_add(c8, &counts[8]);
 }
 
 __global__ void count_zero(const uint32_t* __restrict__ v, uint32_t n,
@@ -632,13 +637,13 @@ std::unique_ptr<prgpu_graph> assemble_vertices(uint32_t n, const uint64_t* off, 
         PRGPU_LAUNCHED("src_maps");
     }
     ph.mark("row_off + source ids");
-    DevBuf<unsigned long long> counts(7);
-    PRGPU_CUDA(cudaMemsetAsync(counts.p, 0, 7 * sizeof(unsigned long long), st));
+    DevBuf<unsigned long long> counts(9);
+    PRGPU_CUDA(cudaMemsetAsync(counts.p, 0, 9 * sizeof(unsigned long long), st));
     bin_counts<<<grid_for(n), kThreads, 0, st>>>(g->row_off.p, n, counts.p);
     PRGPU_LAUNCHED("bin_counts");
     count_zero<<<grid_for(n), kThreads, 0, st>>>(out_deg, n, counts.p + 3);
     PRGPU_LAUNCHED("count_zero");
-    unsigned long long c[7];
+    unsigned long long c[9];
     uint64_t first_two[2];
     PRGPU_CUDA(cudaMemcpyAsync(c, counts.p, sizeof(c), cudaMemcpyDeviceToHost, st));
     PRGPU_CUDA(cudaMemcpyAsync(first_two, g->row_off.p, sizeof(first_two),
@@ -651,6 +656,9 @@ std::unique_ptr<prgpu_graph> assemble_vertices(uint32_t n, const uint64_t* off, 
     g->sort_end[0] = (uint32_t)c[4];
     g->sort_end[1] = (uint32_t)c[5];
     g->sort_end[2] = (uint32_t)c[6];
+    g->sort_end[3] = (uint32_t)c[7];
+    g->sort_end[4] = g->warp_end;
+    g->sort_end[5] = (uint32_t)c[8];
     g->max_in_degree = max_in;
     (void)first_two;
     return g;
@@ -682,25 +690,27 @@ struct EdgeFill {
         src_of_old.reset();
         const char* rs = std::getenv("PRGPU_ROW_SORT"); // =0: leave rows unsorted (tuning)
         if (rs && std::atoi(rs) == 0) return;
-        const uint32_t h = g->hub_end, m512 = g->sort_end[0], m128 = g->sort_end[1], m32 = g->warp_end,
-                       m8 = g->sort_end[2];
+        // one class per power-of-two length band, each sorted at its own
+        // width (a row is padded to the class's width, so bands halve the
+        // padding of the wide ones)
+        const uint32_t h = g->hub_end, m512 = g->sort_end[0];
         if (m512 > h) {
             sort_rows_block<<<m512 - h, 256, 0, st>>>(g->row_off.p, h, (int)bits_for(std::max(g->nsrc, 2u)),
                                                       g->col.p);
             PRGPU_LAUNCHED("sort_rows_block");
         }
-        if (m128 > m512) {
-            sort_rows_warp<16><<<(m128 - m512 + 7) / 8, 256, 0, st>>>(g->row_off.p, m512, m128, g->col.p);
-            PRGPU_LAUNCHED("sort_rows_warp16");
-        }
-        if (m32 > m128) {
-            sort_rows_warp<4><<<(m32 - m128 + 7) / 8, 256, 0, st>>>(g->row_off.p, m128, m32, g->col.p);
-            PRGPU_LAUNCHED("sort_rows_warp4");
-        }
-        if (m8 > m32) {
-            sort_rows_warp<1><<<(m8 - m32 + 7) / 8, 256, 0, st>>>(g->row_off.p, m32, m8, g->col.p);
-            PRGPU_LAUNCHED("sort_rows_warp1");
-        }
+        auto warp_sort = [&](auto items, int c) {
+            constexpr int I = decltype(items)::value;
+            const uint32_t r0 = g->sort_end[c], r1 = g->sort_end[c + 1];
+            if (r1 <= r0) return;
+            sort_rows_warp<I><<<(r1 - r0 + 7) / 8, 256, 0, st>>>(g->row_off.p, r0, r1, g->col.p);
+            PRGPU_LAUNCHED("sort_rows_warp");
+        };
+        warp_sort(std::integral_constant<int, 16>{}, 0); // 257..512
+        warp_sort(std::integral_constant<int, 8>{}, 1);  // 129..256
+        warp_sort(std::integral_constant<int, 4>{}, 2);  // 65..128
+        warp_sort(std::integral_constant<int, 2>{}, 3);  // 33..64
+        warp_sort(std::integral_constant<int, 1>{}, 4);  // 9..32
     }
 };
 
