@@ -1694,7 +1694,7 @@ void pagerank_series(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
     const char* sk = std::getenv("PRGPU_SERIES_KEEP"); // =0/1 forces the variant (tests)
     const bool keep_chain = sk ? std::atoi(sk) != 0 : hrows * kHistBlock * sizeof(double) <= (2ull << 30);
     DevBuf<double> acc((size_t)K * n), coef(K);
-    std::vector<double> c(K, 0.0), pw_run(K, 1.0);
+    std::vector<double> pw_run(K, 1.0);
     std::vector<int> done_at(K, 0);
     if (!keep_chain) PRGPU_CUDA(cudaMemsetAsync(acc.p, 0, (size_t)K * n * sizeof(double), st));
     auto keep = [&](int parity, double y_empty) {
@@ -1708,20 +1708,50 @@ void pagerank_series(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
         hist.push_back(dst);
         yempty.push_back(y_empty);
     };
+    // Host staging in pinned (mapped-pool) memory, so nothing below blocks
+    // the host: per parity the chain's trace row and LaneState after a step,
+    // and the in-loop variant's per-lane coefficients.
+    struct StepOut {
+        double tr[4];
+        LaneState L;
+    };
+    static_assert(sizeof(StepOut) <= kSlotInts * sizeof(int), "slot too small");
+    static_assert(2 * PRGPU_MAX_LANES * sizeof(double) <= kSlotInts * sizeof(int), "slot too small");
+    struct SlotHold {
+        int* p[3];
+        SlotHold() { for (auto& x : p) x = mapped_slot_get(); }
+        ~SlotHold() { for (auto* x : p) mapped_slot_put(x); }
+    } slots;
+    StepOut* hout[2] = {reinterpret_cast<StepOut*>(slots.p[0]), reinterpret_cast<StepOut*>(slots.p[1])};
+    double* hcoef = reinterpret_cast<double*>(slots.p[2]); // [2][PRGPU_MAX_LANES]
+    Event landed[2];
     // the in-loop variant: after step t every live lane adds (1 - alpha) alpha^t y_t,
-    // a lane stopping at t adds alpha^t y_t and is done
+    // a lane stopping at t adds alpha^t y_t and is done.  The coefficient row
+    // of parity t&1 is rewritten two steps later, after the host has waited
+    // for an event recorded behind this step's copy.
     auto accumulate = [&](int parity, double y_empty, int step) {
         if (keep_chain) return;
+        double* cr = hcoef + (step & 1) * PRGPU_MAX_LANES;
         for (int k = 0; k < K; ++k) {
-            c[k] = 0.0;
+            cr[k] = 0.0;
             if (done_at[k] && done_at[k] < step) continue;
-            c[k] = (done_at[k] == step && step > 0) ? pw_run[k] : (1.0 - alpha[k]) * pw_run[k];
+            cr[k] = (done_at[k] == step && step > 0) ? pw_run[k] : (1.0 - alpha[k]) * pw_run[k];
         }
-        PRGPU_CUDA(cudaMemcpyAsync(coef.p, c.data(), K * sizeof(double), cudaMemcpyHostToDevice, st));
+        PRGPU_CUDA(cudaMemcpyAsync(coef.p, cr, K * sizeof(double), cudaMemcpyHostToDevice, st));
         series_accumulate<<<blocks_for(n), kNT, 0, st>>>(s->P.rank[parity], rows, y_empty, n, coef.p, K, acc.p);
         PRGPU_LAUNCHED("series_accumulate");
-        PRGPU_CUDA(cudaStreamSynchronize(st)); // c is reused next step
         for (int k = 0; k < K; ++k) pw_run[k] = pw_run[k] * alpha[k];
+    };
+    // step t (1-based): y_t into rank[t&1], its trace row and lane state
+    // staged for the host, y_t kept; the host reads them after landed[t&1]
+    auto enqueue = [&](int step) {
+        launch_pull(s.get()); // y_t into rank[t&1]; trace[t-1] = norms of y_t - y_{t-1}
+        StepOut* o = hout[step & 1];
+        PRGPU_CUDA(cudaMemcpyAsync(o->tr, s->trace.p + (size_t)(step - 1) * 4, sizeof(o->tr),
+                                   cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaMemcpyAsync(&o->L, s->lanes.p, sizeof(LaneState), cudaMemcpyDeviceToHost, st));
+        keep(step & 1, 0.0);
+        PRGPU_CUDA(cudaEventRecord(landed[step & 1], st));
     };
     session_init(s.get());
     cudaEvent_t e0 = s->e0, e1 = s->e1;
@@ -1730,20 +1760,41 @@ void pagerank_series(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
     accumulate(0, 1.0 / (double)n, 0);
     int live = K, t = 0;
     std::vector<double> pw(K, 1.0); // alpha^t
+    // One step of lookahead: step t+1 is enqueued before the host decides on
+    // step t, so the GPU never waits for the host; it is skipped when the
+    // chain's last decay ratio predicts every live lane stops at t (a wrong
+    // guess costs one unused pull, or one host round trip).
+    double d1 = 0.0, d2 = 0.0; // the stop norm of the chain at t-1, t-2 (lane-independent)
+    bool queued = false;       // step t+1 already enqueued
+    if (p->max_iterations > 0) enqueue(1);
     while (live > 0 && t < p->max_iterations) {
-        launch_pull(s.get()); // y_{t+1} into rank[(t+1)&1]; trace[t] = norms of y_{t+1} - y_t
         ++t;
-        double tr[4];
-        LaneState L;
-        PRGPU_CUDA(cudaMemcpyAsync(tr, s->trace.p + (size_t)(t - 1) * 4, sizeof(tr), cudaMemcpyDeviceToHost, st));
-        PRGPU_CUDA(cudaMemcpyAsync(&L, s->lanes.p, sizeof(L), cudaMemcpyDeviceToHost, st));
-        keep(t & 1, 0.0);
-        PRGPU_CUDA(cudaStreamSynchronize(st));
-        if (keep_chain) yempty.back() = L.c0_used;
+        if (!queued && t > 1) enqueue(t);
+        queued = false;
+        if (t < p->max_iterations) {
+            bool predict_done = false;
+            if (d1 > 0.0 && d2 > 0.0) {
+                const double rho = d1 / d2;
+                predict_done = true;
+                for (int k = 0; k < K && predict_done; ++k)
+                    if (!its[k]) predict_done = pw[k] * alpha[k] * d1 * rho < 0.5 * tol[k];
+            }
+            if (!predict_done) {
+                enqueue(t + 1);
+                queued = true;
+            }
+        }
+        PRGPU_CUDA(cudaEventSynchronize(landed[t & 1]));
+        const StepOut& o = *hout[t & 1];
+        const double tr[4] = {o.tr[0], o.tr[1], o.tr[2], o.tr[3]};
+        const LaneState L = o.L;
+        if (keep_chain) yempty[t] = L.c0_used;
         // a chain that reached a fixed point stops iterating: its later
         // differences are exactly zero
         const bool ran = t - 1 < L.iterations;
         const double e[3] = {ran ? tr[0] : 0.0, ran ? tr[1] : 0.0, ran ? tr[2] : 0.0};
+        d2 = d1;
+        d1 = e[p->norm];
         for (int k = 0; k < K; ++k) {
             if (its[k]) continue; // stopped earlier
             pw[k] = pw[k] * alpha[k];

@@ -62,9 +62,13 @@ def main(tag):
         v, u = s[k].split()[:2]
         return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
     traffic = sum(to_bytes(s, "dram__bytes_read.sum") + to_bytes(s, "dram__bytes_write.sum") for s in kernels)
-    with open(os.path.join(PROF, "traffic.json"), "w") as f:
-        json.dump({"c2": traffic, "source": f"profiles/{tag}_ncu_pull.json (ncu --set full of the "
-                   "pull kernels of one C2 iteration, all 11 lanes active; summed)"}, f, indent=1)
+    tp = os.path.join(PROF, "traffic.json")
+    old = json.load(open(tp)) if os.path.exists(tp) else {}
+    old["c2"] = traffic  # the other configs' entries (ncu captures of their own) are kept
+    old["source"] = (f"profiles/{tag}_ncu_pull.json (ncu --set full of the pull kernels of one C2 "
+                     "iteration, all 11 lanes active; summed)")
+    with open(tp, "w") as f:
+        json.dump(old, f, indent=1)
     print("profiles written; pull traffic per launch", traffic / 1e9, "GB")
 
 

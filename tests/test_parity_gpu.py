@@ -475,12 +475,16 @@ def test_structural_edge_cases_vs_oracle(prl, oracle, name):
         oracle.free_csr(h)
 
 
-@pytest.mark.parametrize("K", [1, 3, 11])
-def test_series_sweep_vs_oracle(prl, oracle, K):
+@pytest.mark.parametrize("K,keep", [(1, None), (3, None), (11, None), (3, "0"), (11, "0")])
+def test_series_sweep_vs_oracle(prl, oracle, K, keep, monkeypatch):
     """The power-series sweep (one alpha = 1 chain, per-lane weighted sums)
     against the oracle's separate runs: iterations (+-1 rule), converged,
     ranks <= 1e-10, and the err traces to the reference's rounding noise;
-    alpha 0 and 1 included; per-lane tolerances and all-norm stop masks."""
+    alpha 0 and 1 included; per-lane tolerances and all-norm stop masks.
+    keep "0" forces the large-graph variant (sums accumulated as the chain
+    runs) that C5 uses."""
+    if keep is not None:
+        monkeypatch.setenv("PRGPU_SERIES_KEEP", keep)
     rng = np.random.default_rng(500 + K)
     n, pairs = oracle.rmat(14, 16, 0.57, 0.19, 0.19, 77)
     h = oracle.build_csr_handle(n, pairs)
@@ -516,6 +520,24 @@ def test_series_sweep_vs_oracle(prl, oracle, K):
                     assert np.allclose(got_tr, ref_tr, rtol=1e-6, atol=1e-13), k
     finally:
         oracle.free_csr(h)
+
+
+@pytest.mark.parametrize("keep", ["1", "0"])
+def test_series_capped_matches_batched(prl, keep, monkeypatch):
+    """Iteration caps 1, 2, 3 and 7 (the chain's lookahead must never run a
+    lane past its cap): the series and the batched run agree on iterations,
+    converged flags, final errors and ranks."""
+    monkeypatch.setenv("PRGPU_SERIES_KEEP", keep)
+    g = prl.generate_rmat(13, 8, 0.57, 0.19, 0.19, 31)
+    alphas = [0.3, 0.85, 0.99]
+    for cap in (1, 2, 3, 7):
+        a = prl.pagerank_batched(g, alphas, 1e-12, prl.NormKind.L2, cap)
+        b = prl.pagerank_batched(g, alphas, 1e-12, prl.NormKind.L2, cap, series=True)
+        for k in range(3):
+            assert b.results[k].iterations == a.results[k].iterations == cap, (cap, k)
+            assert b.results[k].converged == a.results[k].converged
+            assert abs(b.results[k].final_err - a.results[k].final_err) <= 1e-6 * a.results[k].final_err + 1e-16
+            assert np.max(np.abs(b.results[k].ranks - a.results[k].ranks)) <= 1e-13, (cap, k)
 
 
 def test_series_sweep_c2_golden(prl):
