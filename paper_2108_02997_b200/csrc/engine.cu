@@ -1717,11 +1717,15 @@ void pagerank_series(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
     };
     static_assert(sizeof(StepOut) <= kSlotInts * sizeof(int), "slot too small");
     static_assert(2 * PRGPU_MAX_LANES * sizeof(double) <= kSlotInts * sizeof(int), "slot too small");
-    struct SlotHold {
+    struct SlotHold { // returned only once no copy of `st` can still target them (error paths too)
         int* p[3];
-        SlotHold() { for (auto& x : p) x = mapped_slot_get(); }
-        ~SlotHold() { for (auto* x : p) mapped_slot_put(x); }
-    } slots;
+        cudaStream_t st;
+        explicit SlotHold(cudaStream_t s) : st(s) { for (auto& x : p) x = mapped_slot_get(); }
+        ~SlotHold() {
+            cudaStreamSynchronize(st);
+            for (auto* x : p) mapped_slot_put(x);
+        }
+    } slots(st);
     StepOut* hout[2] = {reinterpret_cast<StepOut*>(slots.p[0]), reinterpret_cast<StepOut*>(slots.p[1])};
     double* hcoef = reinterpret_cast<double*>(slots.p[2]); // [2][PRGPU_MAX_LANES]
     Event landed[2];
