@@ -476,6 +476,82 @@ __global__ void __launch_bounds__(256) sort_rows_block(const uint64_t* __restric
     }
 }
 
+// Per-slice variant for graph_from_csr: the caller's rows [v0, v1) (original
+// ids) whose edges have all been placed, one warp per row, each sorted at
+// the width of its length band; rows of 513..4096 are appended to `big` for
+// sort_rows_listed (one block per row).
+template <int ITEMS>
+__device__ __forceinline__ void warp_sort_row(uint32_t* col, uint64_t lo, int d, int lane, void* tmp) {
+    using Sort = cub::WarpMergeSort<uint32_t, ITEMS, 32>;
+    uint32_t k[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const int j = lane * ITEMS + i;
+        k[i] = j < d ? col[lo + j] : 0xFFFFFFFFu;
+    }
+    Sort(*reinterpret_cast<typename Sort::TempStorage*>(tmp)).Sort(k, [](uint32_t a, uint32_t b) { return a < b; });
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const int j = lane * ITEMS + i;
+        if (j < d) col[lo + j] = k[i];
+    }
+}
+
+__global__ void __launch_bounds__(256) sort_rows_orig(const uint64_t* __restrict__ row_off,
+                                                     const uint32_t* __restrict__ new_of_old, uint32_t v0,
+                                                     uint32_t v1, uint32_t* __restrict__ big,
+                                                     unsigned* __restrict__ nbig, uint32_t* __restrict__ col) {
+    constexpr size_t kTmp = sizeof(typename cub::WarpMergeSort<uint32_t, 16, 32>::TempStorage);
+    __shared__ __align__(16) unsigned char tmp[8][kTmp];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t v = v0 + (uint64_t)blockIdx.x * 8 + warp;
+    if (v >= v1) return;
+    const uint32_t r = new_of_old[v];
+    const uint64_t lo = row_off[r];
+    const int d = (int)(row_off[r + 1] - lo);
+    if (d <= 8 || d > (int)kHubMinDegree) return;
+    if (d > 512) {
+        if (lane == 0) big[atomicAdd(nbig, 1u)] = r;
+        return;
+    }
+    if (d <= 32) warp_sort_row<1>(col, lo, d, lane, tmp[warp]);
+    else if (d <= 64) warp_sort_row<2>(col, lo, d, lane, tmp[warp]);
+    else if (d <= 128) warp_sort_row<4>(col, lo, d, lane, tmp[warp]);
+    else if (d <= 256) warp_sort_row<8>(col, lo, d, lane, tmp[warp]);
+    else warp_sort_row<16>(col, lo, d, lane, tmp[warp]);
+}
+
+// the rows appended since the last call: big[done[0] .. nbig), block per row
+__global__ void __launch_bounds__(256) sort_rows_listed(const uint64_t* __restrict__ row_off,
+                                                       const uint32_t* __restrict__ big,
+                                                       const unsigned* __restrict__ nbig,
+                                                       const unsigned* __restrict__ done, int end_bit,
+                                                       uint32_t* __restrict__ col) {
+    using Sort = cub::BlockRadixSort<uint32_t, 256, 16>;
+    __shared__ typename Sort::TempStorage tmp;
+    const unsigned e = *nbig;
+    for (unsigned i = done[0] + blockIdx.x; i < e; i += gridDim.x) {
+        const uint32_t r = big[i];
+        const uint64_t lo = row_off[r];
+        const int d = (int)(row_off[r + 1] - lo);
+        uint32_t k[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int j = threadIdx.x * 16 + q;
+            k[q] = j < d ? col[lo + j] : 0xFFFFFFFFu;
+        }
+        Sort(tmp).Sort(k, 0, end_bit);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int j = threadIdx.x * 16 + q;
+            if (j < d) col[lo + j] = k[q];
+        }
+        __syncthreads(); // tmp is reused by the next row
+    }
+}
+
+__global__ void mark_listed(const unsigned* __restrict__ nbig, unsigned* __restrict__ done) { done[0] = *nbig; }
+
 // source ids in original-id order (tuning: PRGPU_SRC_ORDER=1)
 __global__ void src_maps_orig(const uint32_t* __restrict__ deg, const uint64_t* __restrict__ excl_old,
                               const uint32_t* __restrict__ old_of_new, uint32_t n,
@@ -686,8 +762,33 @@ struct EdgeFill {
                                                            g->row_off.p, src_of_old.p, g->col.p, cnt, bad);
         PRGPU_LAUNCHED("place_edges");
     }
+    // graph_from_csr: sort the caller's rows [v0, v1) (complete once their
+    // slice is placed) while later slices are still in flight
+    DevBuf<uint32_t> big;
+    DevBuf<unsigned> nbig; // [0] appended, [1] sorted
+    bool sliced = false;
+    void sort_slice(uint32_t v0, uint32_t v1, cudaStream_t st) {
+        if (!sliced) {
+            sliced = true;
+            big.alloc(std::max<uint32_t>(g->sort_end[0] - g->hub_end, 1));
+            nbig.alloc(2);
+            PRGPU_CUDA(cudaMemsetAsync(nbig.p, 0, 2 * sizeof(unsigned), st));
+        }
+        if (v1 <= v0) return;
+        sort_rows_orig<<<(v1 - v0 + 7) / 8, 256, 0, st>>>(g->row_off.p, g->new_of_old.p, v0, v1, big.p, nbig.p,
+                                                           g->col.p);
+        PRGPU_LAUNCHED("sort_rows_orig");
+        if (g->sort_end[0] > g->hub_end) {
+            sort_rows_listed<<<2 * 148, 256, 0, st>>>(g->row_off.p, big.p, nbig.p, nbig.p + 1,
+                                                      (int)bits_for(std::max(g->nsrc, 2u)), g->col.p);
+            PRGPU_LAUNCHED("sort_rows_listed");
+            mark_listed<<<1, 1, 0, st>>>(nbig.p, nbig.p + 1);
+            PRGPU_LAUNCHED("mark_listed");
+        }
+    }
     void finish(cudaStream_t st) {
         src_of_old.reset();
+        if (sliced) return; // sorted slice by slice
         const char* rs = std::getenv("PRGPU_ROW_SORT"); // =0: leave rows unsorted (tuning)
         if (rs && std::atoi(rs) == 0) return;
         // one class per power-of-two length band, each sorted at its own
@@ -815,10 +916,20 @@ std::unique_ptr<prgpu_graph> graph_from_csr(uint32_t n, const uint64_t* off, con
         ph.mark("vertex half");
         PRGPU_CUDA(cudaMemsetAsync(cnt.p, 0, (size_t)n * 4, st));
         EdgeFill fill(g.get(), st);
+        const char* rs = std::getenv("PRGPU_ROW_SORT"); // =0: leave rows unsorted (tuning)
+        const bool sort_rows = !(rs && std::atoi(rs) == 0);
+        uint32_t v_done = 0; // caller rows [0, v_done) complete and sorted
         for (size_t c = 0; c < landed.size(); ++c) {
             PRGPU_CUDA(cudaStreamWaitEvent(st, *landed[c], 0));
-            const uint64_t j = c * slice;
-            fill.place(d_off.p, d_nbr.p, j, std::min(e, j + slice), cnt.p, bad.p, st);
+            const uint64_t j = c * slice, je = std::min(e, j + slice);
+            fill.place(d_off.p, d_nbr.p, j, je, cnt.p, bad.p, st);
+            if (!sort_rows) continue;
+            // rows whose last edge is before je (the last slice: every row)
+            const uint32_t v_end = c + 1 == landed.size()
+                                       ? n
+                                       : (uint32_t)(std::upper_bound(off + 1, off + n + 1, je) - (off + 1));
+            fill.sort_slice(v_done, v_end, st);
+            v_done = v_end;
         }
         if (read_flag(bad, st))
             fail(PRGPU_EINVAL, "graph_from_csr: neighbours not ascending/unique/in range");
