@@ -213,7 +213,8 @@ inline CsrGraph download(prgpu_graph* g) {
 /// graph.hpp:204-234 on the device.  The returned host arrays are identical
 /// to the reference build_csr's; the device copy is kept for pagerank().
 inline CsrGraph build_csr(EdgeList el) {
-    if (el.vertex_count == 0) throw std::invalid_argument("build_csr: vertex_count must be >= 1");
+    // vertex_count 0 gives the empty graph, as graph.hpp:204-234 does;
+    // pagerank() then throws (pagerank.hpp:74)
     static_assert(sizeof(std::pair<std::uint32_t, std::uint32_t>) == 8);
     prgpu_graph* g = nullptr;
     b200_detail::check(prgpu_graph_build(el.vertex_count, reinterpret_cast<const std::uint32_t*>(el.edges.data()),
@@ -519,7 +520,9 @@ inline void sweep_graph(const SweepPlan& plan, const CsrGraph& g, const std::str
             BatchedRun b = pagerank_batched(g, chunk, tau_min, plan.norms.front(), plan.max_iterations,
                                             mask, &ref, false);
             total_ms += b.loop_ms;
-            if (rep > 0 && b.trace != first.trace)
+            // bitwise: NaN entries (prgpu.h err_trace) compare equal to themselves
+            if (rep > 0 && (b.trace.size() != first.trace.size() ||
+                            std::memcmp(b.trace.data(), first.trace.data(), b.trace.size() * sizeof(double)) != 0))
                 throw std::logic_error("sweep: iteration trace changed between repeats on " + label);
             if (rep == 0) first = std::move(b);
         }

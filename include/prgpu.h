@@ -137,7 +137,9 @@ typedef struct {
     int* iterations;          /* optional [K] */
     uint8_t* converged;       /* optional [K] */
     double* final_err;        /* optional [K]: err of the last iteration under `norm` */
-    double* err_trace;        /* optional [max_iterations][K][4]: L1, L2, LInf, L1-vs-ref */
+    double* err_trace;        /* optional [max_iterations][K][4]: L1, L2, LInf, L1-vs-ref;
+                                 entries no iteration wrote (after the lane stopped, or a
+                                 quantity the run does not track) are NaN in every entry point */
     double loop_ms;           /* out: device time of the iteration loop (CUDA events) */
     int run_iterations;       /* out: iterations executed (max over lanes) */
 } prgpu_result;
@@ -168,9 +170,12 @@ PRGPU_API int prgpu_pagerank_observed(prgpu_graph* g, const prgpu_params* p, prg
 PRGPU_API int prgpu_session_create(prgpu_graph* g, const prgpu_params* p, prgpu_session** out);
 PRGPU_API int prgpu_session_run(prgpu_session* s, double* loop_ms);
 PRGPU_API int prgpu_session_results(prgpu_session* s, prgpu_result* out);
-/* Device time of `launches` back-to-back launches of the pull kernel alone
- * (CUDA events on the session stream), in ms per launch. */
-PRGPU_API int prgpu_session_time_pull(prgpu_session* s, int launches, double* ms_per_launch);
+/* Device time of one iteration's pull kernels (the hub-chunk + packed pair,
+ * or the single kernel), in ms per iteration: a host-driven run of at most
+ * `launches` iterations that launches only the kernels of the lane mode the
+ * CUDA graph would run, one CUDA event pair per iteration on the session
+ * stream.  x iterations it is at most the graph loop's time. */
+PRGPU_API int prgpu_session_time_pull(prgpu_session* s, int launches, double* ms_per_iteration);
 PRGPU_API void prgpu_session_free(prgpu_session* s);
 
 /* ---- multi-GPU: 1D partition -----------------------------
@@ -232,7 +237,10 @@ PRGPU_API int prgpu_part_local_ranks_device(prgpu_session* s, double* dev_out, u
  * the rank's partials straight into every peer's buffers and signals arrival;
  * the finalize kernel waits for all ranks.  After prgpu_part_init (and a
  * host barrier across ranks), prgpu_part_launch enqueues the whole loop as
- * one CUDA graph; host-driven prgpu_part_step/_finalize also work. */
+ * one CUDA graph; host-driven prgpu_part_step/_finalize also work.
+ * The session must have been created by prgpu_part_create with BOTH
+ * ext_contrib and ext_rank_partials (the latter 2 x partial_doubles): those
+ * are the buffers the peers map; PRGPU_EINVAL otherwise. */
 PRGPU_API int prgpu_part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib,
                                    double* const* peer_partials, unsigned int* const* peer_arrive,
                                    unsigned int* arrive);

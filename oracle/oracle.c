@@ -10,6 +10,8 @@
 #include "oracle.h"
 
 #include <math.h>
+#include <pthread.h>
+#include <time.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -179,33 +181,62 @@ uint32_t orc_rmat_perm(uint32_t x32, uint32_t scale, uint64_t seed) {
     return (uint32_t)x;
 }
 
+void orc_rmat_gen_init(orc_rmat_gen* g, uint32_t scale, double a, double b, double c,
+                       uint64_t seed) {
+    g->scale = scale;
+    g->ta = orc_prob_threshold(a);
+    g->tab = orc_prob_threshold(a + b);
+    g->tabc = orc_prob_threshold(a + b + c);
+    g->kd = stream_key(seed, 1);
+    const uint64_t pk = stream_key(seed, 2); /* orc_rmat_perm's keys */
+    for (int r = 0; r < 3; ++r) g->pk[r] = orc_mix64(pk + (uint64_t)r);
+    g->mask = (scale >= 32) ? 0xFFFFFFFFull : ((1ull << scale) - 1);
+    g->hs = (scale + 1) / 2;
+}
+
+static uint32_t rmat_gen_perm(const orc_rmat_gen* g, uint32_t x32) {
+    uint64_t x = x32;
+    for (int r = 0; r < 3; ++r) {
+        const uint64_t k = g->pk[r];
+        x = (x * (k | 1ull)) & g->mask;
+        x = (x + (k >> 40)) & g->mask;
+        x ^= x >> g->hs;
+    }
+    return (uint32_t)x;
+}
+
+int orc_rmat_gen_edge(const orc_rmat_gen* g, uint64_t i, uint32_t* src_out, uint32_t* dst_out) {
+    uint32_t src = 0, dst = 0;
+    for (uint32_t l = 0; l < g->scale; ++l) {
+        const uint64_t x = orc_mix64(g->kd ^ ((i << 6) | l));
+        const uint32_t bit = 1u << (g->scale - 1 - l);
+        if (x < g->ta) {
+        } else if (x < g->tab) {
+            dst |= bit;
+        } else if (x < g->tabc) {
+            src |= bit;
+        } else {
+            src |= bit;
+            dst |= bit;
+        }
+    }
+    if (src == dst) return 0; /* self-loops removed (BASELINE.json configs) */
+    *src_out = rmat_gen_perm(g, src);
+    *dst_out = rmat_gen_perm(g, dst);
+    return 1;
+}
+
 orc_edges* orc_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
                     uint64_t seed) {
     const uint64_t n64 = 1ull << scale;
     orc_edges* el = orc_edges_new((uint32_t)(n64 > 0xFFFFFFFFull ? 0xFFFFFFFFull : n64));
     const uint64_t m = (uint64_t)edge_factor << scale;
     edges_reserve(el, m);
-    const uint64_t ta = orc_prob_threshold(a);
-    const uint64_t tab = orc_prob_threshold(a + b);
-    const uint64_t tabc = orc_prob_threshold(a + b + c);
-    const uint64_t kd = stream_key(seed, 1);
+    orc_rmat_gen g;
+    orc_rmat_gen_init(&g, scale, a, b, c, seed);
     for (uint64_t i = 0; i < m; ++i) {
-        uint32_t src = 0, dst = 0;
-        for (uint32_t l = 0; l < scale; ++l) {
-            const uint64_t x = orc_mix64(kd ^ ((i << 6) | l));
-            const uint32_t bit = 1u << (scale - 1 - l);
-            if (x < ta) {
-            } else if (x < tab) {
-                dst |= bit;
-            } else if (x < tabc) {
-                src |= bit;
-            } else {
-                src |= bit;
-                dst |= bit;
-            }
-        }
-        if (src == dst) continue; /* self-loops removed (BASELINE.json configs) */
-        edges_push(el, orc_rmat_perm(src, scale, seed), orc_rmat_perm(dst, scale, seed));
+        uint32_t src, dst;
+        if (orc_rmat_gen_edge(&g, i, &src, &dst)) edges_push(el, src, dst);
     }
     return el;
 }
@@ -406,6 +437,101 @@ int orc_pagerank(const orc_csr* g, double alpha, double tol, int norm, int max_i
     memcpy(ranks_out, prev, (size_t)n * sizeof(double)); /* :103 */
     *iterations = iteration;
     *converged = err < tol; /* :105 */
+    free(prev);
+    free(next);
+    return 0;
+}
+
+/* pagerank.hpp:70-108 with the v-loop (:89-93) split over `threads` host
+ * threads.  Each next[v] is computed by exactly the reference's expression in
+ * the same ascending-source order, and the dangling sum (:85-86) and the norm
+ * (:95) stay sequential on the calling thread, so ranks, errors and
+ * iteration counts are BIT-IDENTICAL to orc_pagerank (and to the reference:
+ * tests/test_oracle.py) — SPEC.md:194 allows parallelising the vertex loop.
+ * The CPU baseline for configs whose single-threaded iteration takes minutes
+ * (C4, C5).  elapsed_ms: the loop only, like PageRankResult::elapsed. */
+typedef struct {
+    const orc_csr* g;
+    const double* prev;
+    double* next;
+    double teleport, alpha;
+    uint32_t v0, v1;
+} mt_slice;
+
+static void* mt_pull(void* arg) {
+    const mt_slice* sl = (const mt_slice*)arg;
+    const orc_csr* g = sl->g;
+    for (uint32_t v = sl->v0; v < sl->v1; ++v) {
+        double acc = 0.0;
+        for (uint64_t j = g->in_offsets[v]; j < g->in_offsets[(size_t)v + 1]; ++j) {
+            const uint32_t u = g->in_neighbors[j];
+            acc += sl->prev[u] / g->out_degree[u];
+        }
+        sl->next[v] = sl->teleport + sl->alpha * acc;
+    }
+    return NULL;
+}
+
+int orc_pagerank_mt(const orc_csr* g, double alpha, double tol, int norm, int max_iter, int threads,
+                    double* ranks_out, int* iterations, int* converged, double* err_trace,
+                    double* elapsed_ms) {
+    if (config_invalid(alpha, tol, max_iter)) return 1;
+    const uint32_t n = g->n;
+    if (n == 0) return 1;
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    double* prev = (double*)malloc((size_t)n * sizeof(double));
+    double* next = (double*)malloc((size_t)n * sizeof(double));
+    if (!prev || !next) {
+        free(prev);
+        free(next);
+        return 2;
+    }
+    for (uint32_t v = 0; v < n; ++v) prev[v] = 1.0 / n;
+    for (uint32_t v = 0; v < n; ++v) next[v] = 0.0;
+    /* slices of roughly equal edge counts (plus one unit per row) */
+    uint32_t cut[257];
+    cut[0] = 0;
+    const double total = (double)g->in_offsets[n] + n;
+    for (int t = 1; t < threads; ++t) {
+        const double want = total * t / threads;
+        uint32_t lo = cut[t - 1], hi = n;
+        while (lo < hi) {
+            const uint32_t mid = lo + (hi - lo) / 2;
+            if ((double)g->in_offsets[mid] + mid < want) lo = mid + 1;
+            else hi = mid;
+        }
+        cut[t] = lo;
+    }
+    cut[threads] = n;
+    struct timespec t0, t1;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    int iteration = 0;
+    double err = INFINITY;
+    pthread_t tid[256];
+    mt_slice sl[256];
+    do {
+        double dangling_sum = 0.0;
+        for (uint32_t i = 0; i < g->ndangling; ++i) dangling_sum += prev[g->dangling[i]];
+        const double teleport = (1.0 - alpha) / n + alpha * dangling_sum / n;
+        for (int t = 0; t < threads; ++t) {
+            sl[t] = (mt_slice){g, prev, next, teleport, alpha, cut[t], cut[t + 1]};
+            if (t) pthread_create(&tid[t], NULL, mt_pull, &sl[t]);
+        }
+        mt_pull(&sl[0]);
+        for (int t = 1; t < threads; ++t) pthread_join(tid[t], NULL);
+        err = orc_error_norm(norm, next, prev, n);
+        if (err_trace) err_trace[iteration] = err;
+        ++iteration;
+        double* tt = prev;
+        prev = next;
+        next = tt;
+    } while (err >= tol && iteration < max_iter);
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    if (elapsed_ms) *elapsed_ms = (t1.tv_sec - t0.tv_sec) * 1e3 + (t1.tv_nsec - t0.tv_nsec) * 1e-6;
+    if (ranks_out) memcpy(ranks_out, prev, (size_t)n * sizeof(double));
+    *iterations = iteration;
+    *converged = err < tol;
     free(prev);
     free(next);
     return 0;

@@ -58,6 +58,15 @@ orc_edges* orc_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, do
                     uint64_t seed);
 orc_edges* orc_grid(uint32_t side, double p, double longrange_frac, uint64_t seed);
 uint32_t orc_rmat_perm(uint32_t x, uint32_t scale, uint64_t seed);
+/* edge i of the RMAT stream by itself (orc_rmat = every i in [0, ef << scale)):
+ * lets a builder regenerate the stream in parallel passes instead of holding it */
+typedef struct {
+    uint32_t scale, hs;
+    uint64_t ta, tab, tabc, kd, pk[3], mask;
+} orc_rmat_gen;
+void orc_rmat_gen_init(orc_rmat_gen* g, uint32_t scale, double a, double b, double c,
+                       uint64_t seed);
+int orc_rmat_gen_edge(const orc_rmat_gen* g, uint64_t i, uint32_t* src, uint32_t* dst); /* 0: self-loop */
 
 /* ---- reverse CSR: graph.hpp:47-60, build_csr graph.hpp:204-234 ---- */
 typedef struct {
@@ -83,6 +92,10 @@ int orc_pagerank(const orc_csr* g, double alpha, double tol, int norm, int max_i
 
 /* pagerank.hpp:85-93 for rows off/nbr (reference layout, ascending) from the
  * full prev vector; returns the teleport term.  out[nrows]. */
+/* the same run with the vertex loop on `threads` host threads: bit-identical */
+int orc_pagerank_mt(const orc_csr* g, double alpha, double tol, int norm, int max_iter, int threads,
+                    double* ranks_out, int* iterations, int* converged, double* err_trace,
+                    double* elapsed_ms);
 double orc_pagerank_step_rows(uint32_t n, const double* prev, const uint32_t* out_degree,
                               double alpha, uint32_t nrows, const uint64_t* off,
                               const uint32_t* nbr, double* out);

@@ -95,6 +95,9 @@ class Oracle:
         L.orc_error_norm.restype = C.c_double
         L.orc_pagerank.argtypes = [C.POINTER(_Csr), C.c_double, C.c_double, C.c_int, C.c_int,
                                    _f64p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_void_p]
+        L.orc_pagerank_mt.argtypes = [C.POINTER(_Csr), C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
+                                      C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_void_p,
+                                      C.POINTER(C.c_double)]
         L.orc_dense_pagerank.argtypes = [C.c_uint32, _u32p, C.c_uint64, C.c_double, C.c_double,
                                          C.c_int, C.c_int, _f64p, C.POINTER(C.c_int),
                                          C.POINTER(C.c_int)]
@@ -185,6 +188,49 @@ class Oracle:
             out["err_trace"] = tr[: it.value]
         return out
 
+    def csr_view(self, n, in_offsets, in_neighbors, out_degree):
+        """An orc_csr over caller-owned reference-layout arrays (no copy; the
+        dangling list = out_degree == 0 ascending, graph.hpp:230-231).  The
+        returned object keeps the arrays alive; pass it where a handle goes."""
+        off = np.ascontiguousarray(in_offsets, np.uint64)
+        nbr = np.ascontiguousarray(in_neighbors, np.uint32)
+        deg = np.ascontiguousarray(out_degree, np.uint32)
+        dang = np.flatnonzero(deg == 0).astype(np.uint32)
+        keep = (off, nbr if nbr.size else np.zeros(1, np.uint32), deg, dang if dang.size else
+                np.zeros(1, np.uint32))
+        c = _Csr(n, int(off[-1]), keep[0].ctypes.data_as(C.POINTER(C.c_uint64)),
+                 keep[1].ctypes.data_as(C.POINTER(C.c_uint32)), keep[2].ctypes.data_as(C.POINTER(C.c_uint32)),
+                 keep[3].ctypes.data_as(C.POINTER(C.c_uint32)), int(dang.size))
+
+        class _View:
+            pass
+        v = _View()
+        v.keep, v.csr = keep, c
+        v.ptr = C.pointer(c)
+        return v
+
+    def pagerank_mt(self, view, alpha=0.85, tol=1e-6, norm="l1", max_iter=500, threads=None,
+                    trace=False, want_ranks=True):
+        """orc_pagerank_mt: the vertex loop on `threads` host threads, results
+        bit-identical to the reference; elapsed_ms = loop time."""
+        h = view.ptr if hasattr(view, "ptr") else view
+        n = h.contents.n
+        threads = threads or (os.cpu_count() or 1)
+        ranks = np.zeros(max(n, 1), np.float64) if want_ranks else None
+        it, conv, ms = C.c_int(), C.c_int(), C.c_double()
+        tr = np.zeros(max_iter, np.float64) if trace else None
+        st = self.L.orc_pagerank_mt(h, alpha, tol, _norm_id(norm), max_iter, threads,
+                                    ranks.ctypes.data if want_ranks else None, C.byref(it), C.byref(conv),
+                                    tr.ctypes.data if trace else None, C.byref(ms))
+        if st != 0:
+            raise ValueError("oracle pagerank_mt: invalid argument or out of memory")
+        out = dict(iterations=it.value, converged=bool(conv.value), elapsed_ms=ms.value, threads=threads)
+        if want_ranks:
+            out["ranks"] = ranks[:n]
+        if trace:
+            out["err_trace"] = tr[: it.value]
+        return out
+
     def step_rows(self, prev, out_degree, alpha, off, nbr):
         """One reference iteration (pagerank.hpp:85-93) for the rows whose
         in-neighbours are off/nbr, from the full previous vector.  Returns
@@ -239,6 +285,8 @@ class Ref:
         L.ref_csr_free.argtypes = [C.c_void_p]
         L.ref_csr_from_arrays.argtypes = [C.c_uint32, _u64p, _u32p, _u32p]
         L.ref_csr_from_arrays.restype = C.c_void_p
+        L.ref_csr_rmat.argtypes = [C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint64]
+        L.ref_csr_rmat.restype = C.c_void_p
         L.ref_csr_vertex_count.argtypes = [C.c_void_p]
         L.ref_csr_vertex_count.restype = C.c_uint32
         L.ref_csr_edge_count.argtypes = [C.c_void_p]
@@ -346,6 +394,11 @@ class Ref:
             nbr = np.zeros(1, np.uint32)
         return self.L.ref_csr_from_arrays(n, np.ascontiguousarray(in_offsets, np.uint64), nbr,
                                           np.ascontiguousarray(out_degree, np.uint32))
+
+    def csr_rmat(self, scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1):
+        """The RMAT benchmark graph as a reference CsrGraph, built in place on
+        all host threads (csr_inplace.hpp; the same arrays as build_csr)."""
+        return self.L.ref_csr_rmat(scale, edge_factor, a, b, c, seed)
 
     def csr_arrays(self, h) -> CsrArrays:
         n = self.L.ref_csr_vertex_count(h)

@@ -192,3 +192,19 @@ void* ref_load_mtx(const char* path, char* msg, int cap) {
     }
 }
 }
+
+#include "csr_inplace.hpp"
+
+extern "C" {
+// The RMAT benchmark graph as a reference CsrGraph, built in place on all
+// host threads by csr_inplace.hpp (the same arrays as build_csr,
+// graph.hpp:204-234, which at scale 28 would need ~55 GB and ~16 min on one
+// thread).  The reference arm of bench.py then times the reference's own
+// pagerank() on it.
+void* ref_csr_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c, uint64_t seed) {
+    auto* g = new CsrGraph();
+    uint64_t raw = 0;
+    csr_inplace::build_rmat(*g, scale, edge_factor, a, b, c, seed, &raw);
+    return g;
+}
+}

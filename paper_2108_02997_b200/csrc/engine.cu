@@ -79,6 +79,13 @@ __global__ void extract_ranks(Params P, const uint32_t* __restrict__ new_of_old,
     }
 }
 
+// trace entries no iteration writes (a lane after it stopped, norms an
+// instance does not track) read NaN in every entry point (prgpu.h err_trace)
+__global__ void fill_f64(double* __restrict__ p, size_t n, double v) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
 __global__ void strided_copy(const double* __restrict__ src, uint32_t stride, double* __restrict__ dst,
                              uint32_t rows) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < rows; i += (size_t)gridDim.x * blockDim.x)
@@ -406,6 +413,7 @@ struct prgpu_session {
     DevBuf<unsigned int> need; // fused exchange: [ceil(nsrc/4)] one byte per source, bit q = rank q gathers it
     cudaStream_t ext_stream = nullptr;
     double* ext_contrib_base = nullptr; // caller-provided contribution buffer (partition sessions)
+    double* ext_rank_partials = nullptr; // caller-provided rank partials (2 parities for the fused exchange)
     cudaStream_t cur() const { return ext_stream ? ext_stream : (cudaStream_t)stream; }
     // lanes that stopped, written by the device (host-mapped), for copying
     // results out while the other lanes still iterate (session_solve)
@@ -695,13 +703,18 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     s->rank.alloc(2 * (size_t)KS * n);
     double* cbase = ext_contrib;
     s->ext_contrib_base = ext_contrib;
+    s->ext_rank_partials = ext_rp;
     if (!cbase) { // partitions: room for the narrow lane modes' buffers too (part_contrib_doubles)
         s->contrib.alloc(nranks >= 1 ? part_contrib_doubles(g, s->cfg, K) : 2 * nsrc * KS);
         cbase = s->contrib.p;
     }
     PRGPU_CUDA(cudaMemsetAsync(cbase, 0, 2 * nsrc * KS * sizeof(double), st));
     s->trace.alloc((size_t)s->max_iter * K * 4);
-    PRGPU_CUDA(cudaMemsetAsync(s->trace.p, 0, (size_t)s->max_iter * K * 4 * sizeof(double), st));
+    {
+        const size_t nt = (size_t)s->max_iter * K * 4;
+        fill_f64<<<(unsigned)std::min<size_t>((nt + 255) / 256, 1024), 256, 0, st>>>(s->trace.p, nt, NAN);
+        PRGPU_CUDA(cudaGetLastError());
+    }
     s->lanes.alloc(K);
     s->gs.alloc(1);
 
@@ -790,7 +803,8 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         P.nranks = (uint32_t)nranks;
         double* rp = ext_rp;
         if (!rp) {
-            s->rank_partials.alloc((size_t)nranks * kNQ * KP);
+            // both parity blocks, so the layout is the fused exchange's too
+            s->rank_partials.alloc(2 * (size_t)nranks * kNQ * KP);
             rp = s->rank_partials.p;
         }
         P.rank_partials = rp;
@@ -1147,7 +1161,10 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
     if (npeers < 0 || npeers > kMaxPeers || npeers != s->nranks - 1)
         fail(PRGPU_EINVAL, "set_peers: npeers must be nranks - 1 (<= " + std::to_string(kMaxPeers) + ")");
     if (!arrive) fail(PRGPU_EINVAL, "set_peers: null arrival counter");
-    if (!s->ext_contrib_base) fail(PRGPU_EINVAL, "set_peers: the session needs caller-provided buffers");
+    if (!s->ext_contrib_base || !s->ext_rank_partials)
+        fail(PRGPU_EINVAL, "set_peers: the session needs caller-provided contribution and rank-partial buffers "
+                           "(prgpu_part_session_create ext_contrib / ext_rank_partials, sized by "
+                           "prgpu_part_buffer_sizes)");
     // the fused exchange runs the lane-width modes (their buffers live in the
     // same caller allocation, mapped by the peers at the same offsets);
     // PRGPU_PART_MODES=0 keeps the widest mode only (tuning)
@@ -1692,7 +1709,14 @@ void pagerank_series(prgpu_graph* g, const prgpu_params* p, prgpu_result* out) {
     // keep the chain (one combine at the end) while a block of it is small;
     // on large graphs accumulate every lane as the chain runs instead
     const char* sk = std::getenv("PRGPU_SERIES_KEEP"); // =0/1 forces the variant (tests)
-    const bool keep_chain = sk ? std::atoi(sk) != 0 : hrows * kHistBlock * sizeof(double) <= (2ull << 30);
+    // the whole chain may reach ceil((max_iterations + 2) / kHistBlock) blocks:
+    // keep it only if that many fit in half the free device memory now
+    size_t free_b = 0, total_b = 0;
+    PRGPU_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t block_b = hrows * kHistBlock * sizeof(double);
+    const size_t max_blocks = ((size_t)p->max_iterations + 2 + kHistBlock - 1) / kHistBlock;
+    const bool keep_chain = sk ? std::atoi(sk) != 0
+                               : block_b <= (2ull << 30) && max_blocks * block_b <= free_b / 2;
     DevBuf<double> acc((size_t)K * n), coef(K);
     std::vector<double> pw_run(K, 1.0);
     std::vector<int> done_at(K, 0);
@@ -1900,26 +1924,45 @@ void session_observed(prgpu_session* s, prgpu_result* out, prgpu_observer_fn fn,
 }
 
 double session_time_pull(prgpu_session* s, int launches) {
-    // host-loop run with an event pair per launch; mean device time per launch
+    // Device time of one iteration's pull kernels, as the CUDA graph runs
+    // them: a host-driven pass to convergence (at most `launches`
+    // iterations) that launches, per iteration, only the kernels of the lane
+    // mode the finalizer armed (plus its repack on a mode change) — the
+    // graph's IF nodes skip the others — between ONE event pair.  Mean over
+    // the iterations; x iterations it is below the graph loop's time (which
+    // adds the conditional-node overhead).
     DeviceGuard dg(s->g->device);
     session_init(s);
-    cudaStream_t st = s->stream;
+    cudaStream_t st = s->cur();
+    const uint32_t nsrc = std::max<uint32_t>(s->g->nsrc, 1);
     std::vector<cudaEvent_t> ev(2 * (size_t)launches);
     for (auto& e : ev) PRGPU_CUDA(cudaEventCreate(&e));
     int done = 0;
-    for (; done < launches; ++done) {
+    GlobalState gsh;
+    PRGPU_CUDA(cudaMemcpyAsync(&gsh, s->gs.p, sizeof(gsh), cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    for (; done < launches && gsh.any_active; ++done) {
         PRGPU_CUDA(cudaEventRecord(ev[2 * done], st));
-        launch_pull(s);
+        for (const auto& l : s->launches) {
+            if (l.P.mode_id != gsh.mode) continue;
+            if (l.repack && gsh.layout == gsh.mode) continue;
+            Params P = l.P;
+            P.use_cond = 0;
+            if (l.repack) repack_kernel<<<P.G, kNT, 0, st>>>(P, nsrc);
+            else l.fn<<<P.G, kNT, l.smem, st>>>(P);
+            PRGPU_LAUNCHED("pull_kernel");
+        }
         PRGPU_CUDA(cudaEventRecord(ev[2 * done + 1], st));
-        if (!read_any_active(s)) { ++done; break; }
+        PRGPU_CUDA(cudaMemcpyAsync(&gsh, s->gs.p, sizeof(gsh), cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaStreamSynchronize(st));
     }
     double total = 0;
-    const bool log = std::getenv("PRGPU_TIMING_LOG") != nullptr; // per-launch times (tuning)
+    const bool log = std::getenv("PRGPU_TIMING_LOG") != nullptr; // per-iteration times (tuning)
     for (int i = 0; i < done; ++i) {
         float ms = 0;
         PRGPU_CUDA(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]));
         total += ms;
-        if (log) std::fprintf(stderr, "launch %d: %.4f ms\n", i + 1, ms);
+        if (log) std::fprintf(stderr, "iteration %d: %.4f ms\n", i + 1, ms);
     }
     for (auto& e : ev) cudaEventDestroy(e);
     return done ? total / done : 0.0;

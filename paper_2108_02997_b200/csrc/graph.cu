@@ -318,12 +318,15 @@ __global__ void check_offsets(const uint64_t* __restrict__ off, uint32_t n, uint
 // Engine CSR fill for edges [jb, je) of the original CSR: edge j of original
 // row o lands at row_off[new(o)] + (j - off[o]) as the engine source id of
 // its in-neighbour (rows keep the caller's neighbour order until sorted).
-// With `bad`, also validates: in-neighbours in range and strictly ascending
-// per row, and counts out-degrees into out_cnt (graph_from_csr).
+// With `bad` (graph_from_csr), also validates what pagerank() needs of a
+// hand-filled CsrGraph: in-neighbours in range (graph.hpp:56-59) and with a
+// nonzero caller out-degree (pagerank.hpp:91 divides by it).  Like the
+// reference, rows may hold duplicates and any order, and out_degree is used
+// as given (it need not equal the in-neighbour histogram).
 __global__ void place_edges(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr, uint32_t n,
                             uint64_t jb, uint64_t je, const uint32_t* __restrict__ new_of_old,
                             const uint64_t* __restrict__ row_off, const uint32_t* __restrict__ src_of_old,
-                            uint32_t* __restrict__ col, uint32_t* __restrict__ out_cnt, int* bad) {
+                            uint32_t* __restrict__ col, const uint32_t* __restrict__ out_deg, int* bad) {
     const uint64_t j0 = jb + (uint64_t)blockIdx.x * kEdgeChunk, j1 = min(j0 + kEdgeChunk, je);
     uint32_t r0, r1;
     chunk_rows(off, n, j0, j1, r0, r1);
@@ -332,8 +335,7 @@ __global__ void place_edges(const uint64_t* __restrict__ off, const uint32_t* __
         const uint32_t o = last_row_le(off, r0, r1, j);
         if (bad) {
             if (u >= n) { *bad = 1; continue; }
-            atomicAdd(out_cnt + u, 1u);
-            if (j > off[o] && nbr[j - 1] >= u) *bad = 1;
+            if (out_deg[u] == 0) { *bad = 2; continue; }
         }
         col[row_off[new_of_old[o]] + (j - off[o])] = src_of_old[u];
     }
@@ -350,13 +352,6 @@ __global__ void src_of_old_kernel(const uint2* __restrict__ rowinfo, const uint3
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
          v += (uint64_t)gridDim.x * blockDim.x)
         out[v] = rowinfo[new_of_old[v]].y;
-}
-
-__global__ void compare_u32(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
-                            uint32_t n, int* bad) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        if (a[i] != b[i]) *bad = 1;
 }
 
 // engine CSR -> original-id keys (for download)
@@ -754,12 +749,12 @@ struct EdgeFill {
                                                                src_of_old.p);
         PRGPU_LAUNCHED("src_of_old");
     }
-    void place(const uint64_t* off, const uint32_t* nbr, uint64_t jb, uint64_t je, uint32_t* cnt, int* bad,
+    void place(const uint64_t* off, const uint32_t* nbr, uint64_t jb, uint64_t je, const uint32_t* deg, int* bad,
                cudaStream_t st) {
         if (je <= jb) return;
         const uint64_t blocks = (je - jb + kEdgeChunk - 1) / kEdgeChunk;
         place_edges<<<(unsigned)blocks, kThreads, 0, st>>>(off, nbr, g->n, jb, je, g->new_of_old.p,
-                                                           g->row_off.p, src_of_old.p, g->col.p, cnt, bad);
+                                                           g->row_off.p, src_of_old.p, g->col.p, deg, bad);
         PRGPU_LAUNCHED("place_edges");
     }
     // graph_from_csr: sort the caller's rows [v0, v1) (complete once their
@@ -847,9 +842,20 @@ std::unique_ptr<prgpu_graph> assemble(DevBuf<uint64_t>&& keys_in, uint64_t u, ui
 
 } // namespace
 
+// vertex_count 0: no device arrays; every solve entry point rejects it
+std::unique_ptr<prgpu_graph> empty_graph(int device) {
+    auto g = std::make_unique<prgpu_graph>();
+    g->device = device;
+    g->lg = 1;
+    return g;
+}
+
 std::unique_ptr<prgpu_graph> graph_build_device(uint32_t n, const uint32_t* d_pairs, uint64_t m,
                                                 int device, cudaStream_t st) {
-    if (n == 0) fail(PRGPU_EINVAL, "build_csr: vertex_count must be >= 1");
+    if (n == 0) { // graph.hpp:204-234 returns an empty graph; pagerank() then throws (pagerank.hpp:74)
+        if (m) fail(PRGPU_EINVAL, "build_csr: edge endpoint >= vertex_count");
+        return empty_graph(device);
+    }
     const uint32_t lg = bits_for(n);
     DevBuf<uint64_t> keys(std::max<uint64_t>(m, 1));
     if (m) {
@@ -876,8 +882,8 @@ std::unique_ptr<prgpu_graph> graph_build_host(uint32_t n, const uint32_t* pairs,
 std::unique_ptr<prgpu_graph> graph_from_csr(uint32_t n, const uint64_t* off, const uint32_t* nbr,
                                             const uint32_t* out_degree, int device,
                                             cudaStream_t st) {
-    if (n == 0) fail(PRGPU_EINVAL, "graph_from_csr: vertex_count must be >= 1");
     if (off[0] != 0) fail(PRGPU_EINVAL, "graph_from_csr: in_offsets[0] != 0");
+    if (n == 0) return empty_graph(device); // pagerank() throws on it (pagerank.hpp:74)
     const uint64_t e = off[n];
     const uint32_t lg = bits_for(n);
     PhaseLog ph("from_csr", st);
@@ -910,11 +916,9 @@ std::unique_ptr<prgpu_graph> graph_from_csr(uint32_t n, const uint64_t* off, con
     }
     ph.mark("offsets h2d + check");
     std::unique_ptr<prgpu_graph> g;
-    DevBuf<uint32_t> cnt(n);
     try {
         g = assemble_vertices(n, d_off.p, e, d_deg.p, lg, device, st);
         ph.mark("vertex half");
-        PRGPU_CUDA(cudaMemsetAsync(cnt.p, 0, (size_t)n * 4, st));
         EdgeFill fill(g.get(), st);
         const char* rs = std::getenv("PRGPU_ROW_SORT"); // =0: leave rows unsorted (tuning)
         const bool sort_rows = !(rs && std::atoi(rs) == 0);
@@ -922,7 +926,7 @@ std::unique_ptr<prgpu_graph> graph_from_csr(uint32_t n, const uint64_t* off, con
         for (size_t c = 0; c < landed.size(); ++c) {
             PRGPU_CUDA(cudaStreamWaitEvent(st, *landed[c], 0));
             const uint64_t j = c * slice, je = std::min(e, j + slice);
-            fill.place(d_off.p, d_nbr.p, j, je, cnt.p, bad.p, st);
+            fill.place(d_off.p, d_nbr.p, j, je, d_deg.p, bad.p, st);
             if (!sort_rows) continue;
             // rows whose last edge is before je (the last slice: every row)
             const uint32_t v_end = c + 1 == landed.size()
@@ -931,11 +935,9 @@ std::unique_ptr<prgpu_graph> graph_from_csr(uint32_t n, const uint64_t* off, con
             fill.sort_slice(v_done, v_end, st);
             v_done = v_end;
         }
-        if (read_flag(bad, st))
-            fail(PRGPU_EINVAL, "graph_from_csr: neighbours not ascending/unique/in range");
-        compare_u32<<<grid_for(n), kThreads, 0, st>>>(cnt.p, d_deg.p, n, bad.p);
-        PRGPU_LAUNCHED("compare_u32");
-        if (read_flag(bad, st)) fail(PRGPU_EINVAL, "graph_from_csr: out_degree does not match in_neighbors");
+        const int why = read_flag(bad, st);
+        if (why == 1) fail(PRGPU_EINVAL, "graph_from_csr: in-neighbour >= vertex_count");
+        if (why) fail(PRGPU_EINVAL, "graph_from_csr: an in-neighbour has out_degree 0 (pagerank.hpp:91 would divide by zero)");
         ph.mark("edges placed");
         fill.finish(st);
         ph.mark("rows sorted");
@@ -1008,6 +1010,10 @@ void graph_download(const prgpu_graph* g, uint64_t* h_off, uint32_t* h_nbr, uint
                     uint32_t* h_dang, cudaStream_t st) {
     const uint32_t n = g->n;
     const uint64_t e = g->e;
+    if (n == 0) { // the empty graph: in_offsets = {0}
+        if (h_off) h_off[0] = 0;
+        return;
+    }
     if (h_deg || h_dang) {
         DevBuf<uint32_t> deg(n);
         gather_u32<<<grid_for(n), kThreads, 0, st>>>(g->deg.p, g->new_of_old.p, deg.p, n);

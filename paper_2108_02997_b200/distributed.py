@@ -331,15 +331,37 @@ def _run_peer_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ran
             part.close()
             return _run_distributed_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ranks,
                                        rank, world)
+    # set-up succeeded on EVERY rank, or all ranks release the mappings and
+    # run the NCCL exchange together (a rank that failed alone would leave the
+    # others spinning in the finalize wait on arrivals that never come)
+    setup_ok = True
     try:
         part.set_peers(*peers)
         part.init()
         torch.cuda.current_stream(part.contrib.device).synchronize()
+    except Exception:
+        setup_ok = False
+    if world > 1:
+        flag = torch.tensor([1 if setup_ok else 0], device=part.contrib.device, dtype=torch.int32)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        setup_ok = int(flag.item()) == 1
+    if not setup_ok:
+        # nothing was launched: no peer stores can be in flight
+        for ptr, off in opened:
+            lib().prgpu_ipc_close(C.c_void_p(ptr), off)
+        part.close()
+        if world == 1:
+            raise RuntimeError("fused exchange set-up failed on the only rank")
+        return _run_distributed_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ranks,
+                                   rank, world)
+    launched = False
+    try:
         if world > 1:
             dist.barrier()  # every rank's counters are reset before anyone arrives
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record()
         part.launch()
+        launched = True
         stop.record()
         torch.cuda.current_stream(part.contrib.device).synchronize()
         K = len(alphas)
@@ -351,6 +373,14 @@ def _run_peer_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ran
         if want_ranks:
             res.ranks = _gather_ranks(part, g, K, world)
     finally:
+        # on the error path our own loop is drained first (it finished, or the
+        # bounded arrival wait trapped); peers' stores into our buffers can
+        # only target iterations our loop waited for, so none is in flight
+        if launched:
+            try:
+                torch.cuda.current_stream(part.contrib.device).synchronize()
+            except Exception:
+                pass
         for ptr, off in opened:
             lib().prgpu_ipc_close(C.c_void_p(ptr), off)
         part.close()

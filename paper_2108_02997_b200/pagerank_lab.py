@@ -191,8 +191,8 @@ def _new_graph(fn, *args, device: Optional[int] = None) -> CsrGraph:
 def build_csr(el: EdgeList, device: Optional[int] = None) -> CsrGraph:
     """graph.hpp:204-234 on the device: sort by (target, source), unique,
     count, scan, fill; self-loops kept, duplicates dropped."""
-    if el.vertex_count < 1:
-        raise ValueError("build_csr: vertex_count must be >= 1")
+    # vertex_count 0 gives the empty graph (graph.hpp:204-234); pagerank()
+    # then raises (pagerank.hpp:74)
     pairs = np.ascontiguousarray(el.edges, dtype=np.uint32)
     return _new_graph(lib().prgpu_graph_build, el.vertex_count,
                       pairs.ctypes.data if pairs.size else None, pairs.shape[0], device=device)
@@ -651,7 +651,7 @@ def _sweep_fused(plan: SweepPlan, g: CsrGraph, label: str, ref: np.ndarray) -> l
         for rep in range(plan.repeats):
             br = pagerank_batched(g, chunk, tau_min, NormKind(plan.norms[0]), plan.max_iterations,
                                   stop_mask=mask, ref_ranks=ref, want_ranks=False)
-            if runs and not np.array_equal(br.trace, runs[0].trace):
+            if runs and not np.array_equal(br.trace, runs[0].trace, equal_nan=True):
                 raise RuntimeError(f"sweep: iteration trace changed between repeats on {label}")
             runs.append(br)
         per_iter = sum(r.loop_ms for r in runs) / len(runs) / max(1, runs[0].run_iterations)

@@ -181,3 +181,35 @@ def test_step_rows_is_one_reference_iteration(oracle):
             sub, _ = oracle.step_rows(prev, g.out_degree, alpha, off, nbr)
             assert np.array_equal(sub, nxt[rows])
     oracle.free_csr(h)
+
+
+def test_pagerank_mt_bit_identical(oracle, ref):
+    """orc_pagerank_mt (the vertex loop on host threads, the CPU baseline for
+    C4/C5) gives the reference's ranks, errors and iterations bit for bit."""
+    n, pairs = oracle.rmat(14, 16, 0.57, 0.19, 0.19, 2108)
+    g = oracle.build_csr(n, pairs)
+    h = ref.build_csr_handle(n, pairs)
+    v = oracle.csr_view(n, g.in_offsets, g.in_neighbors, g.out_degree)
+    try:
+        for a, norm in ((0.85, "l1"), (0.95, "l2"), (1.0, "linf")):
+            want = ref.pagerank(h, a, 1e-9, norm, 500, trace=True)
+            for threads in (1, 3, 8):
+                got = oracle.pagerank_mt(v, a, 1e-9, norm, 500, threads=threads, trace=True)
+                assert got["iterations"] == want["iterations"]
+                assert np.array_equal(got["ranks"], want["ranks"])
+                assert np.array_equal(got["err_trace"], want["err_trace"])
+    finally:
+        ref.free_csr(h)
+
+
+def test_inplace_rmat_csr_matches_build_csr(oracle, ref):
+    """csr_inplace.hpp (the reference arm's C5 builder) gives build_csr's arrays."""
+    n, pairs = oracle.rmat(15, 16, 0.57, 0.19, 0.19, 2108)
+    want = ref.build_csr(n, pairs)
+    h = ref.csr_rmat(15, 16, 0.57, 0.19, 0.19, 2108)
+    try:
+        got = ref.csr_arrays(h)
+    finally:
+        ref.free_csr(h)
+    for k in ("in_offsets", "in_neighbors", "out_degree", "dangling"):
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k

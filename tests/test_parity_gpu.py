@@ -83,8 +83,15 @@ def test_known_answers(prl):
     for bad in (dict(alpha=1.5), dict(alpha=-0.1), dict(tolerance=0.0), dict(max_iterations=0)):
         with pytest.raises(ValueError):  # :89-100
             prl.pagerank(two, prl.PageRankConfig(**bad))
-    with pytest.raises(ValueError):
-        prl.build_csr(prl.EdgeList(0))
+    # graph.hpp:204-234: vertex_count 0 builds the empty graph; pagerank()
+    # rejects it (pagerank.hpp:74) after validating the config (:73)
+    empty = prl.build_csr(prl.EdgeList(0))
+    assert empty.vertex_count == 0 and empty.edge_count() == 0
+    assert empty.in_offsets.tolist() == [0] and empty.dangling.size == 0
+    with pytest.raises(ValueError, match="no vertices"):
+        prl.pagerank(empty, prl.PageRankConfig())
+    with pytest.raises(ValueError, match="alpha"):
+        prl.pagerank(empty, prl.PageRankConfig(alpha=2.0))
     # iteration cap honesty (:228-237)
     web = prl.build_csr(el(6, [[0, 1], [0, 2], [1, 2], [2, 0], [3, 2], [4, 0], [4, 3], [2, 4], [1, 5]]))
     r = prl.pagerank(web, prl.PageRankConfig(1.0, 1e-15, prl.NormKind.L1, 50))
@@ -161,13 +168,46 @@ def test_from_csr_roundtrip_and_validation(prl, oracle):
     assert np.array_equal(g.in_offsets, want.in_offsets)
     assert np.array_equal(g.in_neighbors, want.in_neighbors)
     assert np.array_equal(g.dangling, want.dangling)
-    bad = want.in_neighbors.copy()
-    bad[0], bad[1] = bad[1], bad[0]
-    if want.in_offsets[1] >= 2:
-        with pytest.raises(ValueError):
-            prl.csr_from_arrays(n, want.in_offsets, bad, want.out_degree)
     with pytest.raises(ValueError):
         prl.build_csr(prl.EdgeList(3, np.array([[0, 5]], np.uint32)))
+    with pytest.raises(ValueError):  # in-neighbour out of range
+        prl.csr_from_arrays(3, np.array([0, 1, 1, 1], np.uint64), np.array([7], np.uint32),
+                            np.array([1, 0, 0], np.uint32))
+    with pytest.raises(ValueError):  # in-neighbour with out_degree 0: pagerank.hpp:91 divides by it
+        prl.csr_from_arrays(3, np.array([0, 1, 1, 1], np.uint64), np.array([2], np.uint32),
+                            np.array([1, 0, 0], np.uint32))
+
+
+def test_from_csr_hand_filled_like_reference(prl, ref):
+    """A hand-filled CsrGraph (graph.hpp:47-60) is used by pagerank() as given
+    (pagerank.hpp:89-93): rows in any order, duplicate in-neighbours counted
+    twice, out_degree taken from the caller even where it differs from the
+    neighbour histogram.  The device graph accepts the same arrays and the
+    run matches the reference's own pagerank on them."""
+    rs = np.random.default_rng(7)
+    n = 3000
+    rows = []
+    for v in range(n):
+        d = int(rs.integers(0, 12)) if v % 17 else int(rs.integers(200, 5000))  # some hub rows
+        rows.append(rs.integers(0, n, d).astype(np.uint32))  # unsorted, with duplicates
+    off = np.zeros(n + 1, np.uint64)
+    off[1:] = np.cumsum([len(r) for r in rows])
+    nbr = np.concatenate(rows).astype(np.uint32)
+    hist = np.bincount(nbr, minlength=n).astype(np.uint32)
+    deg = hist + (rs.integers(0, 3, n) * (hist > 0)).astype(np.uint32)  # inflated degrees
+    deg[(hist == 0) & (rs.random(n) < 0.3)] = 5  # sources the graph never gathers
+    assert np.any(np.diff(nbr.astype(np.int64)) < 0) and len(np.unique(nbr)) < nbr.size
+    g = prl.csr_from_arrays(n, off, nbr, deg)
+    assert np.array_equal(g.out_degree, deg)
+    h = ref.csr_from_arrays(n, off, nbr, deg)
+    try:
+        for a, norm in ((0.85, "l1"), (0.95, "l2"), (1.0, "linf")):
+            want = ref.pagerank(h, a, 1e-10, norm, 500, trace=True)
+            got = prl.pagerank(g, prl.PageRankConfig(a, 1e-10, nk(prl, norm), 500))
+            assert iterations_match(got.iterations, want["iterations"], want["err_trace"], 1e-10), a
+            assert np.max(np.abs(got.ranks - want["ranks"])) <= RANK_TOL, a
+    finally:
+        ref.free_csr(h)
 
 
 def test_from_csr_sliced_build_matches_generator(prl):
