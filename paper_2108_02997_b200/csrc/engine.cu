@@ -781,6 +781,8 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     // ping-pong buffers [parity][src][KS].
     P.l2mode = 0;
     if (const char* m = std::getenv("PRGPU_L2MODE")) P.l2mode = (uint32_t)std::atoi(m);
+    P.gpol = 0;
+    if (const char* gp = std::getenv("PRGPU_GPOL")) P.gpol = (uint32_t)std::atoi(gp);
     P.hot_src = 0;
     if (const char* h = std::getenv("PRGPU_HOT_MB")) // tuning: L2-resident source rows
         P.hot_src = (uint32_t)std::min<uint64_t>(nsrc, ((uint64_t)std::atoi(h) << 20) / (KS * sizeof(double)));

@@ -115,7 +115,9 @@ struct Params {
     uint32_t iso_begin;          // first row with in- and out-degree 0
     uint32_t G;
     uint32_t hot_src;            // sources [0, hot_src) in the L2-resident region
-    uint32_t l2mode;             // 0 evict hints, 1 persisting window, 2 no hints
+    uint32_t l2mode;             // 0 evict hints, 2 no hints (streams); >= 3 contribution-write hints
+    uint32_t gpol;               // gather L2 policy (tuning): 0 plain; 1 hot evict_last / cold
+                                 // evict_first; 2 hot normal / cold evict_first; 3 hot evict_last / cold normal
     uint32_t skip_mask;          // profiling only (PRGPU_SKIP): 1 chunk, 2 packed, 4 empty tasks,
                                  // 8 rank stores, 16 rank loads, 32 contribution stores
     // multi-GPU partition (1D row ranges): this rank runs tasks [task_begin, task_end)
@@ -260,6 +262,21 @@ __device__ __forceinline__ void load_w(const double* __restrict__ p, double (&v)
 }
 
 template <int W>
+__device__ __forceinline__ void load_w_pol(const double* __restrict__ p, double (&v)[W], uint64_t pol) {
+    if constexpr (W % 2 == 0) {
+#pragma unroll
+        for (int w = 0; w < W; w += 2)
+            asm("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                : "=d"(v[w]), "=d"(v[w + 1])
+                : "l"(p + w), "l"(pol));
+    } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+            asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v[w]) : "l"(p + w), "l"(pol));
+    }
+}
+
+template <int W>
 __device__ __forceinline__ void store_w(double* p, const double (&v)[W]) {
     if constexpr (W % 2 == 0) {
 #pragma unroll
@@ -361,6 +378,7 @@ struct Warp {
     const int* s_active;
     static constexpr bool SMEMP = SMEMP_; // partials in a shared-memory column (frees registers)
     Partials<W, QM, SMEMP> part;
+    uint64_t pol_hot = 0, pol_cold = 0; // gather policies (P.gpol)
 
     __device__ Warp(const Params& p, int parity, int ln, const double* a, const double* c0,
                     const int* act, double* smem_cols, int tid)
@@ -368,6 +386,17 @@ struct Warp {
           rn(p.rank[parity ^ 1]), cpl(p.cbase + p.cold_off[parity] * KS + (ln % LG) * W), s_alpha(a),
           s_c0(c0), s_active(act) {
         part.init(smem_cols, tid);
+        if (p.gpol) {
+            pol_hot = (p.gpol == 2) ? policy_evict_normal() : policy_evict_last();
+            pol_cold = (p.gpol == 3) ? policy_evict_normal() : policy_evict_first();
+        }
+    }
+
+    // one source's contribution row slice (the gather of pagerank.hpp:91)
+    __device__ __forceinline__ void gather(uint32_t src, double (&v)[W]) const {
+        const double* a = cpl + (size_t)src * KS;
+        if (P.gpol) load_w_pol<W>(a, v, src < P.hot_src ? pol_hot : pol_cold);
+        else load_w<W>(a, v);
     }
 
     __device__ __forceinline__ bool lane_ok(int sl) const { return KS == KP || sl * W < KS; }
@@ -521,7 +550,7 @@ struct Warp {
 #pragma unroll
                     for (int w = 0; w < W; ++w) v[j][w] = 0.0;
                     if (ok && pos >= off0 && pos < ne)
-                        load_w<W>(cpl + (size_t)us[j0 + j] * KS, v[j]);
+                        gather(us[j0 + j], v[j]);
                 }
 #pragma unroll
                 for (int j = 0; j < EF; ++j)
@@ -560,7 +589,7 @@ struct Warp {
                         const uint32_t e = base + 32u * j + (i0 + i) * ES + slot;
 #pragma unroll
                         for (int w = 0; w < W; ++w) v[i][w] = 0.0;
-                        if (ok && e < ne) load_w<W>(cpl + (size_t)src * KS, v[i]);
+                        if (ok && e < ne) gather(src, v[i]);
                     }
 #pragma unroll
                     for (int i = 0; i < SB; ++i)
@@ -659,7 +688,7 @@ struct Warp {
                 for (int tq = 0; tq < 4; ++tq) {
                     const uint32_t e = qb + 4u * ES * j + tq;
                     if (live && e >= off0 && e < ne)
-                        load_w<W>(cpl + (size_t)us[j][tq] * KS, v[j][tq]);
+                        gather(us[j][tq], v[j][tq]);
                 }
 #pragma unroll
             for (int j = 0; j < C::QJ; ++j)
@@ -737,7 +766,7 @@ struct Warp {
 #pragma unroll
                         for (int w = 0; w < W; ++w) vals[j][w] = 0.0;
                         if (ok && q + j0 + j >= off0 && q + j0 + j < ne)
-                            load_w<W>(cpl + (size_t)us[j0 + j] * KS, vals[j]);
+                            gather(us[j0 + j], vals[j]);
                     }
 #pragma unroll
                     for (int j = 0; j < EF; ++j)
@@ -813,7 +842,7 @@ struct Warp {
                     for (int j = 0; j < 8; ++j) {
 #pragma unroll
                         for (int w = 0; w < W; ++w) vals[j][w] = 0.0;
-                        if (vb & (1u << j)) load_w<W>(cpl + (size_t)s_col[q + j] * KS, vals[j]);
+                        if (vb & (1u << j)) gather(s_col[q + j], vals[j]);
                     }
 #pragma unroll
                     for (int j = 0; j < 8; ++j)

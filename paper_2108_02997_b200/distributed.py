@@ -265,17 +265,24 @@ def run_distributed(g: CsrGraph, alphas: Sequence[float], tolerance=1e-6,
     other's buffers (CUDA IPC), the pull kernel stores every contribution row
     and the partials straight into all peers over NVLink and the finalize
     kernel waits for the arrivals; the whole loop is one CUDA graph per rank,
-    no collective call and no host round trip per iteration."""
+    no collective call and no host round trip per iteration.
+    exchange="peer-host": the same fused kernels and IPC mappings (peer
+    stores, system-scope fences, arrival counters), but the host steps the
+    loop: pull, stream sync, a barrier across ranks, then the finalize — whose
+    arrival wait is already satisfied, so no kernel ever waits on another
+    process.  Slower (a host round trip per iteration); it is what runs the
+    fused exchange between processes that share one GPU (tests), where
+    kernels spinning on each other are not allowed to co-run."""
     import torch
     import torch.distributed as dist
     rank, world = dist.get_rank(), dist.get_world_size()
     stream = torch.cuda.Stream(device=g.device)  # engine, copies and NCCL share it
     with torch.cuda.stream(stream):
-        if exchange == "peer":
+        if exchange in ("peer", "peer-host"):
             return _run_peer_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ranks,
-                                rank, world)
+                                rank, world, host_steps=exchange == "peer-host")
         if exchange != "nccl":
-            raise ValueError("exchange must be 'nccl' or 'peer'")
+            raise ValueError("exchange must be 'nccl', 'peer' or 'peer-host'")
         return _run_distributed_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ranks,
                                    rank, world)
 
@@ -294,7 +301,19 @@ def _ipc_open(handle: bytes, offset: int, device: int) -> int:
     return p.value
 
 
-def _run_peer_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ranks, rank, world):
+def _agree_min(flag: int, device) -> int:
+    """MIN of an int over the ranks, on whatever backend the group runs
+    (NCCL wants a device tensor, gloo a host one)."""
+    import torch
+    import torch.distributed as dist
+    on_host = dist.get_backend() == "gloo"
+    t = torch.tensor([flag], dtype=torch.int32, device="cpu" if on_host else device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return int(t.item())
+
+
+def _run_peer_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ranks, rank, world,
+                 host_steps: bool = False):
     import torch
     import torch.distributed as dist
     part = _Part(g, alphas, tolerance, norm, max_iterations, stop_mask, rank, world, g.device, fused=True)
@@ -323,9 +342,7 @@ def _run_peer_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ran
                 opened.append((ptr, off))
                 peers[j].append(ptr)
         # every rank mapped every peer, or all fall back to the NCCL exchange
-        flag = torch.tensor([1 if ok else 0], device=part.contrib.device, dtype=torch.int32)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        if int(flag.item()) == 0:
+        if _agree_min(1 if ok else 0, part.contrib.device) == 0:
             for ptr, off in opened:
                 lib().prgpu_ipc_close(C.c_void_p(ptr), off)
             part.close()
@@ -342,9 +359,7 @@ def _run_peer_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ran
     except Exception:
         setup_ok = False
     if world > 1:
-        flag = torch.tensor([1 if setup_ok else 0], device=part.contrib.device, dtype=torch.int32)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        setup_ok = int(flag.item()) == 1
+        setup_ok = _agree_min(1 if setup_ok else 0, part.contrib.device) == 1
     if not setup_ok:
         # nothing was launched: no peer stores can be in flight
         for ptr, off in opened:
@@ -360,8 +375,21 @@ def _run_peer_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ran
             dist.barrier()  # every rank's counters are reset before anyone arrives
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record()
-        part.launch()
-        launched = True
+        if host_steps:
+            cur = torch.cuda.current_stream(part.contrib.device)
+            launched = True
+            for _ in range(max_iterations):
+                part.step()       # stores rows + partials into the peers, then arrives
+                cur.synchronize()
+                if world > 1:
+                    dist.barrier()  # every rank's stores and arrivals are complete
+                part.finalize()   # arrival wait already satisfied: returns at once
+                cur.synchronize()
+                if not part.active():
+                    break
+        else:
+            part.launch()
+            launched = True
         stop.record()
         torch.cuda.current_stream(part.contrib.device).synchronize()
         K = len(alphas)
@@ -435,7 +463,12 @@ def _gather_ranks(part: _Part, g: CsrGraph, K: int, world: int) -> np.ndarray:
         eng = torch.zeros((K, g.vertex_count), dtype=torch.float64, device=dev)
         part.owned_ranks_into(eng)
         if world > 1:
-            dist.all_reduce(eng, op=dist.ReduceOp.SUM)
+            if dist.get_backend() == "gloo":  # host reduction (exact: disjoint rows, zeros elsewhere)
+                host = eng.cpu()
+                dist.all_reduce(host, op=dist.ReduceOp.SUM)
+                eng.copy_(host)
+            else:
+                dist.all_reduce(eng, op=dist.ReduceOp.SUM)
         return _to_caller_host(eng, g, dev)
     rows = [q.row_end - q.row_begin for q in part.parts]
     ld = max(rows)
