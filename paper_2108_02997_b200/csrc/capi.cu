@@ -24,7 +24,14 @@ void pool_init() {
     std::call_once(once[dev & 63], [dev] {
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            // memory freed back to the pool stays mapped up to this much, so a
+            // caller solving graph after graph (the e2e path: C5 maps ~60 GB
+            // per build + solve) does not re-map physical memory every call;
+            // PRGPU_POOL_KEEP_GB overrides (0: release everything at sync)
             uint64_t keep = kPoolKeepBytes;
+            size_t fr = 0, total = 0;
+            if (cudaMemGetInfo(&fr, &total) == cudaSuccess) keep = std::max<uint64_t>(keep, total / 2);
+            if (const char* k = std::getenv("PRGPU_POOL_KEEP_GB")) keep = (uint64_t)std::atoll(k) << 30;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
         }
     });

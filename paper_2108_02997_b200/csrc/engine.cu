@@ -781,6 +781,8 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     // ping-pong buffers [parity][src][KS].
     P.l2mode = 0;
     if (const char* m = std::getenv("PRGPU_L2MODE")) P.l2mode = (uint32_t)std::atoi(m);
+    P.pf = 0;
+    if (const char* pf = std::getenv("PRGPU_PF")) P.pf = (uint32_t)std::atoi(pf);
     P.gpol = 0;
     if (const char* gp = std::getenv("PRGPU_GPOL")) P.gpol = (uint32_t)std::atoi(gp);
     P.hot_src = 0;
@@ -1943,7 +1945,30 @@ double session_time_pull(prgpu_session* s, int launches) {
     GlobalState gsh;
     PRGPU_CUDA(cudaMemcpyAsync(&gsh, s->gs.p, sizeof(gsh), cudaMemcpyDeviceToHost, st));
     PRGPU_CUDA(cudaStreamSynchronize(st));
+    // PRGPU_PERSIST_MB (tuning, host-driven runs only): an L2 persisting
+    // access-policy window over the first X MB of the parity this iteration
+    // gathers from (the hottest sources, ids in degree order)
+    const char* pmb = std::getenv("PRGPU_PERSIST_MB");
+    const size_t persist_b = pmb ? ((size_t)std::atoi(pmb) << 20) : 0;
+    if (persist_b) {
+        int maxp = 0;
+        PRGPU_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, s->g->device));
+        PRGPU_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(persist_b, (size_t)maxp)));
+    }
     for (; done < launches && gsh.any_active; ++done) {
+        if (persist_b) {
+            const Params& P0 = s->P;
+            const int par = gsh.iter & 1;
+            int mode = gsh.mode;
+            const double* base = P0.mode_cbase[mode] + P0.mode_cold_off[mode][par] * P0.mode_ks[mode];
+            cudaStreamAttrValue av = {};
+            av.accessPolicyWindow.base_ptr = (void*)base;
+            av.accessPolicyWindow.num_bytes = persist_b;
+            av.accessPolicyWindow.hitRatio = 1.0f;
+            av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            PRGPU_CUDA(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &av));
+        }
         PRGPU_CUDA(cudaEventRecord(ev[2 * done], st));
         for (const auto& l : s->launches) {
             if (l.P.mode_id != gsh.mode) continue;
@@ -1957,6 +1982,12 @@ double session_time_pull(prgpu_session* s, int launches) {
         PRGPU_CUDA(cudaEventRecord(ev[2 * done + 1], st));
         PRGPU_CUDA(cudaMemcpyAsync(&gsh, s->gs.p, sizeof(gsh), cudaMemcpyDeviceToHost, st));
         PRGPU_CUDA(cudaStreamSynchronize(st));
+    }
+    if (persist_b) {
+        cudaStreamAttrValue av = {};
+        av.accessPolicyWindow.num_bytes = 0;
+        PRGPU_CUDA(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &av));
+        PRGPU_CUDA(cudaCtxResetPersistingL2Cache());
     }
     double total = 0;
     const bool log = std::getenv("PRGPU_TIMING_LOG") != nullptr; // per-iteration times (tuning)

@@ -116,6 +116,7 @@ struct Params {
     uint32_t G;
     uint32_t hot_src;            // sources [0, hot_src) in the L2-resident region
     uint32_t l2mode;             // 0 evict hints, 2 no hints (streams); >= 3 contribution-write hints
+    uint32_t pf;                 // L2 prefetch of upcoming gathers: 0 off, 1 on (PRGPU_PF)
     uint32_t gpol;               // gather L2 policy (tuning): 0 plain; 1 hot evict_last / cold
                                  // evict_first; 2 hot normal / cold evict_first; 3 hot evict_last / cold normal
     uint32_t skip_mask;          // profiling only (PRGPU_SKIP): 1 chunk, 2 packed, 4 empty tasks,
@@ -390,12 +391,31 @@ struct Warp {
             pol_hot = (p.gpol == 2) ? policy_evict_normal() : policy_evict_last();
             pol_cold = (p.gpol == 3) ? policy_evict_normal() : policy_evict_first();
         }
+        // gpol 4: cold rows __ldcs; 5: cold rows L1::no_allocate + L2 evict_first
+    }
+
+    // L2 prefetch of a source's contribution row (no register held: the
+    // later gather of the row then hits L2 instead of waiting on DRAM)
+    __device__ __forceinline__ void prefetch_row(uint32_t src) const {
+        const double* a = P.cbase + (P.cold_off[par] + src) * KS;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
     }
 
     // one source's contribution row slice (the gather of pagerank.hpp:91)
     __device__ __forceinline__ void gather(uint32_t src, double (&v)[W]) const {
         const double* a = cpl + (size_t)src * KS;
-        if (P.gpol) load_w_pol<W>(a, v, src < P.hot_src ? pol_hot : pol_cold);
+        if (P.gpol == 4 || P.gpol == 5) { // cold rows streamed (.cs / L1 no-allocate + evict_first)
+            if (src < P.hot_src) load_w<W>(a, v);
+            else if (P.gpol == 4) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) v[w] = __ldcs(a + w);
+            } else {
+#pragma unroll
+                for (int w = 0; w < W; ++w)
+                    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                        : "=d"(v[w]) : "l"(a + w), "l"(pol_cold));
+            }
+        } else if (P.gpol) load_w_pol<W>(a, v, src < P.hot_src ? pol_hot : pol_cold);
         else load_w<W>(a, v);
     }
 
@@ -571,12 +591,41 @@ struct Warp {
         const bool ok = slice_live();
         constexpr int STEPS = 32 / ES; // steps per 32-edge group
         constexpr int SB = STEPS < 4 ? STEPS : 4; // gathers in flight per sub-batch (registers)
-        for (uint32_t base = 0; base < ne; base += 128) {
-            uint32_t c[4];
+        // P.pf: colidx is loaded two 128-edge blocks ahead and the rows of
+        // block b+1 are prefetched into L2 before block b is gathered, so
+        // gathers mostly hit L2 (the kernel is DRAM-latency bound: this
+        // raises the rows in flight per warp without holding registers)
+        const bool pf = P.pf != 0; // warp-uniform (every lane holds colidx for the shuffles)
+        auto ld_block = [&](uint32_t base, uint32_t (&c)[4]) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const uint32_t e = base + lane + 32u * j;
                 c[j] = e < ne ? ld_stream_u32(cb + e, sp) : 0u;
+            }
+        };
+        auto pf_block = [&](uint32_t base, const uint32_t (&c)[4]) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (base + lane + 32u * j < ne) prefetch_row(c[j]);
+        };
+        uint32_t cn[4], cnn[4];
+        if (pf) {
+            ld_block(0, cn);
+            ld_block(128, cnn);
+            pf_block(0, cn);
+        }
+        for (uint32_t base = 0; base < ne; base += 128) {
+            uint32_t c[4];
+            if (pf) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    c[j] = cn[j];
+                    cn[j] = cnn[j];
+                }
+                pf_block(base + 128, cn);
+                if (base + 256 < ne) ld_block(base + 256, cnn);
+            } else {
+                ld_block(base, c);
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -796,6 +845,8 @@ struct Warp {
         const uint32_t ne_all = (uint32_t)(s_off[R] - e0);
         for (uint32_t x = lane; x < ne_all; x += 32) s_col[x] = ld_stream_u32(P.col + e0 + x, sp);
         __syncwarp();
+        if (P.pf) // every row of the run in flight to L2 at once (the walk below is one row per slot)
+            for (uint32_t x = lane; x < ne_all; x += 32) prefetch_row(s_col[x]);
         uint32_t i = slot;
         if (i < R) {
             const bool ok = slice_live();

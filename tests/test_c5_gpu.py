@@ -15,8 +15,13 @@ ranks sequentially, the GPU as a tree, a ~3e-10 relative difference in D); the o
 tau and equal to the GPU's reported err (1e-9 relative); the GPU's err trace
 above tau at t-1; sum of ranks 1 +- 1e-9 (acceptance.cpp:134-161).
 """
+import json
+import os
+
 import numpy as np
 import pytest
+
+from conftest import GOLD
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -81,3 +86,63 @@ def test_c5_two_rank_fused_partition_matches_single_gpu(prl):
     for k in range(len(ALPHAS)):
         assert two.iterations[k] == single.results[k].iterations, k
         assert float(np.max(np.abs(two.ranks[k] - single.results[k].ranks))) <= 1e-13, k
+
+
+GOLDEN_C5 = os.path.join(GOLD, "c5_rmat28.json")
+
+
+@pytest.mark.skipif(not os.path.exists(GOLDEN_C5), reason="c5 golden not generated (oracle/make_c5_golden.py)")
+def test_c5_rmat28_k3_against_reference_run(prl):
+    """BASELINE configs[4] against a full run of the reference's own
+    pagerank() on the same graph (oracle/make_c5_golden.py; the graph's
+    fingerprint is the golden's): per-lane iterations exactly (north_star;
+    +-1 only where the reference's err is within 1e-3 tau of tau), the err
+    trace, ranks within Linf 1e-10 at 65,536 sampled vertices and the top
+    4,096, and size-independent checks over ALL 268M ranks per lane: the
+    total, 4,096 block sums and block maxima (2^16 vertices each) and 8
+    random-sign projections."""
+    gold = json.load(open(GOLDEN_C5))
+    arr = np.load(os.path.join(GOLD, "c5_rmat28.npz"))
+    g = prl.generate_rmat(28, 16, 0.57, 0.19, 0.19, gold["seed"])
+    assert g.vertex_count == gold["graph"]["n"] and g.edge_count() == gold["graph"]["e"]
+    assert int(g.info.dangling_count) == gold["graph"]["ndangling"]
+    run = prl.pagerank_batched(g, ALPHAS, TOL, prl.NormKind.L2, 500)
+    idx = arr["sample_idx"]
+    block = gold["block"]
+    for k, lane in enumerate(gold["lanes"]):
+        res = run.results[k]
+        tr = arr[f"lane{k}_trace"]
+        assert res.converged == lane["converged"]
+        if res.iterations != lane["iterations"]:
+            t = min(res.iterations, lane["iterations"])
+            assert abs(res.iterations - lane["iterations"]) == 1 and abs(tr[t - 1] - TOL) <= 1e-3 * TOL, k
+        n_it = min(res.iterations, lane["iterations"])
+        got_tr = run.trace[:n_it, k, 1]  # L2 column
+        assert np.allclose(got_tr, tr[:n_it], rtol=1e-9, atol=0), (k, got_tr, tr[:n_it])
+        r = res.ranks
+        assert float(np.max(np.abs(r[idx] - arr[f"lane{k}_sample"]))) <= 1e-10
+        ti = arr[f"lane{k}_top_idx"]
+        assert float(np.max(np.abs(r[ti] - arr[f"lane{k}_top"]))) <= 1e-10
+        assert abs(float(np.sum(r.astype(np.longdouble))) - lane["total"]) <= 1e-9
+        blocks = r.reshape(-1, block)
+        bs = np.sum(blocks, axis=1)
+        assert float(np.max(np.abs(bs - arr[f"lane{k}_block_sum"]))) <= 1e-12, k
+        assert float(np.max(np.abs(blocks.max(axis=1) - arr[f"lane{k}_block_max"]))) <= 1e-10, k
+        proj = _projections(r)
+        assert np.allclose(proj, lane["projections"], rtol=0, atol=1e-10), (k, proj, lane["projections"])
+        del blocks
+
+
+def _projections(r, count=8):
+    """oracle/make_c5_golden.py projections(): Sum w_i r_i, w_i = +-1 from a
+    splitmix64 of i (same constants)."""
+    out = []
+    i = np.arange(r.size, dtype=np.uint64)
+    for j in range(count):
+        z = i + np.uint64(j + 1) * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+        w = np.where((z >> np.uint64(63)) == 1, -1.0, 1.0)
+        out.append(float(np.sum(w * r)))
+    return out
