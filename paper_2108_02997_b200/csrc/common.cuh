@@ -8,6 +8,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -163,6 +166,19 @@ inline uint32_t bits_for(uint64_t n) { // ceil(log2(n)), >= 1
     return b;
 }
 
+// Hot/cold source split of the engine CSR (the split pull):
+// every row's in-edges partitioned, in their order, into those whose source
+// id is < hot (the most-gathered sources: their contributions stay
+// L2-resident while only they are gathered) and the rest, as two CSRs over
+// the same rows.  An iteration pulls the hot CSR first (row partials), then
+// the cold one (adds the partial, epilogue).
+struct SourceSplit {
+    uint32_t hot = 0;
+    uint64_t e_hot = 0, e_cold = 0;
+    DevBuf<uint64_t> off_hot, off_cold; // [n+1]
+    DevBuf<uint32_t> col_hot, col_cold; // [e_hot + 16], [e_cold + 16]
+};
+
 } // namespace prgpu
 
 // The device graph: engine layout (relabelled) + the permutation back to the
@@ -186,4 +202,12 @@ struct prgpu_graph {
     uint32_t hub_end = 0, warp_end = 0, nonempty_end = 0;
     bool locality = false; // rows in the caller's order within classes (low-degree graphs)
     uint32_t sort_end[6] = {0, 0, 0, 0, 0, 0}; // rows with in-degree > 512, 256, 128, 64, 32, 8
+    // source splits built on demand by sessions (graph_source_split), by threshold
+    std::mutex split_mu;
+    std::map<uint32_t, std::unique_ptr<prgpu::SourceSplit>> splits;
 };
+
+namespace prgpu {
+// the graph's hot/cold split at threshold `hot` (built on first use, cached)
+const SourceSplit& graph_source_split(prgpu_graph* g, uint32_t hot, cudaStream_t st);
+} // namespace prgpu

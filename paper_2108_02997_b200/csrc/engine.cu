@@ -387,6 +387,7 @@ struct prgpu_session {
     Params P{};
     Stream stream;
     DevBuf<double> rank, contrib, partials, trace, ref, chunk_acc;
+    DevBuf<double> hot_part; // split pull: [nonempty rows][KS] hot partial sums
     DevBuf<double> mode_contrib[kMaxModes]; // narrow modes' contribution buffers (after `stream`:
                                             // freed on it before it is destroyed)
     DevBuf<LaneState> lanes;
@@ -783,6 +784,8 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     if (const char* m = std::getenv("PRGPU_L2MODE")) P.l2mode = (uint32_t)std::atoi(m);
     P.pf = 0;
     if (const char* pf = std::getenv("PRGPU_PF")) P.pf = (uint32_t)std::atoi(pf);
+    P.split = 0;
+    P.hp = nullptr;
     P.gpol = 0;
     if (const char* gp = std::getenv("PRGPU_GPOL")) P.gpol = (uint32_t)std::atoi(gp);
     P.hot_src = 0;
@@ -972,6 +975,53 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         modes.erase(modes.begin(), modes.end() - 1);
     }
     part_cols = std::max(part_cols, build_launches(modes, P, s->launches, s->mode0));
+    // Split pull (single GPU): each iteration pulls the hot-source CSR first
+    // (sources [0, hot): their contribution rows, the most gathered ones,
+    // stay L2-resident while nothing else is gathered; row sums kept in
+    // hot_part), then the cold-source CSR, whose epilogue adds the hot
+    // partial.  Every pull launch of a mode becomes a hot copy (no partials,
+    // no finalize) ahead of the cold original.  PRGPU_SPLIT_MB = the hot
+    // table's size in the run's widest rows (0: one pass).
+    const uint32_t split_hot = [&]() -> uint32_t {
+        if (nranks >= 1) return 0;
+        const char* sm = std::getenv("PRGPU_SPLIT_MB");
+        const uint64_t mb = sm ? (uint64_t)std::atoll(sm) : 0;
+        if (!mb) return 0;
+        const uint64_t h = (mb << 20) / ((uint64_t)KS * sizeof(double));
+        return h >= g->nsrc ? 0u : (uint32_t)h; // everything hot: one pass
+    }();
+    if (split_hot && g->nonempty_end) {
+        const SourceSplit& sp = graph_source_split(g, split_hot, st);
+        s->hot_part.alloc((size_t)g->nonempty_end * KS);
+        std::vector<prgpu_session::Launch> ls;
+        for (size_t i = 0; i < s->launches.size();) {
+            size_t j = i; // [i, j): one mode's launches
+            while (j < s->launches.size() && s->launches[j].P.mode_id == s->launches[i].P.mode_id) ++j;
+            for (size_t k = i; k < j; ++k)
+                if (s->launches[k].repack) ls.push_back(s->launches[k]);
+            for (size_t k = i; k < j; ++k) {
+                if (s->launches[k].repack) continue;
+                prgpu_session::Launch h = s->launches[k];
+                h.P.split = 1;
+                h.P.row_off = sp.off_hot.p;
+                h.P.col = sp.col_hot.p;
+                h.P.hp = s->hot_part.p;
+                h.P.no_finalize = 1;
+                ls.push_back(h);
+            }
+            for (size_t k = i; k < j; ++k) {
+                if (s->launches[k].repack) continue;
+                prgpu_session::Launch c = s->launches[k];
+                c.P.split = 2;
+                c.P.row_off = sp.off_cold.p;
+                c.P.col = sp.col_cold.p;
+                c.P.hp = s->hot_part.p;
+                ls.push_back(c);
+            }
+            i = j;
+        }
+        s->launches = std::move(ls);
+    }
     s->partials.alloc(part_cols);
     P.partials = s->partials.p;
     s->modal_P.partials = s->partials.p;

@@ -948,6 +948,136 @@ std::unique_ptr<prgpu_graph> graph_from_csr(uint32_t n, const uint64_t* off, con
     return g;
 }
 
+// ---- hot/cold source split (SourceSplit) ----------------------------------------
+// Per row, its in-edges with source id < hot, counted (split_count) and then
+// placed (split_place) in their order into the hot CSR, the rest into the
+// cold one.  Rows with more than kHubMinDegree in-edges get a CTA (256-edge
+// windows, a CTA-wide prefix of the warps' hot counts keeps the order), the
+// others a warp (32-edge windows, ballot prefix).
+template <bool PLACE>
+__global__ void split_rows_warp(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col, uint32_t r0,
+                                uint32_t r1, uint32_t hot, uint64_t* __restrict__ cnt_hot,
+                                const uint64_t* __restrict__ off_hot, const uint64_t* __restrict__ off_cold,
+                                uint32_t* __restrict__ col_hot, uint32_t* __restrict__ col_cold) {
+    const uint32_t lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint32_t r = r0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); r < r1;
+         r += (gridDim.x * blockDim.x) >> 5) {
+        const uint64_t lo = off[r], hi = off[r + 1];
+        uint64_t h = PLACE ? off_hot[r] : 0, c = PLACE ? off_cold[r] : 0;
+        for (uint64_t j = lo; j < hi; j += 32) {
+            const bool in = j + lane < hi;
+            const uint32_t src = in ? col[j + lane] : 0u;
+            const bool is_hot = in && src < hot;
+            const unsigned bh = __ballot_sync(0xffffffffu, is_hot), bc = __ballot_sync(0xffffffffu, in && !is_hot);
+            if (PLACE) {
+                if (is_hot) col_hot[h + __popc(bh & lt)] = src;
+                else if (in) col_cold[c + __popc(bc & lt)] = src;
+                c += __popc(bc);
+            }
+            h += __popc(bh);
+        }
+        if (!PLACE && lane == 0) cnt_hot[r] = h;
+    }
+}
+
+template <bool PLACE>
+__global__ void __launch_bounds__(256) split_rows_block(const uint64_t* __restrict__ off,
+                                                        const uint32_t* __restrict__ col, uint32_t hot,
+                                                        uint64_t* __restrict__ cnt_hot,
+                                                        const uint64_t* __restrict__ off_hot,
+                                                        const uint64_t* __restrict__ off_cold,
+                                                        uint32_t* __restrict__ col_hot,
+                                                        uint32_t* __restrict__ col_cold) {
+    __shared__ unsigned s_h[8], s_c[8];
+    const uint32_t r = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint64_t lo = off[r], hi = off[r + 1];
+    uint64_t h = PLACE ? off_hot[r] : 0, c = PLACE ? off_cold[r] : 0;
+    for (uint64_t j0 = lo; j0 < hi; j0 += 256) {
+        const uint64_t j = j0 + threadIdx.x;
+        const bool in = j < hi;
+        const uint32_t src = in ? col[j] : 0u;
+        const bool is_hot = in && src < hot;
+        const unsigned bh = __ballot_sync(0xffffffffu, is_hot), bc = __ballot_sync(0xffffffffu, in && !is_hot);
+        if (lane == 0) {
+            s_h[warp] = __popc(bh);
+            s_c[warp] = __popc(bc);
+        }
+        __syncthreads();
+        uint64_t ph = 0, pc = 0, th = 0, tc = 0;
+        for (uint32_t w = 0; w < 8; ++w) {
+            if (w < warp) {
+                ph += s_h[w];
+                pc += s_c[w];
+            }
+            th += s_h[w];
+            tc += s_c[w];
+        }
+        if (PLACE) {
+            if (is_hot) col_hot[h + ph + __popc(bh & lt)] = src;
+            else if (in) col_cold[c + pc + __popc(bc & lt)] = src;
+        }
+        h += th;
+        c += tc;
+        __syncthreads();
+    }
+    if (!PLACE && threadIdx.x == 0) cnt_hot[r] = h;
+}
+
+__global__ void split_cold_off(const uint64_t* __restrict__ off, const uint64_t* __restrict__ off_hot, uint32_t n,
+                               uint64_t* __restrict__ off_cold) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= n; v += (uint64_t)gridDim.x * blockDim.x)
+        off_cold[v] = off[v] - off_hot[v];
+}
+
+const SourceSplit& graph_source_split(prgpu_graph* g, uint32_t hot, cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(g->split_mu);
+    auto it = g->splits.find(hot);
+    if (it != g->splits.end()) return *it->second;
+    AllocScope scope(st); // the split's buffers come from the pool like the graph's own
+    auto sp = std::make_unique<SourceSplit>();
+    sp->hot = hot;
+    const uint32_t n = g->n, hub = g->hub_end, rows = g->nonempty_end;
+    const unsigned wgrid = rows > hub ? grid_for((uint64_t)(rows - hub) * 32) : 0;
+    sp->off_hot.alloc((size_t)n + 1);
+    PRGPU_CUDA(cudaMemsetAsync(sp->off_hot.p, 0, ((size_t)n + 1) * 8, st));
+    if (hub) {
+        split_rows_block<false><<<hub, 256, 0, st>>>(g->row_off.p, g->col.p, hot, sp->off_hot.p, nullptr, nullptr,
+                                                     nullptr, nullptr);
+        PRGPU_LAUNCHED("split_rows_block");
+    }
+    if (wgrid) {
+        split_rows_warp<false><<<wgrid, kThreads, 0, st>>>(g->row_off.p, g->col.p, hub, rows, hot, sp->off_hot.p,
+                                                           nullptr, nullptr, nullptr, nullptr);
+        PRGPU_LAUNCHED("split_rows_warp");
+    }
+    exclusive_scan_u64(sp->off_hot.p, (uint64_t)n + 1, st); // hot counts -> hot row offsets
+    PRGPU_CUDA(cudaMemcpyAsync(&sp->e_hot, sp->off_hot.p + n, 8, cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    sp->e_cold = g->e - sp->e_hot;
+    sp->off_cold.alloc((size_t)n + 1);
+    split_cold_off<<<grid_for((uint64_t)n + 1), kThreads, 0, st>>>(g->row_off.p, sp->off_hot.p, n, sp->off_cold.p);
+    PRGPU_LAUNCHED("split_cold_off");
+    sp->col_hot.alloc(sp->e_hot + 16);
+    sp->col_cold.alloc(sp->e_cold + 16);
+    PRGPU_CUDA(cudaMemsetAsync(sp->col_hot.p + sp->e_hot, 0, 16 * 4, st));
+    PRGPU_CUDA(cudaMemsetAsync(sp->col_cold.p + sp->e_cold, 0, 16 * 4, st));
+    if (hub) {
+        split_rows_block<true><<<hub, 256, 0, st>>>(g->row_off.p, g->col.p, hot, nullptr, sp->off_hot.p,
+                                                    sp->off_cold.p, sp->col_hot.p, sp->col_cold.p);
+        PRGPU_LAUNCHED("split_rows_block");
+    }
+    if (wgrid) {
+        split_rows_warp<true><<<wgrid, kThreads, 0, st>>>(g->row_off.p, g->col.p, hub, rows, hot, nullptr,
+                                                          sp->off_hot.p, sp->off_cold.p, sp->col_hot.p,
+                                                          sp->col_cold.p);
+        PRGPU_LAUNCHED("split_rows_warp");
+    }
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    return *(g->splits[hot] = std::move(sp));
+}
+
 std::unique_ptr<prgpu_graph> graph_generate_rmat(uint32_t scale, uint32_t ef, double a, double b,
                                                  double c, uint64_t seed, int device,
                                                  cudaStream_t st) {

@@ -117,6 +117,11 @@ struct Params {
     uint32_t hot_src;            // sources [0, hot_src) in the L2-resident region
     uint32_t l2mode;             // 0 evict hints, 2 no hints (streams); >= 3 contribution-write hints
     uint32_t pf;                 // L2 prefetch of upcoming gathers: 0 off, 1 on (PRGPU_PF)
+    // split pull (SourceSplit): 1 = hot pass (row_off/col are the hot CSR;
+    // each row's sum goes to hp, no epilogue), 2 = cold pass (the row's hot
+    // partial hp + the cold sum, then the epilogue), 0 = one pass
+    int split;
+    double* hp;                  // [nonempty rows][ks] hot partial sums
     uint32_t gpol;               // gather L2 policy (tuning): 0 plain; 1 hot evict_last / cold
                                  // evict_first; 2 hot normal / cold evict_first; 3 hot evict_last / cold normal
     uint32_t skip_mask;          // profiling only (PRGPU_SKIP): 1 chunk, 2 packed, 4 empty tasks,
@@ -456,8 +461,20 @@ struct Warp {
         }
     }
 
+    // split pull, hot pass: the row's hot-source sum is kept for the cold pass
+    __device__ __forceinline__ void store_hot(uint32_t v, int sl, const double (&acc)[W]) {
+        if (!lane_ok(sl)) return;
+        double* h = P.hp + (size_t)v * P.ks + sl * W;
+#pragma unroll
+        for (int w = 0; w < W; ++w) __stcs(h + w, acc[w]);
+    }
+
     // fused epilogue for row v, lanes [sl*W, sl*W + W)
     __device__ __forceinline__ void epilogue(uint32_t v, int sl, const double (&acc)[W]) {
+        if (P.split == 1) {
+            store_hot(v, sl, acc);
+            return;
+        }
         const uint2 ri = ld_stream_u2(P.rowinfo + v, stream_policy(P));
         epilogue_with<true>(v, sl, acc, ri, acc);
     }
@@ -466,8 +483,20 @@ struct Warp {
     // Ranks are row-major [row][KS]: a lane group reads and writes one
     // contiguous row (3 sectors at K = 11) instead of K scattered words.
     template <bool LOAD_PREV = false>
-    __device__ __forceinline__ void epilogue_with(uint32_t v, int sl, const double (&acc)[W], uint2 ri,
+    __device__ __forceinline__ void epilogue_with(uint32_t v, int sl, const double (&acc_in)[W], uint2 ri,
                                                   const double (&o_in)[W]) {
+        if (P.split == 1) {
+            store_hot(v, sl, acc_in);
+            return;
+        }
+        double acc[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc[w] = acc_in[w];
+        if (P.split == 2 && lane_ok(sl)) { // hot partial first, then the cold sum (a fixed order)
+            const double* h = P.hp + (size_t)v * P.ks + sl * W;
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[w] = __dadd_rn(__ldcs(h + w), acc[w]);
+        }
         const uint32_t d = ri.x;
         double o[W];
         if constexpr (LOAD_PREV) {
@@ -915,6 +944,7 @@ struct Warp {
     // ---- rows with no in-edges: rank = c0; write c0/d for rows with out-edges,
     //      and (sweep mode) the L1 distance to the reference -------------------------
     __device__ void empty_task(uint32_t t) {
+        if (P.split == 1) return; // no in-edges: nothing for the hot pass
         const uint64_t sp = stream_policy(P);
         const uint32_t base = P.empty_begin + t * P.er;
         const uint32_t end = min(base + P.er, P.n);
@@ -1073,6 +1103,8 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
             }
         }
     }
+
+    if (P.split == 1) return; // hot pass: row sums only, no partials
 
     // ---- CTA partials, fixed order ------------------------------------------------
 #pragma unroll

@@ -612,3 +612,37 @@ def test_series_sweep_c2_golden(prl):
         assert np.max(np.abs(r.ranks[idx] - arr[f"lane{k}_sample"])) <= RANK_TOL
         assert np.max(np.abs(r.ranks[arr[f"lane{k}_top_idx"]] - arr[f"lane{k}_top"])) <= RANK_TOL
         assert abs(float(np.sum(r.ranks.astype(np.longdouble))) - float(arr[f"lane{k}_total"])) <= 1e-9
+
+
+@pytest.mark.parametrize("split_mb", ["1", "4"])
+def test_split_pull_matches_oracle(prl, oracle, monkeypatch, split_mb):
+    """The split pull (PRGPU_SPLIT_MB: hot-source CSR pass, then cold-source
+    pass adding the hot partial) against the oracle: exact iterations, ranks
+    within 1e-10, for one and several lanes and every norm; and against the
+    one-pass run (same iterations, ranks to rounding)."""
+    n, pairs = oracle.rmat(17, 16, 0.57, 0.19, 0.19, 2108)
+    h = oracle.build_csr_handle(n, pairs)
+    g = prl.build_csr(edge_list(prl, n, pairs))
+    try:
+        one = prl.pagerank_batched(g, [0.95, 0.85, 0.6], 1e-9, prl.NormKind.L2, 300)
+        monkeypatch.setenv("PRGPU_SPLIT_MB", split_mb)
+        for norm in ("l1", "l2", "linf"):
+            want = oracle.pagerank(h, 0.85, 1e-9, norm, 300)
+            got = prl.pagerank(g, prl.PageRankConfig(0.85, 1e-9, nk(prl, norm), 300))
+            assert got.iterations == want["iterations"], norm
+            assert np.max(np.abs(got.ranks - want["ranks"])) <= RANK_TOL, norm
+        two = prl.pagerank_batched(g, [0.95, 0.85, 0.6], 1e-9, prl.NormKind.L2, 300)
+        for a, b, alpha in zip(one.results, two.results, (0.95, 0.85, 0.6)):
+            assert a.iterations == b.iterations
+            assert np.max(np.abs(a.ranks - b.ranks)) <= 1e-15
+            want = oracle.pagerank(h, alpha, 1e-9, "l2", 300)
+            assert b.iterations == want["iterations"]
+            assert np.max(np.abs(b.ranks - want["ranks"])) <= RANK_TOL
+        eleven = [0.5 + 0.05 * i for i in range(11)]
+        w = prl.pagerank_batched(g, eleven, 1e-6, prl.NormKind.L1, 300)
+        monkeypatch.delenv("PRGPU_SPLIT_MB")
+        u = prl.pagerank_batched(g, eleven, 1e-6, prl.NormKind.L1, 300)
+        for a, b in zip(w.results, u.results):
+            assert a.iterations == b.iterations and np.max(np.abs(a.ranks - b.ranks)) <= 1e-15
+    finally:
+        oracle.free_csr(h)
