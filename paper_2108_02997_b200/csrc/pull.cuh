@@ -692,7 +692,8 @@ struct Warp {
         const uint32_t first = P.chunk_first[row];
         const uint32_t nch = P.chunk_first[row + 1] - first;
         const uint64_t rlo = ld_stream_u64(P.row_off + row, sp), rhi = ld_stream_u64(P.row_off + row + 1, sp);
-        const uint64_t lo = rlo + (uint64_t)(t - first) * P.chunk;
+        // (a split pass's part of the row can end before this chunk: empty range)
+        const uint64_t lo = min(rlo + (uint64_t)(t - first) * P.chunk, rhi);
         const uint64_t hi = min(lo + P.chunk, rhi);
         double acc[W];
 #pragma unroll
