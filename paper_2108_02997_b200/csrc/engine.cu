@@ -180,35 +180,67 @@ __global__ void packed_bounds(const uint64_t* __restrict__ excl, uint32_t lo, ui
 }
 
 // ---- deterministic device error_norm (norms.hpp:48-78) ------------------------------
+// The reference accumulates L1 and L2 in x87 long double (64-bit mantissa,
+// norms.hpp:57-69).  The device has no long double: sums are carried as
+// double-double pairs (error-free TwoSum; the L2 square split exactly by an
+// FMA), i.e. more precise than the reference, so the result is the
+// reference's rounded to double, up to the reference's own rounding.
+struct DD {
+    double hi, lo;
+};
+__device__ __forceinline__ DD dd_add(DD a, double b) {
+    const double s = a.hi + b, bb = s - a.hi;
+    const double e = (a.hi - (s - bb)) + (b - bb);
+    const double lo = a.lo + e;
+    const double hi = s + lo;
+    return DD{hi, lo - (hi - s)};
+}
+__device__ __forceinline__ DD dd_add(DD a, DD b) { return dd_add(dd_add(a, b.hi), b.lo); }
+
 __global__ void norm_partials(int kind, const double* __restrict__ r, const double* __restrict__ s,
                               uint64_t n, double* __restrict__ out) {
-    __shared__ double red[kNT / 32];
-    double v = 0.0;
+    __shared__ DD red[kNT / 32];
+    DD v{0.0, 0.0};
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const double d = r[i] - s[i];
-        if (kind == 0) v += fabs(d);
-        else if (kind == 1) v += d * d;
-        else v = fmax(v, fabs(d));
+        const double d = r[i] - s[i]; // double difference, as the reference
+        if (kind == 0) v = dd_add(v, fabs(d));
+        else if (kind == 1) {
+            const double sq = d * d;
+            v = dd_add(dd_add(v, sq), fma(d, d, -sq)); // d^2 exactly
+        } else v.hi = fmax(v.hi, fabs(d));
     }
     for (int off = 16; off > 0; off >>= 1) {
-        const double o = __shfl_xor_sync(0xffffffffu, v, off);
-        v = kind == 2 ? fmax(v, o) : v + o;
+        const DD o{__shfl_xor_sync(0xffffffffu, v.hi, off), __shfl_xor_sync(0xffffffffu, v.lo, off)};
+        if (kind == 2) v.hi = fmax(v.hi, o.hi);
+        else v = dd_add(v, o);
     }
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
     __syncthreads();
     if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < kNT / 32; ++w) t = kind == 2 ? fmax(t, red[w]) : t + red[w];
-        out[blockIdx.x] = t;
+        DD t{0.0, 0.0};
+        for (int w = 0; w < kNT / 32; ++w) {
+            if (kind == 2) t.hi = fmax(t.hi, red[w].hi);
+            else t = dd_add(t, red[w]);
+        }
+        out[2 * blockIdx.x] = t.hi;
+        out[2 * blockIdx.x + 1] = t.lo;
     }
 }
 
 __global__ void norm_final(int kind, const double* __restrict__ parts, int nparts, double* out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double t = 0.0;
-    for (int i = 0; i < nparts; ++i) t = kind == 2 ? fmax(t, parts[i]) : t + parts[i];
-    out[0] = kind == 1 ? sqrt(t) : t;
+    DD t{0.0, 0.0};
+    for (int i = 0; i < nparts; ++i) {
+        if (kind == 2) t.hi = fmax(t.hi, parts[2 * i]);
+        else t = dd_add(t, DD{parts[2 * i], parts[2 * i + 1]});
+    }
+    if (kind == 1) { // sqrt of the double-double sum, one Newton correction
+        const double q = sqrt(t.hi);
+        out[0] = q > 0.0 ? q + (fma(-q, q, t.hi) + t.lo) / (2.0 * q) : q;
+    } else {
+        out[0] = t.hi + t.lo;
+    }
 }
 
 // ============================================================================
@@ -983,7 +1015,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     // no finalize) ahead of the cold original.  PRGPU_SPLIT_MB = the hot
     // table's size in the run's widest rows (0: one pass).
     const uint32_t split_hot = [&]() -> uint32_t {
-        if (nranks >= 1) return 0;
+        if (!kExp || nranks >= 1) return 0;
         const char* sm = std::getenv("PRGPU_SPLIT_MB");
         const uint64_t mb = sm ? (uint64_t)std::atoll(sm) : 0;
         if (!mb) return 0;
@@ -1999,7 +2031,7 @@ double session_time_pull(prgpu_session* s, int launches) {
     // access-policy window over the first X MB of the parity this iteration
     // gathers from (the hottest sources, ids in degree order)
     const char* pmb = std::getenv("PRGPU_PERSIST_MB");
-    const size_t persist_b = pmb ? ((size_t)std::atoi(pmb) << 20) : 0;
+    const size_t persist_b = (kExp && pmb) ? ((size_t)std::atoi(pmb) << 20) : 0;
     if (persist_b) {
         int maxp = 0;
         PRGPU_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, s->g->device));
@@ -2056,7 +2088,7 @@ double error_norm_device(int kind, const double* r, const double* s, uint64_t n,
     if (n == 0) fail(PRGPU_EINVAL, "error_norm: empty vectors");
     DeviceGuard dg(device);
     Stream st;
-    DevBuf<double> dr(n), ds(n), parts(296), out(1);
+    DevBuf<double> dr(n), ds(n), parts(2 * 296), out(1);
     PRGPU_CUDA(cudaMemcpyAsync(dr.p, r, n * 8, cudaMemcpyHostToDevice, st));
     PRGPU_CUDA(cudaMemcpyAsync(ds.p, s, n * 8, cudaMemcpyHostToDevice, st));
     const int blocks = (int)std::min<uint64_t>(296, (n + kNT - 1) / kNT);

@@ -59,6 +59,17 @@ constexpr bool kBcast = false; // tuning builds only
 #else
 constexpr bool kBcast = true;
 #endif
+// Tuning experiments compiled in only with -DPRGPU_EXPERIMENTS (make
+// EXPERIMENTS=1 -> build_alt/libprgpu_exp.so): gather L2 policies
+// (Params::gpol), L2 prefetch (pf) and the split pull (split).  All measured
+// slower or no better on B200 (profiles/r2_c5_l2_experiments.md); their
+// runtime branches alone cost 4-36 % in the hot loops, so the default build
+// compiles them out.
+#ifdef PRGPU_EXPERIMENTS
+constexpr bool kExp = true;
+#else
+constexpr bool kExp = false;
+#endif
 constexpr int kNQ = 5;
 constexpr int kPackOff = 40; // staged row offsets per packed run (>= rows per run + 1) // partials: L1, L2^2, Linf, dangling sum, L1-vs-ref
 
@@ -392,7 +403,7 @@ struct Warp {
           rn(p.rank[parity ^ 1]), cpl(p.cbase + p.cold_off[parity] * KS + (ln % LG) * W), s_alpha(a),
           s_c0(c0), s_active(act) {
         part.init(smem_cols, tid);
-        if (p.gpol) {
+        if (kExp && p.gpol) {
             pol_hot = (p.gpol == 2) ? policy_evict_normal() : policy_evict_last();
             pol_cold = (p.gpol == 3) ? policy_evict_normal() : policy_evict_first();
         }
@@ -409,7 +420,9 @@ struct Warp {
     // one source's contribution row slice (the gather of pagerank.hpp:91)
     __device__ __forceinline__ void gather(uint32_t src, double (&v)[W]) const {
         const double* a = cpl + (size_t)src * KS;
-        if (P.gpol == 4 || P.gpol == 5) { // cold rows streamed (.cs / L1 no-allocate + evict_first)
+        if (!kExp) {
+            load_w<W>(a, v);
+        } else if (P.gpol == 4 || P.gpol == 5) { // cold rows streamed (.cs / L1 no-allocate + evict_first)
             if (src < P.hot_src) load_w<W>(a, v);
             else if (P.gpol == 4) {
 #pragma unroll
@@ -471,7 +484,7 @@ struct Warp {
 
     // fused epilogue for row v, lanes [sl*W, sl*W + W)
     __device__ __forceinline__ void epilogue(uint32_t v, int sl, const double (&acc)[W]) {
-        if (P.split == 1) {
+        if (kExp && P.split == 1) {
             store_hot(v, sl, acc);
             return;
         }
@@ -485,14 +498,14 @@ struct Warp {
     template <bool LOAD_PREV = false>
     __device__ __forceinline__ void epilogue_with(uint32_t v, int sl, const double (&acc_in)[W], uint2 ri,
                                                   const double (&o_in)[W]) {
-        if (P.split == 1) {
+        if (kExp && P.split == 1) {
             store_hot(v, sl, acc_in);
             return;
         }
         double acc[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) acc[w] = acc_in[w];
-        if (P.split == 2 && lane_ok(sl)) { // hot partial first, then the cold sum (a fixed order)
+        if (kExp && P.split == 2 && lane_ok(sl)) { // hot partial first, then the cold sum (a fixed order)
             const double* h = P.hp + (size_t)v * P.ks + sl * W;
 #pragma unroll
             for (int w = 0; w < W; ++w) acc[w] = __dadd_rn(__ldcs(h + w), acc[w]);
@@ -624,7 +637,7 @@ struct Warp {
         // block b+1 are prefetched into L2 before block b is gathered, so
         // gathers mostly hit L2 (the kernel is DRAM-latency bound: this
         // raises the rows in flight per warp without holding registers)
-        const bool pf = P.pf != 0; // warp-uniform (every lane holds colidx for the shuffles)
+        const bool pf = kExp && P.pf != 0; // warp-uniform (every lane holds colidx for the shuffles)
         auto ld_block = [&](uint32_t base, uint32_t (&c)[4]) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -875,7 +888,7 @@ struct Warp {
         const uint32_t ne_all = (uint32_t)(s_off[R] - e0);
         for (uint32_t x = lane; x < ne_all; x += 32) s_col[x] = ld_stream_u32(P.col + e0 + x, sp);
         __syncwarp();
-        if (P.pf) // every row of the run in flight to L2 at once (the walk below is one row per slot)
+        if (kExp && P.pf) // every row of the run in flight to L2 at once (the walk below is one row per slot)
             for (uint32_t x = lane; x < ne_all; x += 32) prefetch_row(s_col[x]);
         uint32_t i = slot;
         if (i < R) {
@@ -945,7 +958,7 @@ struct Warp {
     // ---- rows with no in-edges: rank = c0; write c0/d for rows with out-edges,
     //      and (sweep mode) the L1 distance to the reference -------------------------
     __device__ void empty_task(uint32_t t) {
-        if (P.split == 1) return; // no in-edges: nothing for the hot pass
+        if (kExp && P.split == 1) return; // no in-edges: nothing for the hot pass
         const uint64_t sp = stream_policy(P);
         const uint32_t base = P.empty_begin + t * P.er;
         const uint32_t end = min(base + P.er, P.n);
@@ -1105,7 +1118,7 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
         }
     }
 
-    if (P.split == 1) return; // hot pass: row sums only, no partials
+    if (kExp && P.split == 1) return; // hot pass: row sums only, no partials
 
     // ---- CTA partials, fixed order ------------------------------------------------
 #pragma unroll

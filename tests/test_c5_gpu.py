@@ -117,8 +117,12 @@ def test_c5_rmat28_k3_against_reference_run(prl):
             t = min(res.iterations, lane["iterations"])
             assert abs(res.iterations - lane["iterations"]) == 1 and abs(tr[t - 1] - TOL) <= 1e-3 * TOL, k
         n_it = min(res.iterations, lane["iterations"])
+        # the L2 norm of the change is the sensitive quantity: late in the run
+        # each rank moves by ~1e-10 while the GPU and reference iterates differ
+        # by ~1e-18 (the dangling sum's order), so the traces agree to ~1e-7
+        # relative (measured 1.4e-7); the crossings keep a >= 14 % margin to tau
         got_tr = run.trace[:n_it, k, 1]  # L2 column
-        assert np.allclose(got_tr, tr[:n_it], rtol=1e-9, atol=0), (k, got_tr, tr[:n_it])
+        assert np.allclose(got_tr, tr[:n_it], rtol=1e-6, atol=0), (k, got_tr, tr[:n_it])
         r = res.ranks
         assert float(np.max(np.abs(r[idx] - arr[f"lane{k}_sample"]))) <= 1e-10
         ti = arr[f"lane{k}_top_idx"]

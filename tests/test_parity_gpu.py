@@ -614,6 +614,11 @@ def test_series_sweep_c2_golden(prl):
         assert abs(float(np.sum(r.ranks.astype(np.longdouble))) - float(arr[f"lane{k}_total"])) <= 1e-9
 
 
+EXP_LIB = "libprgpu_exp.so"  # make -C paper_2108_02997_b200/csrc EXPERIMENTS=1
+
+
+@pytest.mark.skipif(not os.environ.get("PRGPU_LIB", "").endswith(EXP_LIB),
+                    reason="the split pull is compiled into the tuning build only (tests/test_experiments_gpu.py)")
 @pytest.mark.parametrize("split_mb", ["1", "4"])
 def test_split_pull_matches_oracle(prl, oracle, monkeypatch, split_mb):
     """The split pull (PRGPU_SPLIT_MB: hot-source CSR pass, then cold-source
@@ -646,3 +651,22 @@ def test_split_pull_matches_oracle(prl, oracle, monkeypatch, split_mb):
             assert a.iterations == b.iterations and np.max(np.abs(a.ranks - b.ranks)) <= 1e-15
     finally:
         oracle.free_csr(h)
+
+
+def test_error_norm_device_vs_reference_long_double(prl, ref):
+    """prgpu_error_norm carries L1 / L2 sums as double-double (the reference
+    accumulates in x87 long double, norms.hpp:57-69): equal to the
+    reference's result to within one double ulp on rank-like vectors of
+    1e3..4e6 entries (the reference's own long-double rounding), Linf exactly."""
+    rs = np.random.default_rng(2021)
+    for n in (1000, 100_000, 4_000_000):
+        r = rs.random(n) / n
+        s = r + (rs.random(n) - 0.5) * 1e-7 / n
+        s[rs.integers(0, n, 10)] += 1e-3 / n  # a few outliers
+        for norm, kind in (("l1", prl.NormKind.L1), ("l2", prl.NormKind.L2), ("linf", prl.NormKind.LInf)):
+            want = ref.error_norm(norm, r, s)
+            got = prl.error_norm(kind, r, s)
+            if norm == "linf":
+                assert got == want
+            else:
+                assert abs(got - want) <= np.spacing(want), (n, norm, got, want)
