@@ -259,8 +259,8 @@ def run_distributed(g: CsrGraph, alphas: Sequence[float], tolerance=1e-6,
     """One rank of an N-GPU run (torch.distributed initialised with NCCL,
     one process per GPU).
 
-    exchange="nccl": contribution rows of rank r travel by a broadcast from r,
-    the partial vectors by an all-gather, between host-enqueued pull and
+    exchange="nccl": one all-gather per iteration of every rank's new
+    contribution rows and partial-sum vector, between host-enqueued pull and
     finalize kernels.  exchange="peer": the fused path — the ranks map each
     other's buffers (CUDA IPC), the pull kernel stores every contribution row
     and the partials straight into all peers over NVLink and the finalize
@@ -421,7 +421,17 @@ def _run_distributed_on(g, alphas, tolerance, norm, max_iterations, stop_mask, w
     part = _Part(g, alphas, tolerance, norm, max_iterations, stop_mask, rank, world, g.device)
     part.set_stream()
     part.init()
-    mine = torch.empty(part.ppr, dtype=torch.float64, device=part.contrib.device)
+    dev = part.contrib.device
+    # ONE all-gather per iteration: each rank's row of the exchange buffer is
+    # its new contribution rows (its source range, padded to the longest
+    # range) followed by its partial-sum vector; every rank then copies the
+    # peers' rows into place on the device
+    lens = [(q.src_end - q.src_begin) * part.stride for q in part.parts]
+    span = max(lens) if lens else 0
+    row = span + part.ppr
+    on_host = dist.get_backend() == "gloo"
+    send = torch.zeros(row, dtype=torch.float64, device=dev)
+    recv = torch.zeros(world * row, dtype=torch.float64, device=dev)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()
     start.record()
@@ -433,10 +443,19 @@ def _run_distributed_on(g, alphas, tolerance, norm, max_iterations, stop_mask, w
     while its < max_iterations:
         par = part.step()
         if world > 1:
+            send[:lens[rank]].copy_(part.chunk(par, rank))
+            send[span:].copy_(part.slot[rank])
+            if on_host:  # gloo (processes sharing a GPU in the tests): the collective on host copies
+                hr = recv.new_empty(recv.shape, device="cpu")
+                dist.all_gather_into_tensor(hr, send.cpu())
+                recv.copy_(hr)
+            else:
+                dist.all_gather_into_tensor(recv, send)
             for r in range(world):
-                dist.broadcast(part.chunk(par, r), src=r)
-            mine.copy_(part.slot[rank])
-            dist.all_gather_into_tensor(part.partials, mine)
+                if r != rank:
+                    base = r * row
+                    part.chunk(par, r).copy_(recv[base:base + lens[r]])
+                    part.slot[r].copy_(recv[base + span:base + row])
         part.finalize()
         its += 1
         if its % WINDOW == 0 and not part.active():
@@ -476,7 +495,12 @@ def _gather_ranks(part: _Part, g: CsrGraph, K: int, world: int) -> np.ndarray:
     check(lib().prgpu_part_local_ranks_device(part._s, C.c_void_p(local.data_ptr()), ld), "local ranks")
     if world > 1:
         gathered = torch.empty((world, K, ld), dtype=torch.float64, device=dev)
-        dist.all_gather_into_tensor(gathered, local)
+        if dist.get_backend() == "gloo":
+            hg = torch.empty((world, K, ld), dtype=torch.float64)
+            dist.all_gather_into_tensor(hg, local.cpu())
+            gathered.copy_(hg)
+        else:
+            dist.all_gather_into_tensor(gathered, local)
     else:
         gathered = local.unsqueeze(0)
     eng = torch.cat([gathered[r, :, :rows[r]] for r in range(world)], dim=1)  # [K][n], engine rows

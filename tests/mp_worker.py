@@ -15,6 +15,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     out, scale, alphas = sys.argv[1], int(sys.argv[2]), [float(a) for a in sys.argv[3].split(",")]
+    exchange = sys.argv[4] if len(sys.argv) > 4 else "peer-host"
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(0)
@@ -23,7 +24,7 @@ def main():
     from paper_2108_02997_b200 import distributed
     g = prl.generate_rmat(scale, 16, 0.57, 0.19, 0.19, 2108, device=0)
     r = distributed.run_distributed(g, alphas, 1e-9, prl.NormKind.L1, 200, want_ranks=True,
-                                    exchange="peer-host")
+                                    exchange=exchange)
     np.savez(out, ranks=r.ranks, iterations=r.iterations, sent=r.sent_bytes)
     dist.barrier()
     dist.destroy_process_group()
