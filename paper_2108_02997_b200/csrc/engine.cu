@@ -257,9 +257,14 @@ struct LaneCfg {
     int paths = 3;          // task kinds compiled in (pull_kernel PATHS)
     int KP() const { return LG * W; }
     size_t smem() const {
+        const bool async = paths == 1 && kAsyncHub && LG > 1 && (KS == 2 || KS == 4); // pull.cuh async_hub
         const size_t staged = KP() == 1 ? (size_t)kWarps * 2 * WIN * sizeof(double) // STAGED
-                              : paths == 2 ? (size_t)kWarps * (kPackOff + (2 * WIN + 8) / 2) * sizeof(double)
-                                           : 0; // packed_pipe stage
+                              : paths == 2 ? (size_t)kWarps *
+                                                 ((kStagedWide && LG == 4 && KS == 4) ? 2 * WIN * KS
+                                                                                     : kPackOff + (2 * WIN + 8) / 2) *
+                                                 sizeof(double)
+                              : async      ? (size_t)kWarps * 2 * kAsyncBlock * KS * sizeof(double)
+                                           : 0; // packed_pipe stage / cp.async ring
         const bool smemp = W >= 6 || (paths != 3 && KP() > 1);
         const size_t cols = smemp ? (size_t)popc_c(QM) * W * kNT * sizeof(double) : 0;     // Partials
         return staged + cols;

@@ -260,6 +260,38 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
+// L2-only 16-byte copies (rows gathered once per iteration: no L1 allocation)
+__device__ __forceinline__ void cp_async16_cg(void* smem, const void* g) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Hub chunks of the 2- and 4-lane instances (16- and 32-byte contribution
+// rows) gather through shared memory with cp.async instead of registers:
+// per warp a ring of two 128-edge blocks, the next block's rows in flight
+// while the current one is summed (8x the rows in flight per warp of the
+// register path, which the hub kernel's DRAM-latency stalls call for).  The
+// summation order is the register path's, so results are bit-identical.
+// Measured slower on C5 (hub kernel 36.6 -> 46.1 ms: the 74 KB ring halves the
+// resident warps and the 16-byte halves of a row are two L2 requests; DRAM
+// bytes 186 -> 208 GB): tuning build only.
+#ifndef PRGPU_ASYNC_HUB
+#define PRGPU_ASYNC_HUB 1
+#endif
+constexpr bool kAsyncHub = kExp && PRGPU_ASYNC_HUB != 0;
+// Packed runs of the 4-lane instance staged in shared memory like K = 1
+// (every gather of the run in flight, then per-row sums in edge order)
+// instead of one lane group walking each row (packed_pipe).  Tuning switch.
+#ifndef PRGPU_STAGED_WIDE
+#define PRGPU_STAGED_WIDE 0
+#endif
+constexpr bool kStagedWide = PRGPU_STAGED_WIDE != 0;
+constexpr int kAsyncBlock = 128; // edges per ring block
+template <int LG, int KS>
+constexpr bool async_hub() { return kAsyncHub && LG > 1 && (KS == 2 || KS == 4); }
 
 // gathers: plain read-only loads (measured: L2 residency hints on the
 // contributions did not pay, and the policy/address arithmetic per edge did)
@@ -691,6 +723,64 @@ struct Warp {
         }
     }
 
+    // cp.async ring (async_hub): see kAsyncHub.  `stage` = this warp's
+    // 2 * kAsyncBlock * KS doubles.
+    __device__ __forceinline__ void accumulate_async(uint64_t lo, uint64_t hi, double (&acc)[W],
+                                                     double* __restrict__ stage) const {
+        const uint64_t sp = stream_policy(P);
+        const uint32_t ne = (uint32_t)(hi - lo);
+        const uint32_t* __restrict__ cb = P.col + lo;
+        const bool ok = slice_live();
+        constexpr int NP = KS / 2; // 16-byte pieces per row
+        constexpr uint32_t B = kAsyncBlock;
+        const double* __restrict__ ctab = P.cbase + P.cold_off[par] * KS;
+        auto ld_block = [&](uint32_t base, uint32_t (&c)[4]) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t e = base + lane + 32u * j;
+                c[j] = e < ne ? ld_stream_u32(cb + e, sp) : 0u;
+            }
+        };
+        auto issue = [&](uint32_t base, const uint32_t (&c)[4], uint32_t ring) {
+            double* dst = stage + (size_t)ring * B * KS;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t i = lane + 32u * j;
+                if (base + i < ne) {
+                    const double* src = ctab + (size_t)c[j] * KS;
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) cp_async16_cg(dst + (size_t)i * KS + 2 * q, src + 2 * q);
+                }
+            }
+            cp_async_commit();
+        };
+        const uint32_t nb = (ne + B - 1) / B;
+        uint32_t cn[4];
+        {
+            uint32_t c0[4];
+            ld_block(0, c0);
+            if (nb > 1) ld_block(B, cn);
+            issue(0, c0, 0);
+        }
+        for (uint32_t b = 0; b < nb; ++b) {
+            if (b + 1 < nb) issue((b + 1) * B, cn, (b + 1) & 1);
+            else cp_async_commit(); // an empty group keeps the wait count uniform
+            if (b + 2 < nb) ld_block((b + 2) * B, cn);
+            cp_async_wait<1>(); // block b has landed (block b+1 may be in flight)
+            __syncwarp();
+            if (ok) {
+                const double* blk = stage + (size_t)(b & 1) * B * KS + slice * W;
+                const uint32_t cnt = min(B, ne - b * B);
+                // slot s sums edges s, s+ES, ... in order: accumulate_bcast's order
+                for (uint32_t i = slot; i < cnt; i += ES)
+#pragma unroll
+                    for (int w = 0; w < W; ++w) acc[w] += blk[(size_t)i * KS + w];
+            }
+            __syncwarp(); // the ring slot is refilled next iteration
+        }
+        cp_async_wait<0>();
+    }
+
     __device__ __forceinline__ void reduce_slots(double (&acc)[W]) const {
 #pragma unroll
         for (int off = LG; off < 32; off <<= 1)
@@ -699,7 +789,7 @@ struct Warp {
     }
 
     // ---- chunk of a long (hub) row ------------------------------------------------
-    __device__ void chunk_task(uint32_t t) {
+    __device__ void chunk_task(uint32_t t, double* __restrict__ stage = nullptr) {
         const uint64_t sp = stream_policy(P);
         const uint32_t row = P.chunk_row[t];
         const uint32_t first = P.chunk_first[row];
@@ -711,7 +801,10 @@ struct Warp {
         double acc[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) acc[w] = 0.0;
-        if constexpr (LG > 1 && kBcast) accumulate_bcast(lo, hi, acc);
+        if constexpr (async_hub<LG, KS>()) {
+            if (stage) accumulate_async(lo, hi, acc, stage);
+            else accumulate_bcast(lo, hi, acc);
+        } else if constexpr (LG > 1 && kBcast) accumulate_bcast(lo, hi, acc);
         else accumulate(lo, hi, acc);
         reduce_slots(acc);
         if (nch == 1) { // the whole row was this chunk: no hand-off needed
@@ -1088,8 +1181,12 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     // dynamic smem: [kWarps][SMEM_WARP + ASYNC_WARP] staged gathers, then the per-thread
     // partial columns when W >= 6
     // K > 1 packed runs (PATHS == 2): staged row offsets + colidx, in doubles
-    constexpr int PACK_WARP = (PATHS == 2 && !C::STAGED) ? kPackOff + (2 * WIN + 8) / 2 : 0;
-    constexpr int PER_WARP = C::SMEM_WARP + PACK_WARP;
+    constexpr bool WSTAGE = (PATHS == 2) && kStagedWide && LG == 4 && C::KS == 4 && !C::STAGED;
+    constexpr int PACK_WARP = (PATHS == 2 && !C::STAGED) ? (WSTAGE ? C::EMAX * C::KS : kPackOff + (2 * WIN + 8) / 2) : 0;
+    // hub-chunk instances of 2/4 lanes: the cp.async ring (kAsyncHub)
+    constexpr bool ASYNC = (PATHS == 1) && async_hub<LG, C::KS>();
+    constexpr int ASYNC_WARP = ASYNC ? 2 * kAsyncBlock * C::KS : 0;
+    constexpr int PER_WARP = C::SMEM_WARP + PACK_WARP + ASYNC_WARP;
     // the instances of a split iteration keep their partials in shared
     // memory: the registers go to gathers in flight
     constexpr bool SMEMP = (W >= 6) || (PATHS != 3 && C::KP > 1);
@@ -1104,11 +1201,11 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
         const uint32_t t = listed ? __ldg(P.task_list + i) : i;
         if (t < T1) {
             if constexpr ((PATHS & 1) != 0)
-                if (!(P.skip_mask & 1)) w.chunk_task(t);
+                if (!(P.skip_mask & 1)) w.chunk_task(t, ASYNC ? sv : nullptr);
         } else if constexpr ((PATHS & 2) != 0) {
             if (t < T2) {
                 if (!(P.skip_mask & 2)) {
-                    if constexpr (C::STAGED) w.packed_task(t - T1, sv);
+                    if constexpr (C::STAGED || WSTAGE) w.packed_task(t - T1, sv);
                     else if constexpr (PATHS == 2) w.packed_pipe(t - T1, sv);
                     else w.packed_direct(t - T1);
                 }
