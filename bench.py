@@ -537,7 +537,9 @@ def run_partitioned(args, cfg):
     torch.cuda.set_device(local)
     tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if cfg["kind"] == "rmat":
-        g = prl.generate_rmat(cfg["scale"], 16, 0.57, 0.19, 0.19, SEED, device=local)
+        # --shard: each rank builds only its rows' in-edges (SURVEY 8e set-up)
+        g = prl.generate_rmat(cfg["scale"], 16, 0.57, 0.19, 0.19, SEED, device=local,
+                              shard=(rank, world) if args.shard else None)
     else:
         g = prl.generate_grid(cfg["side"], 0.6, 0.01, SEED, device=local)
     n, e = g.vertex_count, g.edge_count()
@@ -589,7 +591,7 @@ def run_partitioned(args, cfg):
     # CSR from pinned host memory, runs the partitioned solve, the ranks are
     # gathered to the host (distributed.run_distributed(want_ranks=True))
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.shard:  # (a shard holds one rank's edges: no host CSR to upload)
         import ctypes as C
         from paper_2108_02997_b200 import _lib
         off = torch.from_numpy(g.in_offsets).pin_memory()
@@ -635,7 +637,8 @@ def run_partitioned(args, cfg):
                            "fused peer-memory exchange (NVLink stores from the pull kernel, CUDA graph loop)"
                            if args.exchange == "peer" else "NCCL exchange per iteration"),
                        "timed_scope": "iteration loop incl. exchange, CUDA events, max over ranks",
-                       "exchange_fallback": fallback, "wall_s": wall},
+                       "exchange_fallback": fallback, "wall_s": wall,
+                       "graph": "per-rank shards (own rows' in-edges)" if args.shard else "whole graph per rank"},
             "gpu_launches": args.steps * r.run_iterations * 2,
             "clocks": clk.summary(),
             "roofline": roof,
@@ -777,6 +780,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="N>1 partitioned solve: fused peer-memory exchange (default) or NCCL calls")
+    ap.add_argument("--shard", action="store_true",
+                    help="N>1 partitioned solve: each rank builds only its rows' in-edges (RMAT configs)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas (weak scaling) instead of the 1D partition")
     args = ap.parse_args()

@@ -84,6 +84,24 @@ PRGPU_API int prgpu_graph_generate_rmat(uint32_t scale, uint32_t edge_factor, do
                               uint64_t seed, int device, prgpu_graph** out);
 PRGPU_API int prgpu_graph_generate_grid(uint32_t side, double p, double longrange_frac, uint64_t seed,
                               int device, prgpu_graph** out);
+/* Rank `rank`'s shard of the same RMAT graph for an `nranks`-rank partition
+ * (SURVEY 8e set-up), built without ever holding the whole edge list: every
+ * rank generates all edges slab by slab, computes the exact global in- and
+ * out-degrees (so the relabelled vertex arrays equal the whole graph's) and
+ * keeps the in-edges of its contiguous range of engine rows only (cost-
+ * balanced; prgpu_graph_shard_info).  Only prgpu_part_create(rank, nranks)
+ * sessions run on it (contiguous rows, every contribution row stored into
+ * every peer); downloading its edges is EINVAL. */
+PRGPU_API int prgpu_graph_generate_rmat_shard(uint32_t scale, uint32_t edge_factor, double a, double b,
+                                              double c, uint64_t seed, int rank, int nranks, int device,
+                                              prgpu_graph** out);
+/* Device memory held by a graph and/or a session (either may be NULL). */
+PRGPU_API int prgpu_device_bytes(const prgpu_graph* g, const prgpu_session* s, uint64_t* graph_bytes,
+                                 uint64_t* session_bytes);
+/* rank / nranks / engine rows [row_begin, row_end) / edges held (a whole
+ * graph: 0, 1, [0, n), its edge count). Any pointer may be NULL. */
+PRGPU_API int prgpu_graph_shard_info(const prgpu_graph* g, int* rank, int* nranks, uint32_t* row_begin,
+                                     uint32_t* row_end, uint64_t* local_edges);
 
 PRGPU_API int prgpu_graph_get_info(const prgpu_graph* g, prgpu_graph_info* info);
 /* Copies the reference-layout CSR back (any pointer may be NULL):

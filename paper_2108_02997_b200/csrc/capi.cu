@@ -45,9 +45,13 @@ std::unique_ptr<prgpu_graph> graph_generate_rmat(uint32_t, uint32_t, double, dou
                                                  uint64_t, int, cudaStream_t);
 std::unique_ptr<prgpu_graph> graph_generate_grid(uint32_t, double, double, uint64_t, int,
                                                  cudaStream_t);
+std::unique_ptr<prgpu_graph> graph_generate_rmat_shard(uint32_t, uint32_t, double, double, double, uint64_t, int,
+                                                       int, int, cudaStream_t);
 void graph_download(const prgpu_graph*, uint64_t*, uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
 prgpu_session* session_create(prgpu_graph*, const prgpu_params*, bool, int, int, double*, double*);
 void part_sizes(prgpu_graph*, const prgpu_params*, int, uint64_t*, uint64_t*);
+uint64_t graph_device_bytes(const prgpu_graph*);
+uint64_t session_device_bytes(const prgpu_session*);
 void part_exchange(prgpu_session*, prgpu_exchange*);
 int part_step(prgpu_session*);
 void part_finalize(prgpu_session*);
@@ -152,6 +156,34 @@ int prgpu_graph_generate_rmat(uint32_t scale, uint32_t ef, double a, double b, d
                               uint64_t seed, int device, prgpu_graph** out) {
     return make_graph(device, out, [&](cudaStream_t st) {
         return prgpu::graph_generate_rmat(scale, ef, a, b, c, seed, device, st);
+    });
+}
+
+int prgpu_graph_generate_rmat_shard(uint32_t scale, uint32_t ef, double a, double b, double c, uint64_t seed,
+                                    int rank, int nranks, int device, prgpu_graph** out) {
+    return make_graph(device, out, [&](cudaStream_t st) {
+        return prgpu::graph_generate_rmat_shard(scale, ef, a, b, c, seed, rank, nranks, device, st);
+    });
+}
+
+int prgpu_graph_shard_info(const prgpu_graph* g, int* rank, int* nranks, uint32_t* row_begin, uint32_t* row_end,
+                           uint64_t* local_edges) {
+    return guarded([&] {
+        if (!g) prgpu::fail(PRGPU_EINVAL, "null graph");
+        const bool sh = g->shard_n > 1;
+        if (rank) *rank = sh ? g->shard_rank : 0;
+        if (nranks) *nranks = sh ? g->shard_n : 1;
+        if (row_begin) *row_begin = sh ? g->shard_rows[g->shard_rank] : 0u;
+        if (row_end) *row_end = sh ? g->shard_rows[g->shard_rank + 1] : g->n;
+        if (local_edges) *local_edges = g->local_e;
+    });
+}
+
+int prgpu_device_bytes(const prgpu_graph* g, const prgpu_session* s, uint64_t* graph_bytes,
+                       uint64_t* session_bytes) {
+    return guarded([&] {
+        if (graph_bytes) *graph_bytes = g ? prgpu::graph_device_bytes(g) : 0;
+        if (session_bytes) *session_bytes = s ? prgpu::session_device_bytes(s) : 0;
     });
 }
 

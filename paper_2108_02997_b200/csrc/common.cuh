@@ -14,6 +14,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "../../include/prgpu.h"
 
@@ -127,6 +128,7 @@ struct DevBuf {
         std::swap(p, o.p); std::swap(n, o.n); std::swap(pooled, o.pooled);
     }
     T* release() { T* q = p; p = nullptr; n = 0; return q; }
+    size_t bytes() const { return n * sizeof(T); }
 };
 
 struct DeviceGuard {
@@ -202,6 +204,14 @@ struct prgpu_graph {
     uint32_t hub_end = 0, warp_end = 0, nonempty_end = 0;
     bool locality = false; // rows in the caller's order within classes (low-degree graphs)
     uint32_t sort_end[6] = {0, 0, 0, 0, 0, 0}; // rows with in-degree > 512, 256, 128, 64, 32, 8
+    // shard graphs (prgpu_graph_generate_rmat_shard, SURVEY 8e set-up): the
+    // vertex arrays are global, `col` holds only the in-edges of engine rows
+    // [shard_rows[rank], shard_rows[rank + 1]); kernels index it as
+    // col - col_base (col_base = row_off[first row]).  shard_n == 0: whole graph.
+    int shard_rank = 0, shard_n = 0;
+    std::vector<uint32_t> shard_rows; // [shard_n + 1] engine-row boundaries of every rank
+    uint64_t col_base = 0;
+    uint64_t local_e = 0;             // edges held (== e unless a shard)
     // source splits built on demand by sessions (graph_source_split), by threshold
     std::mutex split_mu;
     std::map<uint32_t, std::unique_ptr<prgpu::SourceSplit>> splits;

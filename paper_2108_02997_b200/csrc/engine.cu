@@ -30,7 +30,7 @@ __global__ void init_kernel(Params P, uint32_t ndangling) {
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n;
          v += (size_t)gridDim.x * blockDim.x) {
         const uint2 ri = P.rowinfo[v];
-        if (v < P.empty_begin)
+        if (v < P.empty_begin && v >= P.rank_lo && v < P.rank_hi) // a shard's own rows only
             for (uint32_t k = 0; k < P.K; ++k) P.rank[0][v * KS + k] = r0;
         if (ri.x) {
             const double cv = __ddiv_rn(r0, (double)ri.x);
@@ -563,22 +563,43 @@ void build_tasks(prgpu_session* s) {
     const uint32_t cmin = std::max<uint32_t>(1, (win + 31) / 32);
     uint64_t n_packed = 0;
     if (prow) {
-        DevBuf<uint64_t> cost((size_t)prow + 1);
-        packed_costs<<<blocks_for((uint64_t)prow + 1), kNT, 0, st>>>(g->row_off.p, plo, phi, cmin, cost.p);
-        PRGPU_LAUNCHED("packed_costs");
-        size_t tmp = 0;
-        PRGPU_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cost.p, cost.p, (int64_t)prow + 1, st));
-        DevBuf<char> t(std::max<size_t>(tmp, 1));
-        PRGPU_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, cost.p, cost.p, (int64_t)prow + 1, st));
-        g_launches.fetch_add(1);
-        uint64_t total = 0;
-        PRGPU_CUDA(cudaMemcpyAsync(&total, cost.p + prow, 8, cudaMemcpyDeviceToHost, st));
-        PRGPU_CUDA(cudaStreamSynchronize(st));
-        n_packed = (total + win - 1) / win;
+        // runs of rows [a, b): on a shard graph the packed rows are cut at every
+        // shard boundary, so no run spans two ranks' rows
+        std::vector<uint32_t> cuts{plo};
+        if (g->shard_n > 1)
+            for (uint32_t x : g->shard_rows)
+                if (x > plo && x < phi) cuts.push_back(x);
+        cuts.push_back(phi);
+        std::vector<std::pair<DevBuf<uint32_t>, uint64_t>> segs;
+        for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+            const uint32_t a = cuts[k], b = cuts[k + 1], rows = b - a;
+            if (!rows) continue;
+            DevBuf<uint64_t> cost((size_t)rows + 1);
+            packed_costs<<<blocks_for((uint64_t)rows + 1), kNT, 0, st>>>(g->row_off.p, a, b, cmin, cost.p);
+            PRGPU_LAUNCHED("packed_costs");
+            size_t tmp = 0;
+            PRGPU_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cost.p, cost.p, (int64_t)rows + 1, st));
+            DevBuf<char> t(std::max<size_t>(tmp, 1));
+            PRGPU_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, cost.p, cost.p, (int64_t)rows + 1, st));
+            g_launches.fetch_add(1);
+            uint64_t total = 0;
+            PRGPU_CUDA(cudaMemcpyAsync(&total, cost.p + rows, 8, cudaMemcpyDeviceToHost, st));
+            PRGPU_CUDA(cudaStreamSynchronize(st));
+            const uint64_t np = (total + win - 1) / win;
+            DevBuf<uint32_t> r0(np + 1);
+            packed_bounds<<<blocks_for(rows), kNT, 0, st>>>(cost.p, a, b, win, (uint32_t)np, r0.p);
+            PRGPU_LAUNCHED("packed_bounds");
+            PRGPU_CUDA(cudaStreamSynchronize(st));
+            n_packed += np;
+            segs.emplace_back(std::move(r0), np);
+        }
         s->packed_r0.alloc(n_packed + 1);
-        packed_bounds<<<blocks_for(prow), kNT, 0, st>>>(cost.p, plo, phi, win, (uint32_t)n_packed,
-                                                        s->packed_r0.p);
-        PRGPU_LAUNCHED("packed_bounds");
+        uint64_t at = 0; // segment k's runs, then its end row (= the next segment's first)
+        for (auto& sg : segs) {
+            PRGPU_CUDA(cudaMemcpyAsync(s->packed_r0.p + at, sg.first.p, (sg.second + 1) * 4,
+                                       cudaMemcpyDeviceToDevice, st));
+            at += sg.second;
+        }
         PRGPU_CUDA(cudaStreamSynchronize(st));
     } else {
         s->packed_r0.alloc(1);
@@ -669,12 +690,59 @@ __global__ void partition_kernel(Params P, const uint64_t* __restrict__ incl, ui
     bound[3 * b + 2] = lo;
 }
 
+// shard graphs: every rank's tasks are those of its shard's rows (build_tasks
+// cut the packed runs at the shard boundaries; empty-row tasks align to them)
+__global__ void shard_task_bounds(Params P, uint32_t er, const uint32_t* __restrict__ rows, uint32_t nranks,
+                                  const uint32_t* __restrict__ row_of_src, uint32_t nsrc,
+                                  uint64_t* __restrict__ bound) {
+    const uint32_t b = threadIdx.x;
+    if (b > nranks) return;
+    const uint32_t T = P.n_chunk + P.n_packed + P.n_empty_tasks, R = rows[b];
+    uint32_t lo = 0, hi = T; // first task whose row >= R
+    while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (row_of_task(P, mid, er) < R) lo = mid + 1;
+        else hi = mid;
+    }
+    uint32_t a = 0, z = nsrc; // sources with engine row < R
+    while (a < z) {
+        const uint32_t mid = (a + z) / 2;
+        if (row_of_src[mid] < R) a = mid + 1;
+        else z = mid;
+    }
+    bound[3 * b + 0] = b == nranks ? T : lo;
+    bound[3 * b + 1] = R;
+    bound[3 * b + 2] = a;
+}
+
 void plan_partition(prgpu_session* s, int nranks) {
     const prgpu_graph* g = s->g;
     cudaStream_t st = s->stream;
     Params& P = s->P;
     const uint32_t T = P.n_chunk + P.n_packed + P.n_empty_tasks;
     const uint32_t er = 8 * (32 / s->cfg.LG);
+    if (g->shard_n > 1) {
+        if (nranks != g->shard_n) fail(PRGPU_EINVAL, "partition: nranks differs from the graph's shard count");
+        DevBuf<uint32_t> rows((size_t)nranks + 1);
+        DevBuf<uint64_t> bound(3 * ((size_t)nranks + 1));
+        PRGPU_CUDA(cudaMemcpyAsync(rows.p, g->shard_rows.data(), ((size_t)nranks + 1) * 4, cudaMemcpyHostToDevice, st));
+        shard_task_bounds<<<1, 128, 0, st>>>(P, er, rows.p, (uint32_t)nranks, g->row_of_src.p, g->nsrc, bound.p);
+        PRGPU_LAUNCHED("shard_task_bounds");
+        std::vector<uint64_t> b(3 * ((size_t)nranks + 1));
+        PRGPU_CUDA(cudaMemcpyAsync(b.data(), bound.p, b.size() * 8, cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaStreamSynchronize(st));
+        s->parts.resize(nranks);
+        for (int r = 0; r < nranks; ++r) {
+            prgpu_partition& q = s->parts[r];
+            q.task_begin = (uint32_t)b[3 * r];
+            q.task_end = (uint32_t)b[3 * (r + 1)];
+            q.row_begin = (uint32_t)b[3 * r + 1];
+            q.row_end = (uint32_t)b[3 * (r + 1) + 1];
+            q.src_begin = b[3 * r + 2];
+            q.src_end = b[3 * (r + 1) + 2];
+        }
+        return;
+    }
     DevBuf<uint64_t> cost(std::max<uint32_t>(T, 1)), bound(3 * ((size_t)nranks + 1));
     if (T) {
         task_costs_kernel<<<blocks_for(T), kNT, 0, st>>>(P, er, cost.p);
@@ -719,6 +787,9 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
                               int nranks = 0, double* ext_contrib = nullptr, double* ext_rp = nullptr) {
     validate_params(p);
     if (!g || g->n == 0) fail(PRGPU_EINVAL, "pagerank: graph has no vertices");
+    if (g->shard_n > 1 && (nranks != g->shard_n || rank != g->shard_rank))
+        fail(PRGPU_EINVAL, "shard graph: only rank " + std::to_string(g->shard_rank) + " of a " +
+                               std::to_string(g->shard_n) + "-rank partition can run on it");
     DeviceGuard dg(g->device);
     auto s = std::make_unique<prgpu_session>();
     AllocScope scope(s->stream);
@@ -738,7 +809,14 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     PhaseLog ph("session", st);
 
     const int KS = s->cfg.KS;
-    s->rank.alloc(2 * (size_t)KS * n);
+    // rank rows: a shard keeps its own rows' only (indexed from its first row)
+    const uint32_t rank_lo = g->shard_n > 1 ? g->shard_rows[g->shard_rank] : 0u;
+    const uint32_t rank_hi = g->shard_n > 1 ? g->shard_rows[g->shard_rank + 1] : (uint32_t)n;
+    // rows without in-edges never store a rank (their value is c0): rows
+    // [rank_lo, min(rank_hi, nonempty_end)) only (C5: 99.5M of 268M rows)
+    const uint32_t rank_top = std::min<uint32_t>(rank_hi, g->nonempty_end);
+    const size_t rank_rows = std::max<size_t>(rank_top > rank_lo ? rank_top - rank_lo : 0, 1);
+    s->rank.alloc(2 * (size_t)KS * rank_rows);
     double* cbase = ext_contrib;
     s->ext_contrib_base = ext_contrib;
     s->ext_rank_partials = ext_rp;
@@ -792,10 +870,12 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     P.n = g->n;
     P.K = K;
     P.row_off = g->row_off.p;
-    P.col = g->col.p;
+    P.col = g->col.p - g->col_base; // a shard's edges, indexed by the global row offsets
     P.rowinfo = g->rowinfo.p;
-    P.rank[0] = s->rank.p;
-    P.rank[1] = s->rank.p + (size_t)s->cfg.KS * n;
+    P.rank[0] = s->rank.p - (size_t)rank_lo * KS;
+    P.rank[1] = s->rank.p + (size_t)KS * rank_rows - (size_t)rank_lo * KS;
+    P.rank_lo = rank_lo;
+    P.rank_hi = rank_hi;
     P.ks = (uint32_t)s->cfg.KS;
     P.ref = s->ref.p;
     P.trace = s->trace.p;
@@ -1185,6 +1265,7 @@ void deal_tasks(prgpu_session* s) {
     bool split = false;
     for (const auto& l : s->launches) split |= l.P.no_finalize != 0;
     if (N < 2 || (dv && std::atoi(dv) == 0) || !split) return;
+    if (s->g->shard_n > 1) return; // a shard holds one contiguous row range's edges
     cudaStream_t st = s->stream;
     const uint32_t n = s->g->n, nl = s->n_long, T1 = P.n_chunk, np = P.n_packed, ne = P.n_empty_tasks;
     std::vector<uint32_t> cf((size_t)nl + 1), pr((size_t)np + 1);
@@ -1285,7 +1366,8 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
     // only the peers that gather a source receive its row (PRGPU_NEED=0: all)
     P.need = nullptr;
     const char* nv = std::getenv("PRGPU_NEED");
-    if (npeers > 0 && !(nv && std::atoi(nv) == 0)) {
+    // (a shard sees only its own rows' in-neighbours: every row goes to every peer)
+    if (npeers > 0 && !(nv && std::atoi(nv) == 0) && s->g->shard_n <= 1) {
         const uint32_t nsrc = std::max<uint32_t>(s->g->nsrc, 1);
         s->need.alloc((nsrc + 3) / 4);
         PRGPU_CUDA(cudaMemsetAsync(s->need.p, 0, (size_t)(nsrc + 3) / 4 * 4, s->stream));
@@ -2012,6 +2094,24 @@ void session_observed(prgpu_session* s, prgpu_result* out, prgpu_observer_fn fn,
     PRGPU_CUDA(cudaEventElapsedTime(&ms, s->e0, s->e1));
     s->last_loop_ms = ms;
     session_results(s, out);
+}
+
+// device memory held by a graph / a session (its DevBufs)
+uint64_t graph_device_bytes(const prgpu_graph* g) {
+    uint64_t b = g->row_off.bytes() + g->col.bytes() + g->deg.bytes() + g->rowinfo.bytes() + g->row_of_src.bytes() +
+                 g->new_of_old.bytes() + g->old_of_new.bytes();
+    for (const auto& kv : g->splits)
+        b += kv.second->off_hot.bytes() + kv.second->off_cold.bytes() + kv.second->col_hot.bytes() +
+             kv.second->col_cold.bytes();
+    return b;
+}
+uint64_t session_device_bytes(const prgpu_session* s) {
+    uint64_t b = s->rank.bytes() + s->contrib.bytes() + s->partials.bytes() + s->trace.bytes() + s->ref.bytes() +
+                 s->chunk_acc.bytes() + s->hot_part.bytes() + s->lanes.bytes() + s->gs.bytes() +
+                 s->chunk_row.bytes() + s->chunk_first.bytes() + s->packed_r0.bytes() + s->row_cnt.bytes() +
+                 s->task_list.bytes() + s->row_owner.bytes() + s->rank_partials.bytes() + s->need.bytes();
+    for (const auto& m : s->mode_contrib) b += m.bytes();
+    return b;
 }
 
 double session_time_pull(prgpu_session* s, int launches) {

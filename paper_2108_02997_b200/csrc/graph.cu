@@ -116,6 +116,83 @@ __global__ void rmat_keys(uint64_t m, uint32_t scale, uint64_t kd, uint64_t ta, 
     }
 }
 
+// rmat_keys restricted to edges whose (permuted) target lies in [dlo, dhi):
+// appended in any order at a block-aggregated cursor (the slab is sorted
+// afterwards); keys past `cap` are counted, not written (caller retries)
+__global__ void __launch_bounds__(256) rmat_keys_slab(uint64_t m, uint32_t scale, uint64_t kd, uint64_t ta,
+                                                      uint64_t tab, uint64_t tabc, PermKeys pk, uint32_t dlo,
+                                                      uint32_t dhi, uint64_t* __restrict__ keys, uint64_t cap,
+                                                      unsigned long long* __restrict__ cnt) {
+    __shared__ unsigned s_w[8];
+    __shared__ unsigned long long s_base;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < m; i0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = i0 + threadIdx.x;
+        bool keep = false;
+        uint64_t key = 0;
+        if (i < m) {
+            uint32_t src = 0, dst = 0;
+            for (uint32_t l = 0; l < scale; ++l) {
+                const uint64_t x = mix64(kd ^ ((i << 6) | l));
+                const uint32_t bit = 1u << (scale - 1 - l);
+                if (x < ta) {
+                } else if (x < tab) {
+                    dst |= bit;
+                } else if (x < tabc) {
+                    src |= bit;
+                } else {
+                    src |= bit;
+                    dst |= bit;
+                }
+            }
+            if (src != dst) {
+                const uint32_t d = perm_apply(dst, pk);
+                keep = d >= dlo && d < dhi;
+                key = ((uint64_t)d << scale) | perm_apply(src, pk);
+            }
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) s_w[warp] = __popc(b);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            for (int w = 0; w < 8; ++w) t += s_w[w];
+            s_base = t ? atomicAdd(cnt, t) : 0ull;
+        }
+        __syncthreads();
+        unsigned before = 0;
+        for (uint32_t w = 0; w < warp; ++w) before += s_w[w];
+        const uint64_t at = s_base + before + __popc(b & ((1u << lane) - 1u));
+        if (keep && at < cap) keys[at] = key;
+        __syncthreads();
+    }
+}
+
+// shard boundaries: cost of engine row r (in-degree + 2 for rows with
+// in-edges, 1 for the rest)
+__global__ void shard_costs(const uint64_t* __restrict__ row_off, uint32_t n, uint32_t nonempty_end,
+                            uint64_t* __restrict__ cost) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x)
+        cost[r] = r < nonempty_end ? (row_off[r + 1] - row_off[r]) + 2 : 1;
+}
+__global__ void shard_search(const uint64_t* __restrict__ excl, uint32_t n, uint32_t nranks,
+                             uint32_t* __restrict__ out) {
+    const uint32_t b = threadIdx.x;
+    if (b > nranks) return;
+    if (b == 0 || b == nranks) {
+        out[b] = b ? n : 0;
+        return;
+    }
+    const uint64_t target = excl[n] * b / nranks;
+    uint32_t lo = 0, hi = n; // first row whose exclusive prefix >= target
+    while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (excl[mid] < target) lo = mid + 1;
+        else hi = mid;
+    }
+    out[b] = lo;
+}
+
 __global__ void grid_keys(uint32_t side, uint64_t uh, uint64_t tp, uint64_t kg, uint64_t L,
                           uint64_t kl, uint64_t n, uint32_t lg, uint64_t* __restrict__ keys) {
     const uint64_t total = 2 * uh; // candidates
@@ -326,7 +403,8 @@ __global__ void check_offsets(const uint64_t* __restrict__ off, uint32_t n, uint
 __global__ void place_edges(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr, uint32_t n,
                             uint64_t jb, uint64_t je, const uint32_t* __restrict__ new_of_old,
                             const uint64_t* __restrict__ row_off, const uint32_t* __restrict__ src_of_old,
-                            uint32_t* __restrict__ col, const uint32_t* __restrict__ out_deg, int* bad) {
+                            uint32_t* __restrict__ col, const uint32_t* __restrict__ out_deg, int* bad,
+                            uint32_t rb = 0, uint32_t re = 0xFFFFFFFFu, uint64_t col_base = 0) {
     const uint64_t j0 = jb + (uint64_t)blockIdx.x * kEdgeChunk, j1 = min(j0 + kEdgeChunk, je);
     uint32_t r0, r1;
     chunk_rows(off, n, j0, j1, r0, r1);
@@ -337,7 +415,9 @@ __global__ void place_edges(const uint64_t* __restrict__ off, const uint32_t* __
             if (u >= n) { *bad = 1; continue; }
             if (out_deg[u] == 0) { *bad = 2; continue; }
         }
-        col[row_off[new_of_old[o]] + (j - off[o])] = src_of_old[u];
+        const uint32_t r = new_of_old[o];
+        if (r < rb || r >= re) continue; // a shard keeps its own rows only
+        col[row_off[r] + (j - off[o]) - col_base] = src_of_old[u];
     }
 }
 
@@ -740,10 +820,30 @@ std::unique_ptr<prgpu_graph> assemble_vertices(uint32_t n, const uint64_t* off, 
 struct EdgeFill {
     prgpu_graph* g;
     DevBuf<uint32_t> src_of_old;
-    EdgeFill(prgpu_graph* gr, cudaStream_t st) : g(gr) {
+    uint32_t rb = 0, re = 0xFFFFFFFFu; // engine rows whose edges are kept (a shard's)
+    // rows [r_begin, r_end) only (a shard): col holds their edges, from col_base
+    EdgeFill(prgpu_graph* gr, cudaStream_t st, uint32_t r_begin = 0, uint32_t r_end = 0xFFFFFFFFu) : g(gr) {
+        uint64_t n_alloc = g->e; // col entries: [col_base, col_base + n_alloc)
+        g->col_base = 0;
+        g->local_e = g->e;
+        if (r_end != 0xFFFFFFFFu) {
+            rb = r_begin;
+            re = r_end;
+            uint64_t lo = 0, hi = 0;
+            PRGPU_CUDA(cudaMemcpyAsync(&lo, g->row_off.p + rb, 8, cudaMemcpyDeviceToHost, st));
+            PRGPU_CUDA(cudaMemcpyAsync(&hi, g->row_off.p + re, 8, cudaMemcpyDeviceToHost, st));
+            PRGPU_CUDA(cudaStreamSynchronize(st));
+            // the kernels load colidx 128 bits at a time from global indices
+            // that are multiples of 4: the shard's array starts at one
+            g->col_base = lo & ~3ull;
+            g->local_e = hi - lo;
+            n_alloc = hi - g->col_base;
+        }
         // engine edges (+16 zero pad for the kernels' 128-bit colidx loads)
-        g->col.alloc(g->e + 16);
-        PRGPU_CUDA(cudaMemsetAsync(g->col.p + g->e, 0, 16 * sizeof(uint32_t), st));
+        g->col.alloc(n_alloc + 16);
+        PRGPU_CUDA(cudaMemsetAsync(g->col.p + n_alloc, 0, 16 * sizeof(uint32_t), st));
+        if (n_alloc > g->local_e) // the (< 4) alignment slots ahead of a shard's first edge
+            PRGPU_CUDA(cudaMemsetAsync(g->col.p, 0, (n_alloc - g->local_e) * sizeof(uint32_t), st));
         src_of_old.alloc(g->n);
         src_of_old_kernel<<<grid_for(g->n), kThreads, 0, st>>>(g->rowinfo.p, g->new_of_old.p, g->n,
                                                                src_of_old.p);
@@ -754,7 +854,8 @@ struct EdgeFill {
         if (je <= jb) return;
         const uint64_t blocks = (je - jb + kEdgeChunk - 1) / kEdgeChunk;
         place_edges<<<(unsigned)blocks, kThreads, 0, st>>>(off, nbr, g->n, jb, je, g->new_of_old.p,
-                                                           g->row_off.p, src_of_old.p, g->col.p, deg, bad);
+                                                           g->row_off.p, src_of_old.p, g->col.p, deg, bad, rb,
+                                                           re, g->col_base);
         PRGPU_LAUNCHED("place_edges");
     }
     // graph_from_csr: sort the caller's rows [v0, v1) (complete once their
@@ -789,17 +890,20 @@ struct EdgeFill {
         // one class per power-of-two length band, each sorted at its own
         // width (a row is padded to the class's width, so bands halve the
         // padding of the wide ones)
-        const uint32_t h = g->hub_end, m512 = g->sort_end[0];
+        // a shard sorts its own rows only (col indexed from col_base)
+        uint32_t* colv = g->col.p - g->col_base;
+        const uint32_t lo_r = rb, hi_r = std::min<uint32_t>(re, g->n);
+        const uint32_t h = std::max(g->hub_end, lo_r), m512 = std::min(g->sort_end[0], hi_r);
         if (m512 > h) {
             sort_rows_block<<<m512 - h, 256, 0, st>>>(g->row_off.p, h, (int)bits_for(std::max(g->nsrc, 2u)),
-                                                      g->col.p);
+                                                      colv);
             PRGPU_LAUNCHED("sort_rows_block");
         }
         auto warp_sort = [&](auto items, int c) {
             constexpr int I = decltype(items)::value;
-            const uint32_t r0 = g->sort_end[c], r1 = g->sort_end[c + 1];
+            const uint32_t r0 = std::max(g->sort_end[c], lo_r), r1 = std::min(g->sort_end[c + 1], hi_r);
             if (r1 <= r0) return;
-            sort_rows_warp<I><<<(r1 - r0 + 7) / 8, 256, 0, st>>>(g->row_off.p, r0, r1, g->col.p);
+            sort_rows_warp<I><<<(r1 - r0 + 7) / 8, 256, 0, st>>>(g->row_off.p, r0, r1, colv);
             PRGPU_LAUNCHED("sort_rows_warp");
         };
         warp_sort(std::integral_constant<int, 16>{}, 0); // 257..512
@@ -1111,6 +1215,127 @@ std::unique_ptr<prgpu_graph> graph_generate_rmat(uint32_t scale, uint32_t ef, do
     return assemble(std::move(keys), u, n, scale, device, st);
 }
 
+// One rank's shard of the RMAT graph (SURVEY 8e set-up), never holding the
+// whole edge list: every rank generates all edges, in slabs of target ids —
+//   pass 1: per slab, the slab's keys sorted + deduplicated, counted into the
+//           global in- and out-degrees (exact: a (source, target) duplicate
+//           lies in one slab), so every rank computes the same vertex half
+//           (relabel, row offsets, source ids) as the whole-graph build;
+//   shard rows: contiguous engine-row ranges of equal cost (in-degree + 2
+//           per row, 1 per row without in-edges; cuts among those rows on
+//           multiples of 256 so no empty-row task spans two ranks);
+//   pass 2: per slab again, the slab's edges (= its range of the original
+//           CSR) placed into col if their engine row is this rank's; rows
+//           then sorted by source id as in the whole build.
+// Slabs are sized so a slab's keys (+ the sort buffer) stay under ~16 GB.
+std::unique_ptr<prgpu_graph> graph_generate_rmat_shard(uint32_t scale, uint32_t ef, double a, double b, double c,
+                                                       uint64_t seed, int rank, int nranks, int device,
+                                                       cudaStream_t st) {
+    if (scale < 1 || scale > 30) fail(PRGPU_EINVAL, "rmat: scale must be in [1, 30]");
+    if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0))
+        fail(PRGPU_EINVAL, "rmat: probabilities must be >= 0 with a+b+c <= 1");
+    if (nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks) fail(PRGPU_EINVAL, "shard: bad rank / nranks");
+    const uint32_t n = 1u << scale;
+    const uint64_t m = (uint64_t)ef << scale;
+    PermKeys pk;
+    const uint64_t pkey = stream_key(seed, 2);
+    for (int r = 0; r < 3; ++r) pk.k[r] = mix64_host(pkey + (uint64_t)r);
+    pk.mask = (1ull << scale) - 1;
+    pk.hs = (scale + 1) / 2;
+    const uint64_t kd = stream_key(seed, 1), ta = prob_threshold(a), tab = prob_threshold(a + b),
+                   tabc = prob_threshold(a + b + c);
+    const char* sb = std::getenv("PRGPU_SLAB_KEYS"); // keys per slab (tests: small slabs)
+    const uint64_t slab_keys = sb ? std::max<uint64_t>(1024, (uint64_t)std::atoll(sb)) : (1ull << 30);
+    const uint32_t S = (uint32_t)std::min<uint64_t>(n, std::max<uint64_t>(1, (m + slab_keys - 1) / slab_keys));
+    auto slab_lo = [&](uint32_t s) { return (uint32_t)(((uint64_t)n * s) / S); };
+    DevBuf<unsigned long long> cnt(1);
+    // one slab's sorted unique keys (target << scale | source) into `keys`
+    auto slab = [&](uint32_t s, DevBuf<uint64_t>& keys) -> uint64_t {
+        uint64_t cap = (m / S) + (m / S) / 4 + 4096;
+        for (;;) {
+            keys.alloc(cap);
+            PRGPU_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), st));
+            rmat_keys_slab<<<grid_for(m), 256, 0, st>>>(m, scale, kd, ta, tab, tabc, pk, slab_lo(s), slab_lo(s + 1),
+                                                        keys.p, cap, cnt.p);
+            PRGPU_LAUNCHED("rmat_keys_slab");
+            unsigned long long got = 0;
+            PRGPU_CUDA(cudaMemcpyAsync(&got, cnt.p, sizeof(got), cudaMemcpyDeviceToHost, st));
+            PRGPU_CUDA(cudaStreamSynchronize(st));
+            if (got <= cap) {
+                if (!got) return 0;
+                DevBuf<uint64_t> alt(got);
+                sort_keys(keys, alt, got, 2 * (int)scale, st);
+                return unique_keys(keys, alt, got, st);
+            }
+            cap = got + 4096; // a heavier slab than expected: once more at its size
+        }
+    };
+    // pass 1: exact degrees
+    DevBuf<uint32_t> in_deg(n), out_deg(n);
+    PRGPU_CUDA(cudaMemsetAsync(in_deg.p, 0, (size_t)n * 4, st));
+    PRGPU_CUDA(cudaMemsetAsync(out_deg.p, 0, (size_t)n * 4, st));
+    uint64_t e = 0;
+    for (uint32_t s = 0; s < S; ++s) {
+        DevBuf<uint64_t> keys;
+        const uint64_t u = slab(s, keys);
+        if (u) {
+            count_degrees<<<grid_for(u), kThreads, 0, st>>>(keys.p, u, scale, in_deg.p, out_deg.p);
+            PRGPU_LAUNCHED("count_degrees");
+        }
+        e += u;
+    }
+    DevBuf<uint64_t> off((size_t)n + 1);
+    gather_deg_u64<<<grid_for((uint64_t)n + 1), kThreads, 0, st>>>(in_deg.p, nullptr, off.p, n);
+    PRGPU_LAUNCHED("gather_deg_u64");
+    exclusive_scan_u64(off.p, (uint64_t)n + 1, st);
+    in_deg.reset();
+    auto g = assemble_vertices(n, off.p, e, out_deg.p, scale, device, st);
+    // shard rows
+    {
+        DevBuf<uint64_t> cost((size_t)n + 1);
+        PRGPU_CUDA(cudaMemsetAsync(cost.p + n, 0, 8, st));
+        shard_costs<<<grid_for(n), kThreads, 0, st>>>(g->row_off.p, n, g->nonempty_end, cost.p);
+        PRGPU_LAUNCHED("shard_costs");
+        exclusive_scan_u64(cost.p, (uint64_t)n + 1, st);
+        DevBuf<uint32_t> bnd((size_t)nranks + 1);
+        shard_search<<<1, 128, 0, st>>>(cost.p, n, (uint32_t)nranks, bnd.p);
+        PRGPU_LAUNCHED("shard_search");
+        g->shard_rows.resize((size_t)nranks + 1);
+        PRGPU_CUDA(cudaMemcpyAsync(g->shard_rows.data(), bnd.p, ((size_t)nranks + 1) * 4, cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaStreamSynchronize(st));
+        const uint32_t eb = g->nonempty_end;
+        for (int r = 1; r < nranks; ++r) {
+            uint32_t x = g->shard_rows[r];
+            if (x > eb) x = eb + ((x - eb) & ~255u); // empty-row tasks never straddle two ranks
+            g->shard_rows[r] = std::max(x, g->shard_rows[r - 1]);
+        }
+    }
+    g->shard_rank = rank;
+    g->shard_n = nranks;
+    // pass 2: this rank's edges
+    EdgeFill fill(g.get(), st, g->shard_rows[rank], g->shard_rows[rank + 1]);
+    std::vector<uint64_t> offh((size_t)S + 1);
+    for (uint32_t s = 0; s <= S; ++s)
+        PRGPU_CUDA(cudaMemcpyAsync(&offh[s], off.p + slab_lo(s), 8, cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    for (uint32_t s = 0; s < S; ++s) {
+        if (offh[s + 1] == offh[s]) continue;
+        DevBuf<uint64_t> keys;
+        const uint64_t u = slab(s, keys);
+        if (u != offh[s + 1] - offh[s]) fail(PRGPU_ECUDA, "shard: slab edge count changed between passes");
+        DevBuf<uint32_t> nbr(u);
+        keys_low<<<grid_for(u), kThreads, 0, st>>>(keys.p, u, scale, nbr.p);
+        PRGPU_LAUNCHED("keys_low");
+        keys.reset();
+        // the slab is the original CSR's edges [offh[s], offh[s+1]): nbr indexed by global edge index
+        fill.place(off.p, nbr.p - offh[s], offh[s], offh[s + 1], nullptr, nullptr, st);
+        PRGPU_CUDA(cudaStreamSynchronize(st)); // nbr is freed next
+    }
+    fill.finish(st);
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    return g;
+}
+
 std::unique_ptr<prgpu_graph> graph_generate_grid(uint32_t side, double p, double lr, uint64_t seed,
                                                  int device, cudaStream_t st) {
     if (side < 2 || (uint64_t)side * side > 0xFFFFFFFFull)
@@ -1138,6 +1363,7 @@ std::unique_ptr<prgpu_graph> graph_generate_grid(uint32_t side, double p, double
 
 void graph_download(const prgpu_graph* g, uint64_t* h_off, uint32_t* h_nbr, uint32_t* h_deg,
                     uint32_t* h_dang, cudaStream_t st) {
+    if (g->shard_n > 1 && h_nbr) fail(PRGPU_EINVAL, "graph_download: a shard graph holds one rank's edges only");
     const uint32_t n = g->n;
     const uint64_t e = g->e;
     if (n == 0) { // the empty graph: in_offsets = {0}
@@ -1195,6 +1421,7 @@ void graph_download(const prgpu_graph* g, uint64_t* h_off, uint32_t* h_nbr, uint
 // Test tooling for graphs too large to download whole (C5).
 uint64_t graph_rows(const prgpu_graph* g, const uint32_t* h_rows, uint32_t nrows, uint64_t* h_off,
                     uint32_t* h_nbr, uint64_t cap, cudaStream_t st) {
+    if (g->shard_n > 1) fail(PRGPU_EINVAL, "graph_rows: a shard graph holds one rank's edges only");
     for (uint32_t i = 0; i < nrows; ++i)
         if (h_rows[i] >= g->n) fail(PRGPU_EINVAL, "graph_rows: row >= vertex_count");
     h_off[0] = 0;

@@ -106,6 +106,7 @@ struct Params {
     const uint32_t* __restrict__ col;  // source ids
     const uint2* __restrict__ rowinfo; // {out-degree, source id}
     double* rank[2];                   // [n][ks] row-major, K lanes per row (rows < empty_begin only)
+    uint32_t rank_lo, rank_hi;         // rows whose ranks this session holds (a shard's; else 0..n)
     uint32_t ks;                       // rank / contribution row stride (doubles)
     double* cbase;                     // contributions [parity][src][KS], see caddr()
     uint64_t cold_off[2];              // first row of each parity buffer (in rows of KS)

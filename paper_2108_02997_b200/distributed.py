@@ -171,20 +171,23 @@ def _assemble(g: CsrGraph, chunks_by_rank, K) -> np.ndarray:
 
 def emulate(g: CsrGraph, alphas: Sequence[float], nranks: int, tolerance=1e-6,
             norm: NormKind = NormKind.L1, max_iterations: int = 500, stop_mask: int = 0,
-            want_ranks: bool = True, fused: bool = False, graph: bool = False) -> PartResult:
+            want_ranks: bool = True, fused: bool = False, graph: bool = False,
+            shards: Optional[Sequence[CsrGraph]] = None) -> PartResult:
     """All `nranks` partitions in this process on this GPU.  Default: the
     exchange is a device copy of each rank's rows into every other rank's
     buffers (what NCCL does between GPUs).  fused=True: the ranks' kernels
     store into each other's buffers and count arrivals themselves (the
     peer-memory path); the ranks run one after another, so no kernel ever
     waits on another.  graph=True (one rank only): the fused loop as the
-    CUDA graph prgpu_part_launch enqueues."""
+    CUDA graph prgpu_part_launch enqueues.  shards: the ranks' shard graphs
+    (each holds its own rows' edges only)."""
     import torch
     if graph and (not fused or nranks != 1):
         raise ValueError("emulate: graph=True needs fused=True and nranks == 1 (ranks would wait on each other)")
     dev = g.device
-    parts = [_Part(g, alphas, tolerance, norm, max_iterations, stop_mask, r, nranks, dev, fused=fused)
-             for r in range(nranks)]
+    # shards: one shard graph per rank (generate_rmat(shard=(r, nranks))), g any of them
+    parts = [_Part(shards[r] if shards else g, alphas, tolerance, norm, max_iterations, stop_mask, r, nranks, dev,
+                   fused=fused) for r in range(nranks)]
     stream = torch.cuda.Stream(device=dev)  # a real stream: the legacy default is handle 0
     with torch.cuda.stream(stream):
         return _emulate_on(parts, alphas, max_iterations, want_ranks, g, fused, graph)
@@ -496,9 +499,9 @@ def _gather_ranks(part: _Part, g: CsrGraph, K: int, world: int) -> np.ndarray:
     if world > 1:
         gathered = torch.empty((world, K, ld), dtype=torch.float64, device=dev)
         if dist.get_backend() == "gloo":
-            hg = torch.empty((world, K, ld), dtype=torch.float64)
+            hg = torch.empty((world * K, ld), dtype=torch.float64)  # gloo: chunks along dim 0
             dist.all_gather_into_tensor(hg, local.cpu())
-            gathered.copy_(hg)
+            gathered.copy_(hg.view(world, K, ld))
         else:
             dist.all_gather_into_tensor(gathered, local)
     else:

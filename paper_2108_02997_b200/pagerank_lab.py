@@ -166,6 +166,15 @@ class CsrGraph:
         check(lib().prgpu_graph_download(self._h, None, None, deg.ctypes.data, None), "download")
         return deg
 
+    def shard_info(self) -> dict:
+        """rank, nranks, engine rows [row_begin, row_end) and edges held
+        (prgpu_graph_shard_info; a whole graph: 0, 1, all rows, all edges)."""
+        r, nr, rb, re_, le = C.c_int(), C.c_int(), C.c_uint32(), C.c_uint32(), C.c_uint64()
+        check(lib().prgpu_graph_shard_info(self._h, C.byref(r), C.byref(nr), C.byref(rb), C.byref(re_),
+                                           C.byref(le)), "shard info")
+        return dict(rank=r.value, nranks=nr.value, row_begin=rb.value, row_end=re_.value,
+                    local_edges=le.value)
+
     def rows(self, rows):
         """(off[len(rows)+1], nbr): the in-neighbours of the given vertices,
         ascending per row as in in_neighbors, without downloading the whole
@@ -211,8 +220,15 @@ def csr_from_arrays(vertex_count: int, in_offsets, in_neighbors, out_degree,
 
 
 def generate_rmat(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19,
-                  c: float = 0.19, seed: int = 2108, device: Optional[int] = None) -> CsrGraph:
-    """RMAT graph generated and built on the device."""
+                  c: float = 0.19, seed: int = 2108, device: Optional[int] = None,
+                  shard: Optional[tuple] = None) -> CsrGraph:
+    """RMAT graph generated and built on the device.
+    shard=(rank, nranks): only that rank's rows' in-edges (SURVEY 8e set-up;
+    prgpu_graph_generate_rmat_shard) for a partitioned run."""
+    if shard is not None:
+        rank, nranks = shard
+        return _new_graph(lib().prgpu_graph_generate_rmat_shard, scale, edge_factor, a, b, c, seed,
+                          rank, nranks, device=device)
     return _new_graph(lib().prgpu_graph_generate_rmat, scale, edge_factor, a, b, c, seed,
                       device=device)
 
