@@ -1,0 +1,8 @@
+# bench lines for every config at HEAD (profiles/r2_configs.md)
+mkdir -p gpurun_out/r2
+for c in c1 c2 c3 c4 c2series c5series c2k1; do
+  timeout 900 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/r2/bench_$c.log 2>&1; echo "$c rc=$?"
+done
+timeout 900 python bench.py --impl reference --config c2 --steps 5 --warmup 1 > gpurun_out/r2/ref_c2.log 2>&1; echo "ref c2 rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2/launches_c5.csv \
+  python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r2/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
