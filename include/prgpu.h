@@ -263,6 +263,15 @@ PRGPU_API int prgpu_part_set_peers(prgpu_session* s, int npeers, double* const* 
                                    double* const* peer_partials, unsigned int* const* peer_arrive,
                                    unsigned int* arrive);
 PRGPU_API int prgpu_part_launch(prgpu_session* s);
+/* Shard graphs: the needed-only exchange mask is built from every rank's
+ * rows, which no rank holds.  prgpu_part_need_local fills dev_bits (device,
+ * ceil(nsrc/4)*4 bytes, 4-byte aligned; nsrc = vertices with out-degree > 0)
+ * with this rank's bit for every source its rows gather; sum (= OR: the bits
+ * are disjoint) the ranks' buffers, e.g. one all-reduce, and hand the result
+ * to prgpu_part_set_need before prgpu_part_set_peers.  Without it a shard's
+ * fused exchange stores every row into every peer.  At most 8 ranks. */
+PRGPU_API int prgpu_part_need_local(prgpu_session* s, uint8_t* dev_bits);
+PRGPU_API int prgpu_part_set_need(prgpu_session* s, const uint8_t* dev_bits);
 /* Fused exchange volume: contribution rows this rank stores into its peers
  * per iteration while every lane is live (rows of *row_doubles doubles). */
 PRGPU_API int prgpu_part_sent_rows(prgpu_session* s, uint64_t* rows, uint32_t* row_doubles);

@@ -51,6 +51,8 @@ void graph_download(const prgpu_graph*, uint64_t*, uint32_t*, uint32_t*, uint32_
 prgpu_session* session_create(prgpu_graph*, const prgpu_params*, bool, int, int, double*, double*);
 void part_sizes(prgpu_graph*, const prgpu_params*, int, uint64_t*, uint64_t*);
 uint64_t graph_device_bytes(const prgpu_graph*);
+void part_need_local(prgpu_session*, uint8_t*);
+void part_set_need(prgpu_session*, const uint8_t*);
 uint64_t session_device_bytes(const prgpu_session*);
 void part_exchange(prgpu_session*, prgpu_exchange*);
 int part_step(prgpu_session*);
@@ -490,6 +492,20 @@ int prgpu_part_set_peers(prgpu_session* s, int npeers, double* const* peer_contr
         if (!s || (npeers > 0 && (!peer_contrib || !peer_partials || !peer_arrive)))
             prgpu::fail(PRGPU_EINVAL, "null argument");
         prgpu::part_set_peers(s, npeers, peer_contrib, peer_partials, peer_arrive, arrive);
+    });
+}
+
+int prgpu_part_need_local(prgpu_session* s, uint8_t* dev_bits) {
+    return guarded([&] {
+        if (!s || !dev_bits) prgpu::fail(PRGPU_EINVAL, "null argument");
+        prgpu::part_need_local(s, dev_bits);
+    });
+}
+
+int prgpu_part_set_need(prgpu_session* s, const uint8_t* dev_bits) {
+    return guarded([&] {
+        if (!s || !dev_bits) prgpu::fail(PRGPU_EINVAL, "null argument");
+        prgpu::part_set_need(s, dev_bits);
     });
 }
 

@@ -449,6 +449,7 @@ struct prgpu_session {
     DevBuf<double> rank_partials;
     uint64_t sent_rows = 0;    // fused exchange: contribution rows stored into peers per iteration
     DevBuf<unsigned int> need; // fused exchange: [ceil(nsrc/4)] one byte per source, bit q = rank q gathers it
+    bool need_given = false;   // shards: the ranks' OR-reduced mask (prgpu_part_set_need)
     cudaStream_t ext_stream = nullptr;
     double* ext_contrib_base = nullptr; // caller-provided contribution buffer (partition sessions)
     double* ext_rank_partials = nullptr; // caller-provided rank partials (2 parities for the fused exchange)
@@ -1322,6 +1323,48 @@ __global__ void sent_rows_kernel(const uint2* __restrict__ rowinfo, uint32_t row
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
+// this rank's bit of the exchange mask from its own rows only (a shard sees
+// no other rows): bits[src] |= 1 << rank for every source its rows gather
+__global__ void need_local_kernel(const uint64_t* __restrict__ row_off, const uint32_t* __restrict__ col,
+                                  uint32_t r0, uint32_t r1, uint32_t bit, unsigned int* __restrict__ need) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t r = r0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); r < r1;
+         r += (gridDim.x * blockDim.x) >> 5)
+        for (uint64_t j = row_off[r] + lane; j < row_off[r + 1]; j += 32) {
+            const uint32_t src = col[j];
+            atomicOr(need + (src >> 2), bit << (8 * (src & 3)));
+        }
+}
+
+void part_need_local(prgpu_session* s, uint8_t* dev_bits) {
+    DeviceGuard dg(s->g->device);
+    if (s->parts.empty()) fail(PRGPU_EINVAL, "not a partition session");
+    if (s->nranks > 8) fail(PRGPU_EINVAL, "need mask: at most 8 ranks (one byte per source)");
+    const uint32_t nsrc = std::max<uint32_t>(s->g->nsrc, 1);
+    if (reinterpret_cast<uintptr_t>(dev_bits) % 4) fail(PRGPU_EINVAL, "need mask: buffer must be 4-byte aligned");
+    PRGPU_CUDA(cudaMemsetAsync(dev_bits, 0, (size_t)(nsrc + 3) / 4 * 4, s->cur()));
+    const prgpu_partition& me = s->parts[s->part_rank];
+    const uint32_t r1 = std::min(me.row_end, s->P.empty_begin);
+    if (r1 > me.row_begin) {
+        need_local_kernel<<<(unsigned)std::min<uint64_t>(((uint64_t)(r1 - me.row_begin) * 32 + kNT - 1) / kNT,
+                                                         148ull * 64),
+                            kNT, 0, s->cur()>>>(s->P.row_off, s->P.col, me.row_begin, r1, 1u << s->part_rank,
+                                                reinterpret_cast<unsigned int*>(dev_bits));
+        PRGPU_LAUNCHED("need_local");
+    }
+    PRGPU_CUDA(cudaStreamSynchronize(s->cur()));
+}
+
+void part_set_need(prgpu_session* s, const uint8_t* dev_bits) {
+    DeviceGuard dg(s->g->device);
+    if (s->parts.empty()) fail(PRGPU_EINVAL, "not a partition session");
+    const uint32_t nsrc = std::max<uint32_t>(s->g->nsrc, 1);
+    s->need.alloc((nsrc + 3) / 4);
+    PRGPU_CUDA(cudaMemcpyAsync(s->need.p, dev_bits, (size_t)(nsrc + 3) / 4 * 4, cudaMemcpyDeviceToDevice, s->cur()));
+    PRGPU_CUDA(cudaStreamSynchronize(s->cur()));
+    s->need_given = true;
+}
+
 // Fused exchange over peer memory (Params::fused): the peers' buffers as
 // device pointers valid in this process (CUDA IPC or same-device buffers),
 // and the iteration loop as a CUDA graph WHILE { pull ; finalize } that runs
@@ -1366,6 +1409,8 @@ void part_set_peers(prgpu_session* s, int npeers, double* const* peer_contrib, d
     // only the peers that gather a source receive its row (PRGPU_NEED=0: all)
     P.need = nullptr;
     const char* nv = std::getenv("PRGPU_NEED");
+    if (s->need_given && npeers > 0 && !(nv && std::atoi(nv) == 0))
+        P.need = reinterpret_cast<const uint8_t*>(s->need.p); // a shard's, OR-reduced over the ranks
     // (a shard sees only its own rows' in-neighbours: every row goes to every peer)
     if (npeers > 0 && !(nv && std::atoi(nv) == 0) && s->g->shard_n <= 1) {
         const uint32_t nsrc = std::max<uint32_t>(s->g->nsrc, 1);

@@ -103,6 +103,20 @@ class _Part:
     def launch(self):
         check(lib().prgpu_part_launch(self._s), "part launch")
 
+    def shard(self) -> bool:
+        return self.g.shard_info()["nranks"] > 1
+
+    def need_bits(self):
+        """This rank's bit of the needed-only exchange mask (shard graphs:
+        from its own rows), one byte per source, as a device tensor."""
+        torch = self.torch
+        bits = torch.zeros((self.nsrc + 3) // 4 * 4, dtype=torch.uint8, device=self.contrib.device)
+        check(lib().prgpu_part_need_local(self._s, C.c_void_p(bits.data_ptr())), "need local")
+        return bits
+
+    def set_need(self, bits):
+        check(lib().prgpu_part_set_need(self._s, C.c_void_p(bits.data_ptr())), "set need")
+
     def dealt(self) -> bool:
         """Work dealt round-robin (fused partitions): rows are not one range."""
         d = C.c_int()
@@ -198,6 +212,10 @@ def _emulate_on(parts, alphas, max_iterations, want_ranks, g, fused=False, graph
     for p in parts:
         p.set_stream()
     if fused:
+        if len(parts) > 1 and parts[0].shard():  # the ranks' bits summed (disjoint: = OR)
+            total = sum(p.need_bits() for p in parts)
+            for p in parts:
+                p.set_need(total)
         for p in parts:
             peers = [q for q in parts if q is not p]
             p.set_peers([q.contrib.data_ptr() for q in peers], [q.partials.data_ptr() for q in peers],
@@ -356,6 +374,15 @@ def _run_peer_on(g, alphas, tolerance, norm, max_iterations, stop_mask, want_ran
     # others spinning in the finalize wait on arrivals that never come)
     setup_ok = True
     try:
+        if world > 1 and part.shard():  # the needed-only mask from every rank's rows
+            bits = part.need_bits()
+            if dist.get_backend() == "gloo":
+                hb = bits.cpu()
+                dist.all_reduce(hb, op=dist.ReduceOp.SUM)
+                bits.copy_(hb)
+            else:
+                dist.all_reduce(bits, op=dist.ReduceOp.SUM)
+            part.set_need(bits)
         part.set_peers(*peers)
         part.init()
         torch.cuda.current_stream(part.contrib.device).synchronize()

@@ -42,12 +42,17 @@ def test_shards_tile_the_graph_and_match_single_gpu(prl, monkeypatch, scale, nra
     with pytest.raises(ValueError):  # a shard cannot run alone
         prl.pagerank(shards[0], prl.PageRankConfig())
     single = prl.pagerank_batched(full, ALPHAS, 1e-9, prl.NormKind.L2, 300)
-    for fused in (True, False):
+    sent = {}
+    for fused, need in ((True, "1"), (True, "0"), (False, "1")):
+        monkeypatch.setenv("PRGPU_NEED", need)  # 0: every row to every peer
         res = distributed.emulate(shards[0], ALPHAS, nranks, 1e-9, prl.NormKind.L2, 300, want_ranks=True,
                                   fused=fused, shards=shards)
+        sent[(fused, need)] = res.sent_bytes
         for k, r in enumerate(single.results):
             assert int(res.iterations[k]) == r.iterations, (fused, k)
             assert float(np.max(np.abs(res.ranks[k] - r.ranks))) <= 1e-13, (fused, k)
+    # the OR-reduced needed-only mask (prgpu_part_need_local / set_need) sends fewer rows
+    assert 0 < sent[(True, "1")] < sent[(True, "0")]
 
 
 def device_bytes(prl, g=None, sess=None):
