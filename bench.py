@@ -594,9 +594,13 @@ def run_partitioned(args, cfg):
     if not args.no_e2e and not args.shard:  # (a shard holds one rank's edges: no host CSR to upload)
         import ctypes as C
         from paper_2108_02997_b200 import _lib
-        off = torch.from_numpy(g.in_offsets).pin_memory()
-        nbr = torch.from_numpy(g.in_neighbors).pin_memory()
-        deg = torch.from_numpy(g.out_degree).pin_memory()
+        # the host CSR downloaded straight into pinned buffers (no numpy copy:
+        # N ranks x 20 GB of host memory at C5)
+        off = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+        nbr = torch.empty(max(e, 1), dtype=torch.int32, pin_memory=True)
+        deg = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        _lib.check(_lib.lib().prgpu_graph_download(g.handle, off.data_ptr(), nbr.data_ptr(), deg.data_ptr(), None),
+                   "graph download")
         del g  # the e2e steps build their own device graph (C5: two would not fit)
         import gc
         gc.collect()
