@@ -271,6 +271,13 @@ struct LaneCfg {
     }
 };
 
+// CTAs per SM the 11/12-lane instances are compiled for (tuning builds:
+// -DPRGPU_K12_MINB=5/6 trade registers for resident warps)
+#ifndef PRGPU_K12_MINB
+#define PRGPU_K12_MINB 4
+#endif
+constexpr int kMinb12 = PRGPU_K12_MINB;
+
 // per-mode instance alternatives (tuning only)
 inline int k_variant(const char* name) {
     const char* v = std::getenv(name);
@@ -301,7 +308,7 @@ LaneCfg lane_cfg_t(int K, bool all_q) {
     if (K == 2) return wide_cfg<2, 1, 64, 4, 2, PATHS>(all_q);
     if (K <= 4) return wide_cfg<4, 1, 128, 4, 4, PATHS>(all_q);
     if (K <= 8) return wide_cfg<4, 2, 128, 4, 8, PATHS>(all_q);
-    if (K <= 12) return wide_cfg<8, 2, 128, 4, 12, PATHS>(all_q);
+    if (K <= 12) return wide_cfg<8, 2, 128, kMinb12, 12, PATHS>(all_q);
     return wide_cfg<8, 2, 128, 4, 16, PATHS>(all_q);
 }
 
@@ -338,7 +345,7 @@ bool mode_cfg(int KS, int kp, int win, bool all_q, LaneCfg& out, int k1_minb4 = 
         out = wide_cfg<4, 1, 128, 4, 4, PATHS>(all_q);
         return true;
     case 808: out = wide_cfg<4, 2, 128, 4, 8, PATHS>(all_q); return true;
-    case 1216: out = wide_cfg<8, 2, 128, 4, 12, PATHS>(all_q); return true;
+    case 1216: out = wide_cfg<8, 2, 128, kMinb12, 12, PATHS>(all_q); return true;
     case 1616: out = wide_cfg<8, 2, 128, 4, 16, PATHS>(all_q); return true;
     default: return false;
     }
