@@ -194,6 +194,11 @@ PRGPU_API int prgpu_session_results(prgpu_session* s, prgpu_result* out);
  * CUDA graph would run, one CUDA event pair per iteration on the session
  * stream.  x iterations it is at most the graph loop's time. */
 PRGPU_API int prgpu_session_time_pull(prgpu_session* s, int launches, double* ms_per_iteration);
+/* The last run's per-iteration device time of the pull kernels measured
+ * inside the CUDA graph (%globaltimer: the iteration's earliest CTA start to
+ * its finalizing CTA's end), ms; *filled = iterations written (<= cap).
+ * Single-GPU sessions. */
+PRGPU_API int prgpu_session_kernel_times(prgpu_session* s, double* ms_per_iteration, int cap, int* filled);
 PRGPU_API void prgpu_session_free(prgpu_session* s);
 
 /* ---- multi-GPU: 1D partition -----------------------------

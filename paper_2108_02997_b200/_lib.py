@@ -21,7 +21,7 @@ EXPORTS = [
     "prgpu_graph_build", "prgpu_graph_build_device", "prgpu_graph_from_csr",
     "prgpu_graph_generate_rmat", "prgpu_graph_generate_grid", "prgpu_graph_get_info",
     "prgpu_graph_generate_rmat_shard", "prgpu_graph_shard_info", "prgpu_device_bytes",
-    "prgpu_part_need_local", "prgpu_part_set_need",
+    "prgpu_part_need_local", "prgpu_part_set_need", "prgpu_session_kernel_times",
     "prgpu_graph_download", "prgpu_graph_free", "prgpu_pagerank", "prgpu_pagerank_observed",
     "prgpu_session_create", "prgpu_session_run", "prgpu_session_results",
     "prgpu_session_time_pull", "prgpu_session_free", "prgpu_error_norm", "prgpu_last_error",
@@ -95,6 +95,7 @@ def lib():
             "prgpu_graph_generate_rmat_shard": ([u32, u32, dbl, dbl, dbl, u64, i32, i32, i32, pp], i32),
             "prgpu_device_bytes": ([vp, vp, C.POINTER(u64), C.POINTER(u64)], i32),
             "prgpu_part_need_local": ([vp, vp], i32),
+            "prgpu_session_kernel_times": ([vp, C.POINTER(dbl), i32, C.POINTER(i32)], i32),
             "prgpu_part_set_need": ([vp, vp], i32),
             "prgpu_graph_shard_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(u32), C.POINTER(u32),
                                         C.POINTER(u64)], i32),

@@ -52,6 +52,7 @@ prgpu_session* session_create(prgpu_graph*, const prgpu_params*, bool, int, int,
 void part_sizes(prgpu_graph*, const prgpu_params*, int, uint64_t*, uint64_t*);
 uint64_t graph_device_bytes(const prgpu_graph*);
 void part_need_local(prgpu_session*, uint8_t*);
+int session_kernel_times(prgpu_session*, double*, int);
 void part_set_need(prgpu_session*, const uint8_t*);
 uint64_t session_device_bytes(const prgpu_session*);
 void part_exchange(prgpu_session*, prgpu_exchange*);
@@ -492,6 +493,13 @@ int prgpu_part_set_peers(prgpu_session* s, int npeers, double* const* peer_contr
         if (!s || (npeers > 0 && (!peer_contrib || !peer_partials || !peer_arrive)))
             prgpu::fail(PRGPU_EINVAL, "null argument");
         prgpu::part_set_peers(s, npeers, peer_contrib, peer_partials, peer_arrive, arrive);
+    });
+}
+
+int prgpu_session_kernel_times(prgpu_session* s, double* ms_per_iteration, int cap, int* filled) {
+    return guarded([&] {
+        if (!s || !ms_per_iteration || !filled) prgpu::fail(PRGPU_EINVAL, "null argument");
+        *filled = prgpu::session_kernel_times(s, ms_per_iteration, cap);
     });
 }
 

@@ -432,6 +432,7 @@ struct prgpu_session {
     Stream stream;
     DevBuf<double> rank, contrib, partials, trace, ref, chunk_acc;
     DevBuf<double> hot_part; // split pull: [nonempty rows][KS] hot partial sums
+    DevBuf<unsigned long long> ktime; // [max_iter][2] in-graph kernel start / end (ns)
     DevBuf<double> mode_contrib[kMaxModes]; // narrow modes' contribution buffers (after `stream`:
                                             // freed on it before it is destroyed)
     DevBuf<LaneState> lanes;
@@ -911,6 +912,11 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     if (const char* pf = std::getenv("PRGPU_PF")) P.pf = (uint32_t)std::atoi(pf);
     P.split = 0;
     P.hp = nullptr;
+    P.ktime = nullptr;
+    if (nranks == 0) { // single GPU: the in-graph kernel clock (finalize is the pull kernel's)
+        s->ktime.alloc(2 * (size_t)s->max_iter);
+        P.ktime = s->ktime.p;
+    }
     P.gpol = 0;
     if (const char* gp = std::getenv("PRGPU_GPOL")) P.gpol = (uint32_t)std::atoi(gp);
     P.hot_src = 0;
@@ -1614,6 +1620,25 @@ void session_init(prgpu_session* s) {
     if (s->P.fused && s->P.arrive) // peers add to it only after the caller's barrier
         PRGPU_CUDA(cudaMemsetAsync(s->P.arrive, 0, sizeof(unsigned int), s->cur()));
     if (s->host_frozen) std::fill(s->host_frozen, s->host_frozen + s->K, 0); // no kernel in flight
+    if (s->ktime.p) // starts = max (atomicMin), ends = 0
+        PRGPU_CUDA(cudaMemsetAsync(s->ktime.p, 0xFF, s->ktime.bytes(), s->cur()));
+}
+
+// per-iteration device time of the last run's pull kernels, measured inside
+// the CUDA graph (earliest CTA start to the finalizing CTA's end, ns clock):
+// returns the iterations filled
+int session_kernel_times(prgpu_session* s, double* ms, int cap) {
+    DeviceGuard dg(s->g->device);
+    if (!s->ktime.p) fail(PRGPU_EINVAL, "kernel_times: single-GPU sessions only");
+    std::vector<unsigned long long> t(s->ktime.n);
+    PRGPU_CUDA(cudaMemcpyAsync(t.data(), s->ktime.p, s->ktime.bytes(), cudaMemcpyDeviceToHost, s->cur()));
+    PRGPU_CUDA(cudaStreamSynchronize(s->cur()));
+    int n = 0;
+    for (int i = 0; i < s->max_iter && n < cap; ++i) {
+        if (t[2 * i] == ~0ull || t[2 * i + 1] == ~0ull || t[2 * i + 1] < t[2 * i]) break;
+        ms[n++] = (double)(t[2 * i + 1] - t[2 * i]) * 1e-6;
+    }
+    return n;
 }
 
 void launch_pull(prgpu_session* s) {
@@ -2161,7 +2186,8 @@ uint64_t session_device_bytes(const prgpu_session* s) {
     uint64_t b = s->rank.bytes() + s->contrib.bytes() + s->partials.bytes() + s->trace.bytes() + s->ref.bytes() +
                  s->chunk_acc.bytes() + s->hot_part.bytes() + s->lanes.bytes() + s->gs.bytes() +
                  s->chunk_row.bytes() + s->chunk_first.bytes() + s->packed_r0.bytes() + s->row_cnt.bytes() +
-                 s->task_list.bytes() + s->row_owner.bytes() + s->rank_partials.bytes() + s->need.bytes();
+                 s->task_list.bytes() + s->row_owner.bytes() + s->rank_partials.bytes() + s->need.bytes() +
+                 s->ktime.bytes();
     for (const auto& m : s->mode_contrib) b += m.bytes();
     return b;
 }

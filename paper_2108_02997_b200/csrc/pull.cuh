@@ -134,6 +134,10 @@ struct Params {
     // partial hp + the cold sum, then the epilogue), 0 = one pass
     int split;
     double* hp;                  // [nonempty rows][ks] hot partial sums
+    // in-graph kernel time per iteration (%globaltimer, ns): [iter][0] the
+    // earliest start of a CTA of the iteration's pull kernels, [iter][1] the
+    // finalizing CTA's end (single-GPU runs; prgpu_session_kernel_times)
+    unsigned long long* ktime;
     uint32_t gpol;               // gather L2 policy (tuning): 0 plain; 1 hot evict_last / cold
                                  // evict_first; 2 hot normal / cold evict_first; 3 hot evict_last / cold normal
     uint32_t skip_mask;          // profiling only (PRGPU_SKIP): 1 chunk, 2 packed, 4 empty tasks,
@@ -193,6 +197,12 @@ struct Params {
 };
 
 // ---- L2 residency control -------------------------------------------------------
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -1178,6 +1188,7 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     }
     __syncthreads();
     if (!s_flag) return;
+    if (P.ktime && tid == 0 && s_iter < P.gs->max_iter) atomicMin(P.ktime + 2 * s_iter, global_ns());
 
     // dynamic smem: [kWarps][SMEM_WARP + ASYNC_WARP] staged gathers, then the per-thread
     // partial columns when W >= 6
@@ -1300,6 +1311,7 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
         return;
     }
     finalize_lanes<KP, QM>(P, s_tot, s_c0, s_active, s_iter, P.mode_id);
+    if (P.ktime && tid == 0 && s_iter < P.gs->max_iter) P.ktime[2 * s_iter + 1] = global_ns();
 }
 
 // Mode change (Params::mode_id): copy the current contributions (parity of

@@ -761,6 +761,15 @@ class Session:
                     trace=trace[: r.run_iterations], loop_ms=r.loop_ms,
                     run_iterations=r.run_iterations)
 
+    def kernel_times(self) -> np.ndarray:
+        """The last run's per-iteration pull-kernel time (ms) measured inside
+        the CUDA graph (prgpu_session_kernel_times)."""
+        buf = np.zeros(4096, np.float64)
+        n = C.c_int()
+        check(lib().prgpu_session_kernel_times(self._s, buf.ctypes.data_as(C.POINTER(C.c_double)), buf.size,
+                                               C.byref(n)), "kernel times")
+        return buf[: n.value].copy()
+
     def time_pull(self, launches: int) -> float:
         ms = C.c_double()
         check(lib().prgpu_session_time_pull(self._s, launches, C.byref(ms)), "time_pull")
