@@ -92,6 +92,19 @@ GOLDEN_C5 = os.path.join(GOLD, "c5_rmat28.json")
 
 
 @pytest.mark.skipif(not os.path.exists(GOLDEN_C5), reason="c5 golden not generated (oracle/make_c5_golden.py)")
+def test_c5_rmat28_csr_hashes(prl, oracle):
+    """The device-built C5 graph, downloaded in the reference layout, hashes to
+    the golden's fingerprint (the reference-layout arrays the reference run
+    used: oracle/csr_inplace.hpp, itself pinned to build_csr at scales 22/26)."""
+    gold = json.load(open(GOLDEN_C5))["graph"]
+    g = prl.generate_rmat(28, 16, 0.57, 0.19, 0.19, 2108)
+    assert oracle.hash64(g.in_offsets) == gold["h_offsets"]
+    assert oracle.hash64(g.out_degree) == gold["h_degree"]
+    assert oracle.hash64(g.dangling) == gold["h_dangling"]
+    assert oracle.hash64(g.in_neighbors) == gold["h_neighbors"]
+
+
+@pytest.mark.skipif(not os.path.exists(GOLDEN_C5), reason="c5 golden not generated (oracle/make_c5_golden.py)")
 def test_c5_rmat28_k3_against_reference_run(prl):
     """BASELINE configs[4] against a full run of the reference's own
     pagerank() on the same graph (oracle/make_c5_golden.py; the graph's
