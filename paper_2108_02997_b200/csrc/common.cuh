@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -181,6 +182,30 @@ struct SourceSplit {
     DevBuf<uint32_t> col_hot, col_cold; // [e_hot + 16], [e_cold + 16]
 };
 
+// Segment plan of the hub rows (the segmented pull, DESIGN.md "Segmented hub
+// pull").  The source ids are cut into `S` segments — hot segments of
+// `seg_src` sources each (their contribution rows fit L2 together with the
+// streams), the last segment the cold rest when the table is longer — and
+// the in-edges of the rows with in-degree >= T (a prefix of the engine rows,
+// hence a prefix of col) are regrouped into pieces (row, segment): wide
+// pieces (> win edges) first, then small ones, each class segment-major,
+// rows ascending inside a segment, a piece's edges in their row order.  A
+// pull walks the pieces in that order, so at any time every warp gathers from
+// the same segment; each piece leaves a partial sum in slot row * S + seg,
+// and the row's epilogue adds its slots in segment order.  A hot-segment
+// piece of fewer than pmin edges is folded into the row's last-segment piece.
+struct SegPlan {
+    uint32_t seg_src = 0, S = 0, T = 0, win = 0, pmin = 0;
+    uint32_t n_rows = 0;    // segmented rows [0, n_rows)
+    uint64_t e_seg = 0;     // their edges: col[0, e_seg)
+    uint64_t e_wide = 0;    // edges in wide pieces
+    uint32_t n_wp = 0, n_sp = 0;
+    DevBuf<uint32_t> col;   // [e_seg + 16]
+    DevBuf<uint64_t> off;   // [n_wp + n_sp + 1] piece offsets into col (wide pieces first)
+    DevBuf<uint32_t> slot;  // [n_wp + n_sp] row * S + seg
+    uint64_t bytes() const { return col.bytes() + off.bytes() + slot.bytes(); }
+};
+
 } // namespace prgpu
 
 // The device graph: engine layout (relabelled) + the permutation back to the
@@ -215,9 +240,14 @@ struct prgpu_graph {
     // source splits built on demand by sessions (graph_source_split), by threshold
     std::mutex split_mu;
     std::map<uint32_t, std::unique_ptr<prgpu::SourceSplit>> splits;
+    // segment plans built on demand by sessions (graph_seg_plan), by (seg_src, S, T, win)
+    std::map<std::array<uint32_t, 5>, std::unique_ptr<prgpu::SegPlan>> seg_plans;
 };
 
 namespace prgpu {
 // the graph's hot/cold split at threshold `hot` (built on first use, cached)
 const SourceSplit& graph_source_split(prgpu_graph* g, uint32_t hot, cudaStream_t st);
+// the graph's segment plan (built on first use, cached); null when no row has T in-edges
+const SegPlan* graph_seg_plan(prgpu_graph* g, uint32_t seg_src, uint32_t S, uint32_t T, uint32_t win,
+                              uint32_t pmin, cudaStream_t st);
 } // namespace prgpu

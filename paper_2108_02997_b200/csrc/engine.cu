@@ -8,6 +8,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -258,8 +259,9 @@ struct LaneCfg {
     int KP() const { return LG * W; }
     size_t smem() const {
         const bool async = paths == 1 && kAsyncHub && LG > 1 && (KS == 2 || KS == 4); // pull.cuh async_hub
+        const bool packs = paths != 3 && (paths & (2 | 8)) != 0; // packed_pipe instances (pull.cuh PACKS)
         const size_t staged = KP() == 1 ? (size_t)kWarps * 2 * WIN * sizeof(double) // STAGED
-                              : paths == 2 ? (size_t)kWarps *
+                              : packs ? (size_t)kWarps *
                                                  ((kStagedWide && LG == 4 && KS == 4) ? 2 * WIN * KS
                                                                                      : kPackOff + (2 * WIN + 8) / 2) *
                                                  sizeof(double)
@@ -439,6 +441,13 @@ struct prgpu_session {
     DevBuf<GlobalState> gs;
     DevBuf<uint32_t> chunk_row, chunk_first, packed_r0;
     DevBuf<unsigned int> row_cnt;
+    // segmented hub pull (SegPlan): task tables over the plan's pieces, the
+    // wide pieces' chunk hand-off state and the piece partial sums
+    const SegPlan* seg = nullptr;
+    DevBuf<uint32_t> seg_chunk_row, seg_chunk_first, seg_packed_r0;
+    DevBuf<double> seg_chunk_acc, pacc;
+    DevBuf<unsigned int> seg_row_cnt;
+    uint32_t seg_n_wchunk = 0, seg_n_runs = 0, seg_n_comb = 0, seg_chunk_t0 = 0;
     std::vector<LaneState> lanes_host; // device slot order
     std::vector<int> user_of;          // caller lane of each device slot
     cudaGraph_t graph = nullptr;
@@ -635,6 +644,120 @@ void build_tasks(prgpu_session* s) {
     P.part_mode = 0;
     P.part_rank = 0;
     P.nranks = 1;
+}
+
+// Segmented hub pull (SegPlan, common.cuh; single-GPU sessions): task tables
+// over the plan's pieces.  Wide pieces are cut into chunk tasks exactly like
+// hub rows (same chunk size, same hand-off), small pieces are grouped into
+// runs exactly like packed rows; the rows' epilogues become combine tasks.
+// On by default when the contribution table is at least three segments long
+// (measured on B200: C5 620 -> 500 ms per
+// sweep, RMAT-24 x 11 lanes -5 %, C4 -3 %; C2's 194 MB table +5 %, off).
+// PRGPU_SEG=0/1 forces it off/on, PRGPU_SEG_KB the segment size (KB of the
+// run's widest contribution rows), PRGPU_SEG_HOT the number of L2-sized
+// segments before the cold rest, PRGPU_SEG_T the least in-degree of a
+// segmented row, PRGPU_SEG_PMIN the smallest hot-segment piece kept.
+void build_seg_tasks(prgpu_session* s, int nranks) {
+    prgpu_graph* g = s->g;
+    cudaStream_t st = s->stream;
+    if (nranks != 0 || g->shard_n > 1 || g->locality || s->n_long == 0) return;
+    auto env_u = [](const char* name, uint64_t dflt) -> uint64_t {
+        const char* v = std::getenv(name);
+        return v ? (uint64_t)std::atoll(v) : dflt;
+    };
+    const uint64_t row_bytes = (uint64_t)s->cfg.KS * sizeof(double);
+    // 64 MB: the largest slice of the table the L2 keeps (profiles/r1_gather_ceiling.md)
+    const uint64_t seg_bytes = std::max<uint64_t>(env_u("PRGPU_SEG_KB", 64u << 10) << 10, row_bytes);
+    const uint64_t table = (uint64_t)g->nsrc * row_bytes;
+    const char* en = std::getenv("PRGPU_SEG");
+    const bool want = en ? std::atoi(en) != 0 : table >= 3 * seg_bytes;
+    if (!want) return;
+    const uint32_t win = (uint32_t)s->cfg.WIN;
+    const uint32_t seg_src = (uint32_t)std::max<uint64_t>(1, seg_bytes / row_bytes);
+    const uint32_t hot = (uint32_t)std::min<uint64_t>(63, std::max<uint64_t>(1, env_u("PRGPU_SEG_HOT", 16)));
+    const uint32_t s_all = (uint32_t)((table + seg_bytes - 1) / seg_bytes);
+    // the last segment is the cold rest: sources past the hot segments, and
+    // the hot-segment pieces too small to be worth a partial (pmin)
+    if (s_all < 2) return; // the whole table is one segment
+    const uint32_t pmin = (uint32_t)env_u("PRGPU_SEG_PMIN", 0); // measured: folding small pieces loses (C5 +1 % at 8, +4 % at 16)
+    const uint32_t S = (s_all <= hot && pmin == 0) ? s_all : std::min(s_all, hot) + 1;
+    // every hub row by default (C5: T = 512 leaves the rows of 129..511 in-edges to miss: 595 vs 500 ms)
+    const uint32_t T = (uint32_t)std::max<uint64_t>(env_u("PRGPU_SEG_T", 0), (uint64_t)win + 1);
+    const SegPlan* sp = graph_seg_plan(g, seg_src, S, T, win, pmin, st);
+    if (!sp) return;
+    s->seg = sp;
+    const uint32_t emax = s->P.chunk;
+    // chunk tasks of the wide pieces
+    const uint32_t nw = sp->n_wp;
+    DevBuf<uint64_t> first((size_t)nw + 1);
+    chunk_counts<<<blocks_for((uint64_t)nw + 1), kNT, 0, st>>>(sp->off.p, nw, emax, first.p);
+    PRGPU_LAUNCHED("chunk_counts");
+    {
+        size_t tmp = 0;
+        PRGPU_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, first.p, first.p, (int64_t)nw + 1, st));
+        DevBuf<char> t(std::max<size_t>(tmp, 1));
+        PRGPU_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, first.p, first.p, (int64_t)nw + 1, st));
+        g_launches.fetch_add(1);
+    }
+    uint64_t n_chunk = 0;
+    PRGPU_CUDA(cudaMemcpyAsync(&n_chunk, first.p + nw, 8, cudaMemcpyDeviceToHost, st));
+    // the hub rows' own chunk tasks start after the segmented rows'
+    PRGPU_CUDA(cudaMemcpyAsync(&s->seg_chunk_t0, s->chunk_first.p + sp->n_rows, 4, cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    s->seg_chunk_first.alloc((size_t)nw + 1);
+    s->seg_chunk_row.alloc(std::max<uint64_t>(n_chunk, 1));
+    chunk_fill<<<blocks_for((uint64_t)nw + 1), kNT, 0, st>>>(first.p, nw, s->seg_chunk_first.p, s->seg_chunk_row.p);
+    PRGPU_LAUNCHED("chunk_fill");
+    s->seg_chunk_acc.alloc(std::max<uint64_t>(n_chunk, 1) * s->KP);
+    s->seg_row_cnt.alloc(std::max<uint32_t>(nw, 1));
+    PRGPU_CUDA(cudaMemsetAsync(s->seg_row_cnt.p, 0, std::max<uint32_t>(nw, 1) * 4, st));
+    s->seg_n_wchunk = (uint32_t)n_chunk;
+    // runs of small pieces
+    const uint32_t lo = nw, hi = nw + sp->n_sp;
+    uint64_t np = 0;
+    if (hi > lo) {
+        const uint32_t rows = hi - lo;
+        const uint32_t cmin = std::max<uint32_t>(1, (win + 31) / 32);
+        DevBuf<uint64_t> cost((size_t)rows + 1);
+        packed_costs<<<blocks_for((uint64_t)rows + 1), kNT, 0, st>>>(sp->off.p, lo, hi, cmin, cost.p);
+        PRGPU_LAUNCHED("packed_costs");
+        size_t tmp = 0;
+        PRGPU_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cost.p, cost.p, (int64_t)rows + 1, st));
+        DevBuf<char> t(std::max<size_t>(tmp, 1));
+        PRGPU_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, cost.p, cost.p, (int64_t)rows + 1, st));
+        g_launches.fetch_add(1);
+        uint64_t total = 0;
+        PRGPU_CUDA(cudaMemcpyAsync(&total, cost.p + rows, 8, cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaStreamSynchronize(st));
+        np = (total + win - 1) / win;
+        s->seg_packed_r0.alloc(np + 1);
+        packed_bounds<<<blocks_for(rows), kNT, 0, st>>>(cost.p, lo, hi, win, (uint32_t)np, s->seg_packed_r0.p);
+        PRGPU_LAUNCHED("packed_bounds");
+        PRGPU_CUDA(cudaStreamSynchronize(st));
+    } else {
+        s->seg_packed_r0.alloc(1);
+    }
+    s->seg_n_runs = (uint32_t)np;
+    // piece partial sums: a slot per (row, segment), zero where a row has no piece
+    s->pacc.alloc((size_t)sp->n_rows * S * s->KP);
+    PRGPU_CUDA(cudaMemsetAsync(s->pacc.p, 0, s->pacc.bytes(), st));
+    const uint32_t cr = 2 * (32 / (uint32_t)s->cfg.LG);
+    s->seg_n_comb = (sp->n_rows + cr - 1) / cr;
+    Params& P = s->P;
+    P.seg_off = sp->off.p;
+    P.seg_col = sp->col.p;
+    P.seg_slot = sp->slot.p;
+    P.seg_chunk_row = s->seg_chunk_row.p;
+    P.seg_chunk_first = s->seg_chunk_first.p;
+    P.seg_packed_r0 = s->seg_packed_r0.p;
+    P.seg_chunk_acc = s->seg_chunk_acc.p;
+    P.seg_row_cnt = s->seg_row_cnt.p;
+    P.pacc = s->pacc.p;
+    P.n_seg_rows = sp->n_rows;
+    P.seg_S = S;
+    P.pacc_stride = (uint32_t)s->KP;
+    P.seg_pre = 0;
+    P.seg_cr = cr;
 }
 
 // ---- 1D partition (multi-GPU): contiguous task ranges with equal cost, cut at
@@ -928,6 +1051,8 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     ph.mark("params");
     build_tasks(s.get());
     ph.mark("tasks");
+    build_seg_tasks(s.get(), nranks);
+    ph.mark("seg tasks");
     if (nranks >= 1) { // partition session (nranks == 0: the fused single-GPU run)
         if (rank < 0 || rank >= nranks) fail(PRGPU_EINVAL, "partition: rank out of range");
         plan_partition(s.get(), nranks);
@@ -969,6 +1094,9 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     // partitions run the one base kernel; K = 1 see below.
     using ModeList = std::vector<std::pair<int, std::pair<LaneCfg, LaneCfg>>>; // kp, (chunk, packed)
     ModeList modes;
+    // segmented sessions, per mode: wide-piece chunks + hub chunks, small-piece
+    // runs, combine + packed + empty (pull_kernel PATHS 5, 8, 18)
+    std::vector<std::array<LaneCfg, 3>> seg_cfgs;
     {
         const char* sp = std::getenv("PRGPU_SPLIT");   // =0: base kernel only (tuning)
         const char* mm = std::getenv("PRGPU_MODES");   // =0: widest mode only (tuning)
@@ -979,7 +1107,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         // and PRGPU_K1MINB (bit 0 hub, bit 1 packed kernel) override (tuning).
         const char* ks1 = std::getenv("PRGPU_K1SPLIT");
         const bool k1auto = P.n_chunk == 0 ? g->e >= (1ull << 24) : g->e >= (1ull << 29);
-        const bool k1split = s->K == 1 && (ks1 ? std::atoi(ks1) == 1 : k1auto);
+        const bool k1split = s->K == 1 && (s->seg || (ks1 ? std::atoi(ks1) == 1 : k1auto));
         const char* km = std::getenv("PRGPU_K1MINB");
         const int k1_minb4 = km ? std::atoi(km) : (P.n_chunk == 0 ? 2 : 0);
         const bool modal = (s->K > 1 || k1split) && !(sp && std::atoi(sp) == 0);
@@ -990,11 +1118,20 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
                 LaneCfg a, b;
                 const int ks = kp == wide ? s->cfg.KS : kp;
                 if (mode_cfg<1>(ks, kp, s->cfg.WIN, s->all_q, a, k1_minb4) &&
-                    mode_cfg<2>(ks, kp, s->cfg.WIN, s->all_q, b, k1_minb4))
+                    mode_cfg<2>(ks, kp, s->cfg.WIN, s->all_q, b, k1_minb4)) {
                     modes.push_back({kp, {a, b}});
+                    if (s->seg) {
+                        std::array<LaneCfg, 3> sc;
+                        mode_cfg<5>(ks, kp, s->cfg.WIN, s->all_q, sc[0], k1_minb4);
+                        mode_cfg<8>(ks, kp, s->cfg.WIN, s->all_q, sc[1], k1_minb4);
+                        mode_cfg<18>(ks, kp, s->cfg.WIN, s->all_q, sc[2], k1_minb4);
+                        seg_cfgs.push_back(sc);
+                    }
+                }
             }
             if (modes.empty() || modes.back().first != wide) modes.clear(); // no instances: base kernel
         }
+        if (modes.empty()) s->seg = nullptr; // the segmented pull needs the split iteration
     }
     P.part_kp = (uint32_t)KP;
     // contribution buffers of the narrow modes: after the run's own buffers
@@ -1059,6 +1196,53 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         const uint32_t a0 = std::min(Q.task_begin, T1), a1 = std::min(Q.task_end, T1);
         const uint32_t b0 = std::max(Q.task_begin, T1), b1 = std::max(Q.task_end, b0);
         for (int m = 0; m < (int)ml.size(); ++m) {
+            if (s->seg) { // segmented: wide pieces + the other hub rows' chunks; small pieces; the rest
+                const LaneCfg& A = seg_cfgs[m][0];
+                const LaneCfg& A2 = seg_cfgs[m][1];
+                const LaneCfg& B = seg_cfgs[m][2];
+                size_t sa = 0, sa2 = 0, sb = 0;
+                const uint32_t t0 = std::min(s->seg_chunk_t0, T1);
+                const uint32_t GA = grid_for_cfg(A, (uint64_t)s->seg_n_wchunk + (T1 - t0), sa);
+                const uint32_t GA2 = s->seg_n_runs ? grid_for_cfg(A2, s->seg_n_runs, sa2) : 0;
+                const uint32_t GB = grid_for_cfg(B, (uint64_t)s->seg_n_comb + (b1 - b0), sb);
+                Params PM = Q;
+                PM.mode_id = m;
+                PM.cbase = Q.mode_cbase[m];
+                PM.cold_off[0] = Q.mode_cold_off[m][0];
+                PM.cold_off[1] = Q.mode_cold_off[m][1];
+                if (m + 1 < (int)ml.size()) { // narrow mode: repack on entry
+                    PM.G = (uint32_t)dev_sms * 8;
+                    out.push_back({nullptr, PM, 0, true});
+                }
+                Params PA = PM, PA2 = PM, PB = PM;
+                PA.gtot = PA2.gtot = PB.gtot = GA + GB;
+                PA.task_begin = t0;
+                PA.task_end = T1;
+                PA.seg_pre = s->seg_n_wchunk;
+                PA.seg_grab = 1;
+                PA2.seg_grab = 4;
+                if (const char* gr = std::getenv("PRGPU_SEG_GRAB")) PA2.seg_grab = (uint32_t)std::max(1, std::atoi(gr));
+                PA.G = GA;
+                PA.pcol0 = 0;
+                PA.no_finalize = 1;
+                out.push_back({A.fn, PA, sa, false});
+                if (GA2) {
+                    PA2.task_begin = PA2.task_end = 0;
+                    PA2.seg_pre = s->seg_n_runs;
+                    PA2.G = GA2;
+                    PA2.pcol0 = 0;
+                    PA2.no_finalize = 1;
+                    out.push_back({A2.fn, PA2, sa2, false});
+                }
+                PB.task_begin = b0;
+                PB.task_end = b1;
+                PB.seg_pre = s->seg_n_comb;
+                PB.G = GB;
+                PB.pcol0 = GA;
+                out.push_back({B.fn, PB, sb, false});
+                cols = std::max(cols, (size_t)kNQ * ml[m].first * (GA + GB));
+                continue;
+            }
             const LaneCfg& A = ml[m].second.first;
             const LaneCfg& B = ml[m].second.second;
             size_t sa = 0, sb = 0;
@@ -2180,6 +2364,7 @@ uint64_t graph_device_bytes(const prgpu_graph* g) {
     for (const auto& kv : g->splits)
         b += kv.second->off_hot.bytes() + kv.second->off_cold.bytes() + kv.second->col_hot.bytes() +
              kv.second->col_cold.bytes();
+    for (const auto& kv : g->seg_plans) b += kv.second->bytes();
     return b;
 }
 uint64_t session_device_bytes(const prgpu_session* s) {
@@ -2187,7 +2372,8 @@ uint64_t session_device_bytes(const prgpu_session* s) {
                  s->chunk_acc.bytes() + s->hot_part.bytes() + s->lanes.bytes() + s->gs.bytes() +
                  s->chunk_row.bytes() + s->chunk_first.bytes() + s->packed_r0.bytes() + s->row_cnt.bytes() +
                  s->task_list.bytes() + s->row_owner.bytes() + s->rank_partials.bytes() + s->need.bytes() +
-                 s->ktime.bytes();
+                 s->ktime.bytes() + s->seg_chunk_row.bytes() + s->seg_chunk_first.bytes() +
+                 s->seg_packed_r0.bytes() + s->seg_chunk_acc.bytes() + s->pacc.bytes() + s->seg_row_cnt.bytes();
     for (const auto& m : s->mode_contrib) b += m.bytes();
     return b;
 }

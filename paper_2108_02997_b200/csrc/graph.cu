@@ -1182,6 +1182,214 @@ const SourceSplit& graph_source_split(prgpu_graph* g, uint32_t hot, cudaStream_t
     return *(g->splits[hot] = std::move(sp));
 }
 
+// ---- segment plan (SegPlan, common.cuh) ------------------------------------------
+constexpr uint32_t kSegSlab = 32768; // edges per CTA of the counting / key passes
+
+__device__ __forceinline__ uint32_t seg_of(uint32_t src, uint32_t seg_src, uint32_t S) {
+    const uint32_t q = src / seg_src;
+    return q < S ? q : S - 1;
+}
+
+// One CTA per slab of col[0, e_seg): for every row crossing the slab, the
+// number of its edges per segment (COUNT: added to cnt[seg][row], integer
+// atomics) or, once the counts are complete, every edge's sort key
+// class * S + seg (class 1: the edge's piece has <= win edges).
+template <bool KEYS>
+__global__ void __launch_bounds__(256) seg_slab_kernel(const uint64_t* __restrict__ row_off,
+                                                       const uint32_t* __restrict__ col, uint32_t n_rows,
+                                                       uint64_t e_seg, uint32_t seg_src, uint32_t S, uint32_t win,
+                                                       uint32_t* __restrict__ cnt, uint8_t* __restrict__ keys,
+                                                       const uint64_t* __restrict__ merged) {
+    __shared__ uint32_t s_h[64];
+    __shared__ uint32_t s_row;
+    const uint64_t lo = (uint64_t)blockIdx.x * kSegSlab, hi = min(lo + kSegSlab, e_seg);
+    if (threadIdx.x == 0) { // the row holding edge lo: last r with row_off[r] <= lo
+        uint32_t a = 0, b = n_rows;
+        while (b - a > 1) {
+            const uint32_t m = a + (b - a) / 2;
+            if (row_off[m] <= lo) a = m;
+            else b = m;
+        }
+        s_row = a;
+    }
+    __syncthreads();
+    for (uint32_t r = s_row; r < n_rows; ++r) {
+        const uint64_t r0 = row_off[r], r1 = row_off[r + 1];
+        if (r0 >= hi) break;
+        const uint64_t a = max(r0, lo), b = min(r1, hi);
+        const uint64_t mm = KEYS ? merged[r] : 0ull; // segments whose (small) piece went to the cold piece
+        if (threadIdx.x < 64)
+            s_h[threadIdx.x] = (KEYS && threadIdx.x < S && cnt[(size_t)threadIdx.x * n_rows + r] <= win) ? S : 0u;
+        __syncthreads();
+        for (uint64_t j = a + threadIdx.x; j < b; j += 256) {
+            uint32_t sg = seg_of(col[j], seg_src, S);
+            if (KEYS && ((mm >> sg) & 1ull)) sg = S - 1;
+            if (KEYS) keys[j] = (uint8_t)(sg + s_h[sg]);
+            else atomicAdd(&s_h[sg], 1u);
+        }
+        __syncthreads();
+        if (!KEYS && threadIdx.x < S && s_h[threadIdx.x])
+            atomicAdd(&cnt[(size_t)threadIdx.x * n_rows + r], s_h[threadIdx.x]);
+        __syncthreads();
+    }
+}
+
+// A hot-segment piece of fewer than pmin edges costs more (its offsets, its
+// partial's round trip) than the misses it saves: its edges join the row's
+// piece in the last (cold) segment; merged[row] keeps the segments folded.
+__global__ void seg_merge_small(uint32_t* __restrict__ cnt, uint32_t n_rows, uint32_t S, uint32_t pmin,
+                                uint64_t* __restrict__ merged) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += gridDim.x * blockDim.x) {
+        uint64_t m = 0;
+        uint32_t cold = 0;
+        for (uint32_t sg = 0; sg + 1 < S; ++sg) {
+            const uint32_t c = cnt[(size_t)sg * n_rows + r];
+            if (c && c < pmin) {
+                cold += c;
+                cnt[(size_t)sg * n_rows + r] = 0;
+                m |= 1ull << sg;
+            }
+        }
+        if (cold) cnt[(size_t)(S - 1) * n_rows + r] += cold;
+        merged[r] = m;
+    }
+}
+
+// flattened pieces f = (class * S + seg) * n_rows + row, f in [0, 2F]: length
+// and presence (element 2F is the sentinel that receives the totals)
+__global__ void seg_piece_len(const uint32_t* __restrict__ cnt, uint64_t F, uint32_t win,
+                              uint64_t* __restrict__ len, uint64_t* __restrict__ flag) {
+    for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f <= 2 * F;
+         f += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t c = 0;
+        if (f < 2 * F) {
+            c = cnt[f < F ? f : f - F];
+            const bool small = c <= win;
+            if (small != (f >= F)) c = 0;
+        }
+        len[f] = c;
+        flag[f] = c != 0;
+    }
+}
+
+__global__ void seg_piece_fill(const uint64_t* __restrict__ start, const uint64_t* __restrict__ pidx,
+                               const uint32_t* __restrict__ cnt, uint64_t F, uint32_t n_rows, uint32_t S,
+                               uint32_t win, uint64_t* __restrict__ off, uint32_t* __restrict__ slot) {
+    for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f <= 2 * F;
+         f += (uint64_t)gridDim.x * blockDim.x) {
+        if (f == 2 * F) {
+            off[pidx[f]] = start[f];
+            continue;
+        }
+        const uint64_t g = f < F ? f : f - F;
+        const uint32_t c = cnt[g];
+        if (c == 0 || ((c <= win) != (f >= F))) continue;
+        const uint64_t p = pidx[f];
+        off[p] = start[f];
+        slot[p] = (uint32_t)(g % n_rows) * S + (uint32_t)(g / n_rows);
+    }
+}
+
+__global__ void count_rows_ge(const uint64_t* __restrict__ row_off, uint32_t n, uint32_t T,
+                              unsigned int* __restrict__ out) {
+    unsigned int c = 0;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+        c += (row_off[r + 1] - row_off[r]) >= T;
+    if (c) atomicAdd(out, c);
+}
+
+const SegPlan* graph_seg_plan(prgpu_graph* g, uint32_t seg_src, uint32_t S, uint32_t T, uint32_t win,
+                              uint32_t pmin, cudaStream_t st) {
+    if (S < 1 || S > 64 || seg_src == 0 || T <= win) fail(PRGPU_EINVAL, "segment plan: bad parameters");
+    if (g->shard_n > 1 || g->locality) return nullptr; // rows not in degree order / col not whole
+    std::lock_guard<std::mutex> lock(g->split_mu);
+    const std::array<uint32_t, 5> key{seg_src, S, T, win, pmin};
+    auto it = g->seg_plans.find(key);
+    if (it != g->seg_plans.end()) return it->second->n_rows ? it->second.get() : nullptr;
+    AllocScope scope(st);
+    PhaseLog ph("segplan", st);
+    auto sp = std::make_unique<SegPlan>();
+    sp->seg_src = seg_src;
+    sp->S = S;
+    sp->T = T;
+    sp->win = win;
+    sp->pmin = pmin;
+    // rows are in in-degree order: the rows with >= T in-edges are a prefix
+    {
+        DevBuf<unsigned int> c(1);
+        PRGPU_CUDA(cudaMemsetAsync(c.p, 0, 4, st));
+        count_rows_ge<<<grid_for(g->n), kThreads, 0, st>>>(g->row_off.p, g->n, T, c.p);
+        PRGPU_LAUNCHED("count_rows_ge");
+        PRGPU_CUDA(cudaMemcpyAsync(&sp->n_rows, c.p, 4, cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaStreamSynchronize(st));
+    }
+    if (sp->n_rows == 0) {
+        g->seg_plans[key] = std::move(sp);
+        return nullptr;
+    }
+    const uint32_t nr = sp->n_rows;
+    PRGPU_CUDA(cudaMemcpyAsync(&sp->e_seg, g->row_off.p + nr, 8, cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaStreamSynchronize(st));
+    const uint64_t es = sp->e_seg, F = (uint64_t)S * nr;
+    const unsigned slabs = (unsigned)((es + kSegSlab - 1) / kSegSlab);
+    DevBuf<uint32_t> cnt(F);
+    PRGPU_CUDA(cudaMemsetAsync(cnt.p, 0, F * 4, st));
+    seg_slab_kernel<false><<<slabs, 256, 0, st>>>(g->row_off.p, g->col.p, nr, es, seg_src, S, win, cnt.p, nullptr,
+                                                  nullptr);
+    PRGPU_LAUNCHED("seg_slab_kernel<count>");
+    DevBuf<uint64_t> merged(nr);
+    seg_merge_small<<<grid_for(nr), kThreads, 0, st>>>(cnt.p, nr, S, pmin, merged.p);
+    PRGPU_LAUNCHED("seg_merge_small");
+    ph.mark("count");
+    {
+        DevBuf<uint8_t> kin(es), kout(es);
+        seg_slab_kernel<true><<<slabs, 256, 0, st>>>(g->row_off.p, g->col.p, nr, es, seg_src, S, win, cnt.p, kin.p,
+                                                     merged.p);
+        PRGPU_LAUNCHED("seg_slab_kernel<keys>");
+        sp->col.alloc(es + 16);
+        PRGPU_CUDA(cudaMemsetAsync(sp->col.p + es, 0, 16 * 4, st));
+        // one stable radix pass over the (class, segment) key keeps rows, and
+        // each row's edge order, inside every (class, segment) group
+        const int bits = (int)bits_for(2ull * S);
+        size_t tmp = 0;
+        PRGPU_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin.p, kout.p, g->col.p, sp->col.p, (int64_t)es, 0,
+                                                   bits, st));
+        DevBuf<char> t(std::max<size_t>(tmp, 1));
+        PRGPU_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, kin.p, kout.p, g->col.p, sp->col.p, (int64_t)es, 0,
+                                                   bits, st));
+        g_launches.fetch_add(1);
+        ph.mark("keys + sort");
+    }
+    {
+        DevBuf<uint64_t> len(2 * F + 1), flag(2 * F + 1);
+        seg_piece_len<<<grid_for(2 * F + 1), kThreads, 0, st>>>(cnt.p, F, win, len.p, flag.p);
+        PRGPU_LAUNCHED("seg_piece_len");
+        exclusive_scan_u64(len.p, 2 * F + 1, st);
+        exclusive_scan_u64(flag.p, 2 * F + 1, st);
+        uint64_t np = 0, nw = 0;
+        PRGPU_CUDA(cudaMemcpyAsync(&np, flag.p + 2 * F, 8, cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaMemcpyAsync(&nw, flag.p + F, 8, cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaMemcpyAsync(&sp->e_wide, len.p + F, 8, cudaMemcpyDeviceToHost, st));
+        PRGPU_CUDA(cudaStreamSynchronize(st));
+        sp->n_wp = (uint32_t)nw;
+        sp->n_sp = (uint32_t)(np - nw);
+        sp->off.alloc(np + 1);
+        sp->slot.alloc(std::max<uint64_t>(np, 1));
+        seg_piece_fill<<<grid_for(2 * F + 1), kThreads, 0, st>>>(len.p, flag.p, cnt.p, F, nr, S, win, sp->off.p,
+                                                                  sp->slot.p);
+        PRGPU_LAUNCHED("seg_piece_fill");
+        PRGPU_CUDA(cudaStreamSynchronize(st));
+        ph.mark("pieces");
+    }
+    if (std::getenv("PRGPU_TIMING_LOG"))
+        std::fprintf(stderr, "[segplan] rows %u edges %llu (%.1f%% of E) S %u seg_src %u wide pieces %u (%llu edges) small %u\n",
+                     nr, (unsigned long long)es, 100.0 * (double)es / (double)std::max<uint64_t>(g->e, 1), S, seg_src,
+                     sp->n_wp, (unsigned long long)sp->e_wide, sp->n_sp);
+    SegPlan* out = sp.get();
+    g->seg_plans[key] = std::move(sp);
+    return out;
+}
+
 std::unique_ptr<prgpu_graph> graph_generate_rmat(uint32_t scale, uint32_t ef, double a, double b,
                                                  double c, uint64_t seed, int device,
                                                  cudaStream_t st) {

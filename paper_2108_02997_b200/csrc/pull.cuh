@@ -95,6 +95,10 @@ struct GlobalState {
     int max_iter;
     int mode;   // lane-width mode of the next iteration (see Params::mode_id)
     int layout; // mode whose contribution buffer holds the current contributions
+    // segmented pull: next piece task of the wide-piece and the small-piece
+    // kernels (handed out in order, so every warp works in the same source
+    // segment at any time); the finalizer resets them
+    unsigned int seg_next[2];
 };
 
 constexpr int kMaxModes = 5;
@@ -194,7 +198,25 @@ struct Params {
     const uint32_t* task_list;
     uint32_t list_begin, list_end;
     const uint8_t* row_owner;
+    // segmented hub pull (SegPlan, common.cuh): the in-edges of rows [0,
+    // n_seg_rows) regrouped into (row, source segment) pieces that are pulled
+    // segment by segment, so the contribution rows gathered at any time are
+    // one L2-sized slice of the table.  A piece leaves its partial sum in
+    // pacc[slot]; the rows' epilogues (combine tasks) add their slots in
+    // segment order.  seg_pre: the kernel's leading seg tasks (PATHS 4: chunks
+    // of wide pieces, 8: runs of small pieces, 16: combine tasks).
+    const uint64_t* seg_off;       // [pieces + 1] into seg_col (wide pieces first)
+    const uint32_t* seg_col;
+    const uint32_t* seg_slot;      // [pieces] row * seg_S + segment
+    const uint32_t* seg_chunk_row; // [seg chunks] wide piece of each chunk task
+    const uint32_t* seg_chunk_first; // [wide pieces + 1]
+    const uint32_t* seg_packed_r0; // [runs + 1] piece ranges of the small-piece runs
+    double* seg_chunk_acc;         // [seg chunks][KP]
+    unsigned int* seg_row_cnt;     // [wide pieces]
+    double* pacc;                  // [n_seg_rows * seg_S][pacc_stride]
+    uint32_t n_seg_rows, seg_S, pacc_stride, seg_pre, seg_cr, seg_grab;
 };
+
 
 // ---- L2 residency control -------------------------------------------------------
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -306,8 +328,31 @@ constexpr bool async_hub() { return kAsyncHub && LG > 1 && (KS == 2 || KS == 4);
 
 // gathers: plain read-only loads (measured: L2 residency hints on the
 // contributions did not pay, and the policy/address arithmetic per edge did)
+// PRGPU_GATHER_LTC (tuning builds: 64 / 128 / 256): the gathers carry an L2
+// prefetch-size qualifier.  A missed 32-byte row moves 128 bytes of DRAM with
+// a plain load and 64 with .L2::64B (scripts/microbench_fetch_size.cu); the
+// random-row rate itself (~36 G rows/s) does not change.
+#ifndef PRGPU_GATHER_LTC
+#define PRGPU_GATHER_LTC 0
+#endif
+#define PRGPU_STR2(x) #x
+#define PRGPU_STR(x) PRGPU_STR2(x)
 template <int W>
 __device__ __forceinline__ void load_w(const double* __restrict__ p, double (&v)[W]) {
+#if PRGPU_GATHER_LTC != 0
+    if constexpr (W % 2 == 0) {
+#pragma unroll
+        for (int w = 0; w < W; w += 2)
+            asm("ld.global.nc.L2::" PRGPU_STR(PRGPU_GATHER_LTC) "B.v2.f64 {%0,%1}, [%2];"
+                : "=d"(v[w]), "=d"(v[w + 1])
+                : "l"(p + w));
+    } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+            asm("ld.global.nc.L2::" PRGPU_STR(PRGPU_GATHER_LTC) "B.f64 %0, [%1];" : "=d"(v[w]) : "l"(p + w));
+    }
+    return;
+#endif
     if constexpr (W % 2 == 0) {
 #pragma unroll
         for (int w = 0; w < W; w += 2) {
@@ -623,9 +668,10 @@ struct Warp {
 
     // Accumulate edges [lo, hi) into acc with 128-bit colidx loads; slot s
     // takes quads s, s+ES, ... (fixed order: quad-major, then position).
-    __device__ __forceinline__ void accumulate(uint64_t lo, uint64_t hi, double (&acc)[W]) const {
+    __device__ __forceinline__ void accumulate(const uint32_t* __restrict__ col, uint64_t lo, uint64_t hi,
+                                               double (&acc)[W]) const {
         const uint64_t sp = stream_policy(P);
-        const uint32_t* __restrict__ cb = P.col + (lo & ~3ull);
+        const uint32_t* __restrict__ cb = col + (lo & ~3ull);
         const uint32_t off0 = (uint32_t)(lo & 3ull);
         const uint32_t ne = (uint32_t)(hi - lo) + off0; // <= 2*WIN + 3
         const bool ok = slice_live();
@@ -669,10 +715,11 @@ struct Warp {
     // block, coalesced) and each edge's source id is broadcast to its lane
     // group with one shuffle, so the index work is not repeated LG times.
     // Slot s sums edges s, s+ES, s+2ES, ... of the block, in order.
-    __device__ __forceinline__ void accumulate_bcast(uint64_t lo, uint64_t hi, double (&acc)[W]) const {
+    __device__ __forceinline__ void accumulate_bcast(const uint32_t* __restrict__ col, uint64_t lo, uint64_t hi,
+                                                     double (&acc)[W]) const {
         const uint64_t sp = stream_policy(P);
         const uint32_t ne = (uint32_t)(hi - lo);
-        const uint32_t* __restrict__ cb = P.col + lo;
+        const uint32_t* __restrict__ cb = col + lo;
         const bool ok = slice_live();
         constexpr int STEPS = 32 / ES; // steps per 32-edge group
         constexpr int SB = STEPS < 4 ? STEPS : 4; // gathers in flight per sub-batch (registers)
@@ -736,11 +783,11 @@ struct Warp {
 
     // cp.async ring (async_hub): see kAsyncHub.  `stage` = this warp's
     // 2 * kAsyncBlock * KS doubles.
-    __device__ __forceinline__ void accumulate_async(uint64_t lo, uint64_t hi, double (&acc)[W],
-                                                     double* __restrict__ stage) const {
+    __device__ __forceinline__ void accumulate_async(const uint32_t* __restrict__ col, uint64_t lo, uint64_t hi,
+                                                     double (&acc)[W], double* __restrict__ stage) const {
         const uint64_t sp = stream_policy(P);
         const uint32_t ne = (uint32_t)(hi - lo);
-        const uint32_t* __restrict__ cb = P.col + lo;
+        const uint32_t* __restrict__ cb = col + lo;
         const bool ok = slice_live();
         constexpr int NP = KS / 2; // 16-byte pieces per row
         constexpr uint32_t B = kAsyncBlock;
@@ -799,13 +846,35 @@ struct Warp {
             for (int w = 0; w < W; ++w) acc[w] += __shfl_xor_sync(0xffffffffu, acc[w], off);
     }
 
-    // ---- chunk of a long (hub) row ------------------------------------------------
+    // a piece's partial sum (segmented pull): slot `sl` of the piece's row
+    __device__ __forceinline__ void piece_store(uint32_t slot_id, int sl, const double (&acc)[W]) {
+        if (lane_ok(sl)) store_w<W>(P.pacc + (size_t)slot_id * P.pacc_stride + sl * W, acc);
+    }
+
+    // ---- chunk of a long (hub) row, or (PIECE) of a wide piece ------------------------
+    template <bool PIECE = false>
     __device__ void chunk_task(uint32_t t, double* __restrict__ stage = nullptr) {
+        // the tables a chunk task reads: the hub rows' own, or the wide pieces'
+        struct {
+            const uint32_t* __restrict__ chunk_row;
+            const uint32_t* __restrict__ chunk_first;
+            const uint64_t* __restrict__ off;
+            const uint32_t* __restrict__ col;
+            double* acc;
+            unsigned int* cnt;
+        } T;
+        if constexpr (PIECE) {
+            T.chunk_row = P.seg_chunk_row; T.chunk_first = P.seg_chunk_first; T.off = P.seg_off;
+            T.col = P.seg_col; T.acc = P.seg_chunk_acc; T.cnt = P.seg_row_cnt;
+        } else {
+            T.chunk_row = P.chunk_row; T.chunk_first = P.chunk_first; T.off = P.row_off;
+            T.col = P.col; T.acc = P.chunk_acc; T.cnt = P.row_cnt;
+        }
         const uint64_t sp = stream_policy(P);
-        const uint32_t row = P.chunk_row[t];
-        const uint32_t first = P.chunk_first[row];
-        const uint32_t nch = P.chunk_first[row + 1] - first;
-        const uint64_t rlo = ld_stream_u64(P.row_off + row, sp), rhi = ld_stream_u64(P.row_off + row + 1, sp);
+        const uint32_t row = T.chunk_row[t];
+        const uint32_t first = T.chunk_first[row];
+        const uint32_t nch = T.chunk_first[row + 1] - first;
+        const uint64_t rlo = ld_stream_u64(T.off + row, sp), rhi = ld_stream_u64(T.off + row + 1, sp);
         // (a split pass's part of the row can end before this chunk: empty range)
         const uint64_t lo = min(rlo + (uint64_t)(t - first) * P.chunk, rhi);
         const uint64_t hi = min(lo + P.chunk, rhi);
@@ -813,20 +882,23 @@ struct Warp {
 #pragma unroll
         for (int w = 0; w < W; ++w) acc[w] = 0.0;
         if constexpr (async_hub<LG, KS>()) {
-            if (stage) accumulate_async(lo, hi, acc, stage);
-            else accumulate_bcast(lo, hi, acc);
-        } else if constexpr (LG > 1 && kBcast) accumulate_bcast(lo, hi, acc);
-        else accumulate(lo, hi, acc);
+            if (stage) accumulate_async(T.col, lo, hi, acc, stage);
+            else accumulate_bcast(T.col, lo, hi, acc);
+        } else if constexpr (LG > 1 && kBcast) accumulate_bcast(T.col, lo, hi, acc);
+        else accumulate(T.col, lo, hi, acc);
         reduce_slots(acc);
         if (nch == 1) { // the whole row was this chunk: no hand-off needed
-            if (lane < LG) epilogue(row, slice, acc);
+            if (lane < LG) {
+                if constexpr (PIECE) piece_store(P.seg_slot[row], slice, acc);
+                else epilogue(row, slice, acc);
+            }
             return;
         }
-        if (lane < LG) store_w<W>(P.chunk_acc + (size_t)t * KP + slice * W, acc);
+        if (lane < LG) store_w<W>(T.acc + (size_t)t * KP + slice * W, acc);
         __threadfence();
         __syncwarp();
         unsigned last = 0;
-        if (lane == 0) last = (atomicAdd(P.row_cnt + row, 1u) == nch - 1);
+        if (lane == 0) last = (atomicAdd(T.cnt + row, 1u) == nch - 1);
         last = __shfl_sync(0xffffffffu, last, 0);
         if (!last) return;
         __threadfence();
@@ -834,38 +906,71 @@ struct Warp {
 #pragma unroll
         for (int w = 0; w < W; ++w) acc[w] = 0.0;
         for (uint32_t c = slot; c < nch; c += ES) {
-            const double* p = P.chunk_acc + (size_t)(first + c) * KP + slice * W;
+            const double* p = T.acc + (size_t)(first + c) * KP + slice * W;
 #pragma unroll
             for (int w = 0; w < W; ++w) acc[w] += __ldcg(p + w);
         }
         reduce_slots(acc);
-        if (lane < LG) epilogue(row, slice, acc);
-        if (lane == 0) P.row_cnt[row] = 0;
+        if (lane < LG) {
+            if constexpr (PIECE) piece_store(P.seg_slot[row], slice, acc);
+            else epilogue(row, slice, acc);
+        }
+        if (lane == 0) T.cnt[row] = 0;
+    }
+
+    // ---- epilogues of the segmented rows: a row's piece partials in segment order --------
+    __device__ void combine_task(uint32_t t) {
+        const uint32_t base = t * P.seg_cr;
+        const uint32_t end = min(base + P.seg_cr, P.n_seg_rows);
+        const uint32_t S = P.seg_S;
+        const bool lok = lane_ok(slice);
+        for (uint32_t v = base + slot; v < end; v += ES) {
+            double acc[W];
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[w] = 0.0;
+            if (lok) {
+                const double* p = P.pacc + (size_t)v * S * P.pacc_stride + slice * W;
+#pragma unroll 4
+                for (uint32_t j = 0; j < S; ++j) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) acc[w] += __ldcs(p + (size_t)j * P.pacc_stride + w);
+                }
+            }
+            epilogue(v, slice, acc);
+        }
     }
 
     // ---- packed run of rows, K = 1: all gathers in flight, staged in smem ----------------
+    // PIECE: the run's "rows" are small pieces (segmented pull): offsets and
+    // colidx from the segment plan, a piece's sum stored to its slot
+    template <bool PIECE = false>
     __device__ void packed_task(uint32_t t, double* __restrict__ sv) {
         const uint64_t sp = stream_policy(P);
-        const uint32_t r0 = P.packed_r0[t], r1 = P.packed_r0[t + 1];
+        const uint32_t* __restrict__ pr = PIECE ? P.seg_packed_r0 : P.packed_r0;
+        const uint64_t* __restrict__ roff = PIECE ? P.seg_off : P.row_off;
+        const uint32_t* __restrict__ colp = PIECE ? P.seg_col : P.col;
+        const uint32_t r0 = pr[t], r1 = pr[t + 1];
         const int R = (int)(r1 - r0); // <= 32
         if (R <= 0) return;
-        const uint64_t e0 = ld_stream_u64(P.row_off + r0, sp);
-        const uint64_t e1 = ld_stream_u64(P.row_off + r1, sp);
+        const uint64_t e0 = ld_stream_u64(roff + r0, sp);
+        const uint64_t e1 = ld_stream_u64(roff + r1, sp);
         // row bounds relative to e0 (a run holds < 2*WIN edges: 32-bit is enough)
-        const uint32_t mylo = (lane < R) ? (uint32_t)(ld_stream_u64(P.row_off + r0 + lane, sp) - e0) : 0;
-        const uint32_t myhi = (lane < R) ? (uint32_t)(ld_stream_u64(P.row_off + r0 + lane + 1, sp) - e0) : 0;
+        const uint32_t mylo = (lane < R) ? (uint32_t)(ld_stream_u64(roff + r0 + lane, sp) - e0) : 0;
+        const uint32_t myhi = (lane < R) ? (uint32_t)(ld_stream_u64(roff + r0 + lane + 1, sp) - e0) : 0;
         // the epilogue's row info and previous rank of row r0 + lane, in flight
         // during the gathers (handed to the reducing lane by a shuffle)
         uint2 my_ri = make_uint2(0, 0);
         double my_prev = 0.0;
-        if constexpr (KP == 1) {
+        if constexpr (PIECE) {
+            if (lane < R) my_ri.x = ld_stream_u32(P.seg_slot + r0 + lane, sp);
+        } else if constexpr (KP == 1) {
             if (lane < R) {
                 my_ri = ld_stream_u2(P.rowinfo + r0 + lane, sp);
                 if (!(P.skip_mask & 16)) my_prev = __ldcs(rp + (size_t)(r0 + lane) * P.ks);
             }
         }
         // cb is the 16-byte aligned colidx base; valid positions [off0, ne).
-        const uint32_t* __restrict__ cb = P.col + (e0 & ~3ull);
+        const uint32_t* __restrict__ cb = colp + (e0 & ~3ull);
         const uint32_t off0 = (uint32_t)(e0 & 3ull);
         const uint32_t ne = (uint32_t)(e1 - e0) + off0;
         const bool live = slice_live();
@@ -919,7 +1024,10 @@ struct Warp {
             for (int off = LG; off < LG * gs; off <<= 1)
 #pragma unroll
                 for (int w = 0; w < W; ++w) acc[w] += __shfl_xor_sync(0xffffffffu, acc[w], off);
-            if constexpr (KP == 1) {
+            if constexpr (PIECE) {
+                const uint32_t sl_id = __shfl_sync(0xffffffffu, my_ri.x, src);
+                if (i < R && sub == 0) piece_store(sl_id, slice, acc);
+            } else if constexpr (KP == 1) {
                 const uint2 ri = make_uint2(__shfl_sync(0xffffffffu, my_ri.x, src),
                                             __shfl_sync(0xffffffffu, my_ri.y, src));
                 const double o[1] = {__shfl_sync(0xffffffffu, my_prev, src)};
@@ -979,18 +1087,22 @@ struct Warp {
     // then each slot walks its rows issuing the next row's row info and
     // previous ranks before gathering the current one, so a row costs a
     // single gather round trip.
+    template <bool PIECE = false>
     __device__ void packed_pipe(uint32_t t, double* __restrict__ stage) {
         constexpr int WIN_ = C::EMAX / 2;
         const uint64_t sp = stream_policy(P);
-        const uint32_t r0 = P.packed_r0[t], r1 = P.packed_r0[t + 1];
+        const uint32_t* __restrict__ pr = PIECE ? P.seg_packed_r0 : P.packed_r0;
+        const uint64_t* __restrict__ roff = PIECE ? P.seg_off : P.row_off;
+        const uint32_t* __restrict__ colp = PIECE ? P.seg_col : P.col;
+        const uint32_t r0 = pr[t], r1 = pr[t + 1];
         const uint32_t R = r1 - r0; // <= 2*WIN / max(1, WIN/32) + 1
         uint64_t* s_off = reinterpret_cast<uint64_t*>(stage);                 // [kPackOff]
         uint32_t* s_col = reinterpret_cast<uint32_t*>(s_off + kPackOff);     // [2*WIN + 8]
-        for (uint32_t x = lane; x <= R; x += 32) s_off[x] = ld_stream_u64(P.row_off + r0 + x, sp);
+        for (uint32_t x = lane; x <= R; x += 32) s_off[x] = ld_stream_u64(roff + r0 + x, sp);
         __syncwarp();
         const uint64_t e0 = s_off[0];
         const uint32_t ne_all = (uint32_t)(s_off[R] - e0);
-        for (uint32_t x = lane; x < ne_all; x += 32) s_col[x] = ld_stream_u32(P.col + e0 + x, sp);
+        for (uint32_t x = lane; x < ne_all; x += 32) s_col[x] = ld_stream_u32(colp + e0 + x, sp);
         __syncwarp();
         if (kExp && P.pf) // every row of the run in flight to L2 at once (the walk below is one row per slot)
             for (uint32_t x = lane; x < ne_all; x += 32) prefetch_row(s_col[x]);
@@ -1001,7 +1113,7 @@ struct Warp {
             auto load_prev = [&](uint32_t v, double (&o)[W]) {
 #pragma unroll
                 for (int w = 0; w < W; ++w) o[w] = 0.0;
-                if (lok) {
+                if (lok && !PIECE) {
                     const double* rr = rp + (size_t)v * P.ks + slice * W;
                     if constexpr (W % 2 == 0) {
 #pragma unroll
@@ -1017,7 +1129,8 @@ struct Warp {
                 }
             };
             uint32_t v = r0 + i;
-            uint2 ri = ld_stream_u2(P.rowinfo + v, sp);
+            // (PIECE: ri.x is the piece's slot)
+            uint2 ri = PIECE ? make_uint2(ld_stream_u32(P.seg_slot + v, sp), 0u) : ld_stream_u2(P.rowinfo + v, sp);
             double o[W];
             load_prev(v, o);
             for (;;) {
@@ -1025,7 +1138,8 @@ struct Warp {
                 const bool more = in < R;
                 const uint32_t vn = r0 + (more ? in : i);
                 // next row's info and previous ranks, in flight during this row's gathers
-                const uint2 nri = ld_stream_u2(P.rowinfo + vn, sp);
+                const uint2 nri =
+                    PIECE ? make_uint2(ld_stream_u32(P.seg_slot + vn, sp), 0u) : ld_stream_u2(P.rowinfo + vn, sp);
                 double no[W];
                 load_prev(vn, no);
                 double acc[W];
@@ -1047,7 +1161,8 @@ struct Warp {
 #pragma unroll
                         for (int w = 0; w < W; ++w) acc[w] += vals[j][w];
                 }
-                epilogue_with<false>(v, slice, acc, ri, o);
+                if constexpr (PIECE) piece_store(ri.x, slice, acc);
+                else epilogue_with<false>(v, slice, acc, ri, o);
                 if (!more) break;
                 i = in;
                 v = vn;
@@ -1156,6 +1271,8 @@ __device__ void finalize_lanes(const Params& P, const double* s_tot, const doubl
         P.gs->iter = iter + 1;
         P.gs->any_active = any;
         P.gs->counter = 0;
+        P.gs->seg_next[0] = 0;
+        P.gs->seg_next[1] = 0;
         __threadfence();
         if (P.use_cond) cudaGraphSetConditional(P.cond, any ? 1u : 0u);
     }
@@ -1193,8 +1310,13 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     // dynamic smem: [kWarps][SMEM_WARP + ASYNC_WARP] staged gathers, then the per-thread
     // partial columns when W >= 6
     // K > 1 packed runs (PATHS == 2): staged row offsets + colidx, in doubles
+    // PATHS bits: 1 hub chunks, 2 packed + empty; segmented pull: 4 chunks
+    // of wide pieces, 8 runs of small pieces, 16 combine tasks (the seg
+    // tasks lead the kernel's task range: Params::seg_pre of them)
+    constexpr bool PACKS = (PATHS & (2 | 8)) != 0;
+    constexpr bool SEG = (PATHS & (4 | 8 | 16)) != 0;
     constexpr bool WSTAGE = (PATHS == 2) && kStagedWide && LG == 4 && C::KS == 4 && !C::STAGED;
-    constexpr int PACK_WARP = (PATHS == 2 && !C::STAGED) ? (WSTAGE ? C::EMAX * C::KS : kPackOff + (2 * WIN + 8) / 2) : 0;
+    constexpr int PACK_WARP = (PACKS && PATHS != 3 && !C::STAGED) ? (WSTAGE ? C::EMAX * C::KS : kPackOff + (2 * WIN + 8) / 2) : 0;
     // hub-chunk instances of 2/4 lanes: the cp.async ring (kAsyncHub)
     constexpr bool ASYNC = (PATHS == 1) && async_hub<LG, C::KS>();
     constexpr int ASYNC_WARP = ASYNC ? 2 * kAsyncBlock * C::KS : 0;
@@ -1209,7 +1331,35 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
     const uint32_t T1 = P.n_chunk, T2 = T1 + P.n_packed;
     const bool listed = P.task_list != nullptr;
     const uint32_t i0 = listed ? P.list_begin : P.task_begin, i1 = listed ? P.list_end : P.task_end;
-    for (uint32_t i = i0 + blockIdx.x * kWarps + warp; i < i1; i += TW) {
+    uint32_t istart = i0 + blockIdx.x * kWarps + warp;
+    if constexpr ((PATHS & (4 | 8)) != 0) {
+        // piece tasks are handed out in order from a device counter, kSegGrab
+        // at a time: the warps stay within a few thousand tasks of each other,
+        // i.e. inside one source segment (a static deal drifts apart by more
+        // than a segment over a kernel).  A piece's sum does not depend on
+        // which warp computes it, so runs stay bit-reproducible.
+        const uint32_t GRAB = P.seg_grab;
+        const uint32_t pre = P.seg_pre;
+        unsigned int* ctr = &P.gs->seg_next[(PATHS & 4) ? 0 : 1];
+        for (;;) {
+            uint32_t b = 0;
+            if (lane == 0) b = atomicAdd(ctr, GRAB);
+            b = __shfl_sync(0xffffffffu, b, 0);
+            if (b >= pre) break;
+            const uint32_t e = min(b + GRAB, pre);
+            for (uint32_t i = b; i < e; ++i) {
+                if constexpr ((PATHS & 4) != 0) w.template chunk_task<true>(i);
+                else if constexpr (C::STAGED) w.template packed_task<true>(i, sv);
+                else w.template packed_pipe<true>(i, sv);
+            }
+        }
+    } else if constexpr ((PATHS & 16) != 0) { // combine tasks lead, then the round-robin carries on
+        const uint32_t pre = P.seg_pre;
+        uint32_t i = blockIdx.x * kWarps + warp;
+        for (; i < pre; i += TW) w.combine_task(i);
+        istart = i0 + (i - pre);
+    }
+    for (uint32_t i = istart; i < i1; i += TW) {
         const uint32_t t = listed ? __ldg(P.task_list + i) : i;
         if (t < T1) {
             if constexpr ((PATHS & 1) != 0)
@@ -1218,7 +1368,7 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
             if (t < T2) {
                 if (!(P.skip_mask & 2)) {
                     if constexpr (C::STAGED || WSTAGE) w.packed_task(t - T1, sv);
-                    else if constexpr (PATHS == 2) w.packed_pipe(t - T1, sv);
+                    else if constexpr (PATHS != 3) w.packed_pipe(t - T1, sv);
                     else w.packed_direct(t - T1);
                 }
             } else if (!(P.skip_mask & 4)) {
@@ -1227,6 +1377,7 @@ __global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
         }
     }
 
+    if constexpr (PATHS == 8) return; // piece sums only: no epilogue ran, no partials
     if (kExp && P.split == 1) return; // hot pass: row sums only, no partials
 
     // ---- CTA partials, fixed order ------------------------------------------------
