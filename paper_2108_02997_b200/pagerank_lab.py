@@ -118,6 +118,10 @@ class CsrGraph:
                 pass
             self._h = None
 
+    def release(self) -> None:
+        """Free the device graph now (host arrays already downloaded stay)."""
+        self.__del__()
+
     @property
     def handle(self):
         return self._h
