@@ -280,6 +280,12 @@ struct LaneCfg {
 #endif
 constexpr int kMinb12 = PRGPU_K12_MINB;
 
+// packed-row window of the 3/4-lane instances (tuning builds: -DPRGPU_W4=64 / 32)
+#ifndef PRGPU_W4
+#define PRGPU_W4 128
+#endif
+constexpr int kW4 = PRGPU_W4;
+
 // per-mode instance alternatives (tuning only)
 inline int k_variant(const char* name) {
     const char* v = std::getenv(name);
@@ -308,7 +314,7 @@ template <int PATHS>
 LaneCfg lane_cfg_t(int K, bool all_q) {
     if (K == 1) return mk_cfg<1, 1, 256, 2, 3, kQmAll, 0, PATHS>();
     if (K == 2) return wide_cfg<2, 1, 64, 4, 2, PATHS>(all_q);
-    if (K <= 4) return wide_cfg<4, 1, 128, 4, 4, PATHS>(all_q);
+    if (K <= 4) return wide_cfg<4, 1, kW4, 4, 4, PATHS>(all_q);
     if (K <= 8) return wide_cfg<4, 2, 128, 4, 8, PATHS>(all_q);
     if (K <= 12) return wide_cfg<8, 2, 128, kMinb12, 12, PATHS>(all_q);
     return wide_cfg<8, 2, 128, 4, 16, PATHS>(all_q);
@@ -344,7 +350,7 @@ bool mode_cfg(int KS, int kp, int win, bool all_q, LaneCfg& out, int k1_minb4 = 
         return true;
     case 404:
         if (k_variant("PRGPU_K4CFG") == 1) { out = wide_cfg<2, 2, 128, 4, 4, PATHS>(all_q); return true; }
-        out = wide_cfg<4, 1, 128, 4, 4, PATHS>(all_q);
+        out = wide_cfg<4, 1, kW4, 4, 4, PATHS>(all_q);
         return true;
     case 808: out = wide_cfg<4, 2, 128, 4, 8, PATHS>(all_q); return true;
     case 1216: out = wide_cfg<8, 2, 128, kMinb12, 12, PATHS>(all_q); return true;

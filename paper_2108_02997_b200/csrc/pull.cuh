@@ -740,24 +740,27 @@ struct Warp {
             for (int j = 0; j < 4; ++j)
                 if (base + lane + 32u * j < ne) prefetch_row(c[j]);
         };
+        // the next block's colidx is loaded before this block's rows are
+        // gathered, so a block costs one round trip (the gathers'), not two
+        // (once the rows come from L2 — the segmented pull — the colidx
+        // stream's DRAM latency is the longer of the two)
         uint32_t cn[4], cnn[4];
+        ld_block(0, cn);
         if (pf) {
-            ld_block(0, cn);
             ld_block(128, cnn);
             pf_block(0, cn);
         }
         for (uint32_t base = 0; base < ne; base += 128) {
             uint32_t c[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) c[j] = cn[j];
             if (pf) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    c[j] = cn[j];
-                    cn[j] = cnn[j];
-                }
+                for (int j = 0; j < 4; ++j) cn[j] = cnn[j];
                 pf_block(base + 128, cn);
                 if (base + 256 < ne) ld_block(base + 256, cnn);
-            } else {
-                ld_block(base, c);
+            } else if (base + 128 < ne) {
+                ld_block(base + 128, cn);
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
