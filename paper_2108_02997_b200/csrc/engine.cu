@@ -582,7 +582,9 @@ void build_tasks(prgpu_session* s) {
     PRGPU_CUDA(cudaMemsetAsync(s->row_cnt.p, 0, std::max<uint32_t>(n_long, 1) * 4, st));
 
     // packed rows [n_long, nonempty_end)
-    const uint32_t plo = n_long, phi = std::max(n_long, g->nonempty_end);
+    // (rows the segment plan covers beyond the hub rows are pulled as pieces, not as packed rows)
+    const uint32_t plo = std::max<uint32_t>(n_long, s->seg ? std::min(s->seg->n_rows, g->nonempty_end) : 0u);
+    const uint32_t phi = std::max(plo, g->nonempty_end);
     const uint32_t prow = phi - plo;
     const uint32_t cmin = std::max<uint32_t>(1, (win + 31) / 32);
     uint64_t n_packed = 0;
@@ -663,10 +665,10 @@ void build_tasks(prgpu_session* s) {
 // run's widest contribution rows), PRGPU_SEG_HOT the number of L2-sized
 // segments before the cold rest, PRGPU_SEG_T the least in-degree of a
 // segmented row, PRGPU_SEG_PMIN the smallest hot-segment piece kept.
-void build_seg_tasks(prgpu_session* s, int nranks) {
+void seg_choose_plan(prgpu_session* s, int nranks) {
     prgpu_graph* g = s->g;
     cudaStream_t st = s->stream;
-    if (nranks != 0 || g->shard_n > 1 || g->locality || s->n_long == 0) return;
+    if (nranks != 0 || g->shard_n > 1 || g->locality) return;
     auto env_u = [](const char* name, uint64_t dflt) -> uint64_t {
         const char* v = std::getenv(name);
         return v ? (uint64_t)std::atoll(v) : dflt;
@@ -687,11 +689,19 @@ void build_seg_tasks(prgpu_session* s, int nranks) {
     if (s_all < 2) return; // the whole table is one segment
     const uint32_t pmin = (uint32_t)env_u("PRGPU_SEG_PMIN", 0); // measured: folding small pieces loses (C5 +1 % at 8, +4 % at 16)
     const uint32_t S = (s_all <= hot && pmin == 0) ? s_all : std::min(s_all, hot) + 1;
-    // every hub row by default (C5: T = 512 leaves the rows of 129..511 in-edges to miss: 595 vs 500 ms)
-    const uint32_t T = (uint32_t)std::max<uint64_t>(env_u("PRGPU_SEG_T", 0), (uint64_t)win + 1);
-    const SegPlan* sp = graph_seg_plan(g, seg_src, S, T, win, pmin, st);
+    // every hub row by default (C5: T = 512 leaves the rows of 129..511 in-edges to miss: 595 vs 500 ms);
+    // a smaller T also segments packed rows (all their pieces are small)
+    const uint32_t T = (uint32_t)std::max<uint64_t>(env_u("PRGPU_SEG_T", (uint64_t)win + 1), 2);
+    s->seg = graph_seg_plan(g, seg_src, S, T, win, pmin, st);
+}
+
+// the plan's task tables (after build_tasks: the chunk size and the hub rows' chunk table)
+void build_seg_tasks(prgpu_session* s) {
+    const SegPlan* sp = s->seg;
     if (!sp) return;
-    s->seg = sp;
+    cudaStream_t st = s->stream;
+    const uint32_t win = (uint32_t)s->cfg.WIN;
+    const uint32_t S = sp->S;
     const uint32_t emax = s->P.chunk;
     // chunk tasks of the wide pieces
     const uint32_t nw = sp->n_wp;
@@ -708,7 +718,8 @@ void build_seg_tasks(prgpu_session* s, int nranks) {
     uint64_t n_chunk = 0;
     PRGPU_CUDA(cudaMemcpyAsync(&n_chunk, first.p + nw, 8, cudaMemcpyDeviceToHost, st));
     // the hub rows' own chunk tasks start after the segmented rows'
-    PRGPU_CUDA(cudaMemcpyAsync(&s->seg_chunk_t0, s->chunk_first.p + sp->n_rows, 4, cudaMemcpyDeviceToHost, st));
+    PRGPU_CUDA(cudaMemcpyAsync(&s->seg_chunk_t0, s->chunk_first.p + std::min(sp->n_rows, s->n_long), 4,
+                               cudaMemcpyDeviceToHost, st));
     PRGPU_CUDA(cudaStreamSynchronize(st));
     s->seg_chunk_first.alloc((size_t)nw + 1);
     s->seg_chunk_row.alloc(std::max<uint64_t>(n_chunk, 1));
@@ -1055,9 +1066,27 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
     P.cold_off[0] = 0;
     P.cold_off[1] = nsrc;
     ph.mark("params");
+    try {
+        seg_choose_plan(s.get(), nranks);
+    } catch (const Error& e) { // no room for the plan (C5: 13 GB + 10 GB of temporaries): the unsegmented pull
+        if (e.code != PRGPU_ENOMEM) throw;
+        cudaGetLastError();
+        s->seg = nullptr;
+    }
+    ph.mark("seg plan");
     build_tasks(s.get());
     ph.mark("tasks");
-    build_seg_tasks(s.get(), nranks);
+    try {
+        build_seg_tasks(s.get());
+    } catch (const Error& e) {
+        if (e.code != PRGPU_ENOMEM) throw;
+        cudaGetLastError();
+        prgpu_session* q = s.get();
+        q->seg = nullptr;
+        q->seg_chunk_row.reset(); q->seg_chunk_first.reset(); q->seg_packed_r0.reset();
+        q->seg_chunk_acc.reset(); q->pacc.reset(); q->seg_row_cnt.reset();
+        build_tasks(q); // packed runs over every packed row again
+    }
     ph.mark("seg tasks");
     if (nranks >= 1) { // partition session (nranks == 0: the fused single-GPU run)
         if (rank < 0 || rank >= nranks) fail(PRGPU_EINVAL, "partition: rank out of range");

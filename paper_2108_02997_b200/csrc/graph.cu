@@ -1300,7 +1300,7 @@ __global__ void count_rows_ge(const uint64_t* __restrict__ row_off, uint32_t n, 
 
 const SegPlan* graph_seg_plan(prgpu_graph* g, uint32_t seg_src, uint32_t S, uint32_t T, uint32_t win,
                               uint32_t pmin, cudaStream_t st) {
-    if (S < 1 || S > 64 || seg_src == 0 || T <= win) fail(PRGPU_EINVAL, "segment plan: bad parameters");
+    if (S < 1 || S > 64 || seg_src == 0 || T < 2) fail(PRGPU_EINVAL, "segment plan: bad parameters");
     if (g->shard_n > 1 || g->locality) return nullptr; // rows not in degree order / col not whole
     std::lock_guard<std::mutex> lock(g->split_mu);
     const std::array<uint32_t, 5> key{seg_src, S, T, win, pmin};

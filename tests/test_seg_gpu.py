@@ -28,6 +28,7 @@ SEG_ENVS = [
     dict(PRGPU_SEG_KB="256", PRGPU_SEG_HOT="63", PRGPU_SEG_T="600", PRGPU_CHUNK="512",
          PRGPU_SEG_PMIN="0"),                                         # every segment hot, chunked wide pieces, no folding
     dict(PRGPU_SEG_KB="4", PRGPU_SEG_HOT="40", PRGPU_SEG_T="257", PRGPU_SEG_PMIN="20"),  # tiny segments, most pieces folded
+    dict(PRGPU_SEG_KB="32", PRGPU_SEG_HOT="8", PRGPU_SEG_T="24"),     # packed rows segmented too
 ]
 
 
