@@ -1323,7 +1323,9 @@ const SegPlan* graph_seg_plan(prgpu_graph* g, uint32_t seg_src, uint32_t S, uint
         PRGPU_CUDA(cudaMemcpyAsync(&sp->n_rows, c.p, 4, cudaMemcpyDeviceToHost, st));
         PRGPU_CUDA(cudaStreamSynchronize(st));
     }
-    if (sp->n_rows == 0) {
+    // (slots row * S + seg are 32-bit: only a far-too-small T could overflow them)
+    if (sp->n_rows == 0 || (uint64_t)sp->n_rows * S >= (1ull << 32)) {
+        sp->n_rows = 0;
         g->seg_plans[key] = std::move(sp);
         return nullptr;
     }
