@@ -1166,7 +1166,11 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
             }
             if (modes.empty() || modes.back().first != wide) modes.clear(); // no instances: base kernel
         }
-        if (modes.empty()) s->seg = nullptr; // the segmented pull needs the split iteration
+        if (modes.empty() && s->seg) { // the segmented pull needs the split iteration
+            const bool took_packed_rows = s->seg->n_rows > s->n_long;
+            s->seg = nullptr;
+            if (took_packed_rows) build_tasks(s.get()); // packed runs over every packed row again
+        }
     }
     P.part_kp = (uint32_t)KP;
     // contribution buffers of the narrow modes: after the run's own buffers
