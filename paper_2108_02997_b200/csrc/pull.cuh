@@ -1284,8 +1284,16 @@ __device__ void finalize_lanes(const Params& P, const double* s_tot, const doubl
 // PATHS: which task kinds this instance compiles (1 hub chunks, 2 packed +
 // empty); a split iteration runs a PATHS=1 and a PATHS=2 instance, each with
 // only its own path's register pressure.
+// CTAs per SM the small-piece instances (PATHS 8) are compiled for (tuning
+// builds: -DPRGPU_A2_MINB=6; 0: the instance's own MINB)
+#ifndef PRGPU_A2_MINB
+#define PRGPU_A2_MINB 0
+#endif
+#ifndef PRGPU_A_MINB // likewise the wide-piece instances (PATHS 5)
+#define PRGPU_A_MINB 0
+#endif
 template <int LG, int W, int WIN, int QJ_, int MINB, int QM = kQmAll, int KS_ = 0, int PATHS = 3>
-__global__ void __launch_bounds__(kNT, MINB) pull_kernel(const Params P) {
+__global__ void __launch_bounds__(kNT, (PATHS == 8 && PRGPU_A2_MINB) ? PRGPU_A2_MINB : (PATHS == 5 && PRGPU_A_MINB) ? PRGPU_A_MINB : MINB) pull_kernel(const Params P) {
     using C = PullCfg<LG, W, WIN, QJ_, KS_>;
     constexpr int KP = C::KP;
     __shared__ double s_alpha[KP], s_c0[KP];
