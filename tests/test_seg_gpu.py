@@ -99,3 +99,35 @@ def test_segmented_pull_series_and_observer(prl, oracle, monkeypatch):
         assert np.max(np.abs(got.ranks - want["ranks"])) <= RANK_TOL
     finally:
         oracle.free_csr(h)
+
+
+@pytest.mark.parametrize("K", [2, 5, 8, 16])
+def test_segmented_pull_lane_counts_ref_trace_and_caps(prl, oracle, monkeypatch, K):
+    """Every lane-count instance of the three segmented kernels, with the
+    L1-vs-reference trace (sweep.hpp:193-196), all-norm stopping and an
+    iteration cap, against the unsegmented run of the same session
+    parameters."""
+    n, pairs = oracle.rmat(15, 16, 0.57, 0.19, 0.19, 11)
+    g = prl.build_csr(edge_list(prl, n, pairs))
+    alphas = [0.5 + 0.5 * k / K for k in range(K)]
+    ref = prl.reference_ranks(g)
+    runs = {}
+    for seg in ("0", "1"):
+        monkeypatch.setenv("PRGPU_SEG", seg)
+        monkeypatch.setenv("PRGPU_SEG_KB", "8")
+        monkeypatch.setenv("PRGPU_SEG_HOT", "6")
+        runs[seg] = (
+            prl.pagerank_batched(g, alphas, 1e-9, prl.NormKind.LInf, 300, stop_mask=7, ref_ranks=ref),
+            prl.pagerank_batched(g, alphas, 1e-12, prl.NormKind.L2, 7),  # capped: nothing converges
+        )
+    for a, b in zip(runs["0"], runs["1"]):
+        assert a.run_iterations == b.run_iterations
+        for x, y in zip(a.results, b.results):
+            assert x.iterations == y.iterations and x.converged == y.converged
+            assert np.max(np.abs(x.ranks - y.ranks)) <= 1e-15
+        ta, tb = a.trace[: a.run_iterations], b.trace[: b.run_iterations]
+        live = ~np.isnan(ta)
+        assert np.array_equal(live, ~np.isnan(tb))
+        # (norms of 1e-12 carry the summation order's rounding, ~1e-18 absolute)
+        assert np.all(np.abs(ta[live] - tb[live]) <= 1e-9 * np.abs(ta[live]) + 1e-16)
+    assert not any(r.converged for r in runs["1"][1].results)
