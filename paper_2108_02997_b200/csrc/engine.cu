@@ -692,7 +692,10 @@ void seg_choose_plan(prgpu_session* s, int nranks) {
     // every hub row by default (C5: T = 512 leaves the rows of 129..511 in-edges to miss: 595 vs 500 ms);
     // a smaller T also segments packed rows (all their pieces are small)
     const uint32_t T = (uint32_t)std::max<uint64_t>(env_u("PRGPU_SEG_T", (uint64_t)win + 1), 2);
-    s->seg = graph_seg_plan(g, seg_src, S, T, win, pmin, st);
+    // pieces longer than wmin edges are pulled by a whole warp (chunk tasks), the others by a lane group
+    // (measured: 3/4 of the packed window, C5 -1 %, RMAT-24 x 11 -1.4 %, C4 +-0; 1/2: +-0, 1/4: +3.5 %)
+    const uint32_t wmin = (uint32_t)std::min<uint64_t>(win, std::max<uint64_t>(1, env_u("PRGPU_SEG_WMIN", 3 * win / 4)));
+    s->seg = graph_seg_plan(g, seg_src, S, T, wmin, pmin, st);
 }
 
 // the plan's task tables (after build_tasks: the chunk size and the hub rows' chunk table)
