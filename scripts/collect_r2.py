@@ -45,7 +45,7 @@ for k in ("c1", "c2", "c2k1", "c3", "c4", "c5", "c2series", "c5series"):
     md.append(f"| {k} | {d['value']:.1f} | {d['ms_per_step']:.2f} | {frac} | {e2e} | {cpu} | "
               f"{d['clocks']['sm_mhz']}, {d['clocks']['reasons']} |")
 refs = []
-if "ref_c5" in lines and lines["ref_c5"]["cpu_baseline"]["cores"] < 16:
+if "ref_c5" not in lines or lines["ref_c5"]["cpu_baseline"]["cores"] < 16:  # the committed 16-lane run
     lines["ref_c5"] = json.load(open(os.path.join(PROF, "r2_bench_reference_c5.json")))
 for k in ("ref_c2", "ref_c5"):
     if k in lines:
