@@ -34,6 +34,13 @@
 // bit-reproducible (sweep.hpp:176-179, acceptance.cpp:331-366).  No
 // floating-point atomics anywhere.
 //
+// Segmented hub pull (graphs whose contribution table exceeds L2, SegPlan in
+// common.cuh): the hub rows' in-edges are regrouped into (row, source
+// segment) pieces, pulled segment by segment — wide pieces as chunk tasks,
+// small pieces as packed runs, both handed out in order from a device counter
+// (a piece's sum does not depend on the warp that computes it) — and a
+// combine task adds a row's piece sums in segment order before its epilogue.
+//
 // K lanes share every edge visit: a lane group of LG threads owns an edge (or
 // a row), thread j of the group carrying W of the lanes, so the source's K
 // contributions ([src][KS] rows) are fetched together.
@@ -1325,7 +1332,6 @@ __global__ void __launch_bounds__(kNT, (PATHS == 8 && PRGPU_A2_MINB) ? PRGPU_A2_
     // of wide pieces, 8 runs of small pieces, 16 combine tasks (the seg
     // tasks lead the kernel's task range: Params::seg_pre of them)
     constexpr bool PACKS = (PATHS & (2 | 8)) != 0;
-    constexpr bool SEG = (PATHS & (4 | 8 | 16)) != 0;
     constexpr bool WSTAGE = (PATHS == 2) && kStagedWide && LG == 4 && C::KS == 4 && !C::STAGED;
     constexpr int PACK_WARP = (PACKS && PATHS != 3 && !C::STAGED) ? (WSTAGE ? C::EMAX * C::KS : kPackOff + (2 * WIN + 8) / 2) : 0;
     // hub-chunk instances of 2/4 lanes: the cp.async ring (kAsyncHub)
@@ -1344,7 +1350,7 @@ __global__ void __launch_bounds__(kNT, (PATHS == 8 && PRGPU_A2_MINB) ? PRGPU_A2_
     const uint32_t i0 = listed ? P.list_begin : P.task_begin, i1 = listed ? P.list_end : P.task_end;
     uint32_t istart = i0 + blockIdx.x * kWarps + warp;
     if constexpr ((PATHS & (4 | 8)) != 0) {
-        // piece tasks are handed out in order from a device counter, kSegGrab
+        // piece tasks are handed out in order from a device counter, Params::seg_grab
         // at a time: the warps stay within a few thousand tasks of each other,
         // i.e. inside one source segment (a static deal drifts apart by more
         // than a segment over a kernel).  A piece's sum does not depend on
