@@ -180,6 +180,33 @@ __global__ void packed_bounds(const uint64_t* __restrict__ excl, uint32_t lo, ui
     }
 }
 
+// One 16-byte record per wide-piece chunk task, so a task costs one load
+// instead of the chunk -> piece -> offsets chain: {first edge (lo, hi), edges,
+// the piece's slot}; bit 31 of the last word marks a chunk of a multi-chunk
+// piece (those go through the hand-off, which looks the piece up itself).
+__global__ void seg_task_records(const uint32_t* __restrict__ chunk_row, const uint32_t* __restrict__ chunk_first,
+                                 const uint64_t* __restrict__ off, const uint32_t* __restrict__ slot,
+                                 uint32_t n_chunk, uint32_t chunk, uint4* __restrict__ rec) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n_chunk; t += gridDim.x * blockDim.x) {
+        const uint32_t p = chunk_row[t], first = chunk_first[p], nch = chunk_first[p + 1] - first;
+        const uint64_t hi = off[p + 1];
+        const uint64_t lo = min(off[p] + (uint64_t)(t - first) * chunk, hi);
+        const uint32_t len = (uint32_t)min((uint64_t)chunk, hi - lo);
+        rec[t] = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), len, nch == 1 ? slot[p] : 0x80000000u);
+    }
+}
+
+// One record per packed run (rows or small pieces): {first edge (lo, hi), first
+// row, edges | rows << 16}, so the run's offsets and colidx are staged together.
+__global__ void run_records(const uint32_t* __restrict__ r0s, const uint64_t* __restrict__ off, uint32_t n_runs,
+                            uint4* __restrict__ rec) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n_runs; t += gridDim.x * blockDim.x) {
+        const uint32_t r0 = r0s[t], r1 = r0s[t + 1];
+        const uint64_t e0 = off[r0];
+        rec[t] = make_uint4((uint32_t)e0, (uint32_t)(e0 >> 32), r0, (uint32_t)(off[r1] - e0) | ((r1 - r0) << 16));
+    }
+}
+
 // ---- deterministic device error_norm (norms.hpp:48-78) ------------------------------
 // The reference accumulates L1 and L2 in x87 long double (64-bit mantissa,
 // norms.hpp:57-69).  The device has no long double: sums are carried as
@@ -451,6 +478,8 @@ struct prgpu_session {
     // wide pieces' chunk hand-off state and the piece partial sums
     const SegPlan* seg = nullptr;
     DevBuf<uint32_t> seg_chunk_row, seg_chunk_first, seg_packed_r0;
+    DevBuf<uint4> seg_task; // [wide-piece chunk tasks] one record per task (seg_task_records)
+    DevBuf<uint4> seg_run_rec, run_rec; // one record per small-piece run / packed-row run (run_records)
     DevBuf<double> seg_chunk_acc, pacc;
     DevBuf<unsigned int> seg_row_cnt;
     uint32_t seg_n_wchunk = 0, seg_n_runs = 0, seg_n_comb = 0, seg_chunk_t0 = 0;
@@ -640,6 +669,13 @@ void build_tasks(prgpu_session* s) {
     P.chunk_row = s->chunk_row.p;
     P.chunk_first = s->chunk_first.p;
     P.packed_r0 = s->packed_r0.p;
+    P.run_rec = nullptr;
+    if (n_packed && !std::getenv("PRGPU_NO_RUNREC")) { // (PRGPU_NO_RUNREC=1, tuning: bounds -> offsets -> colidx)
+        s->run_rec.alloc(n_packed);
+        run_records<<<blocks_for(n_packed), kNT, 0, st>>>(s->packed_r0.p, g->row_off.p, (uint32_t)n_packed, s->run_rec.p);
+        PRGPU_LAUNCHED("run_records");
+        P.run_rec = s->run_rec.p;
+    }
     P.chunk_acc = s->chunk_acc.p;
     P.row_cnt = s->row_cnt.p;
     P.n_chunk = (uint32_t)n_chunk;
@@ -732,6 +768,12 @@ void build_seg_tasks(prgpu_session* s) {
     s->seg_row_cnt.alloc(std::max<uint32_t>(nw, 1));
     PRGPU_CUDA(cudaMemsetAsync(s->seg_row_cnt.p, 0, std::max<uint32_t>(nw, 1) * 4, st));
     s->seg_n_wchunk = (uint32_t)n_chunk;
+    s->seg_task.alloc(std::max<uint64_t>(n_chunk, 1));
+    if (n_chunk) {
+        seg_task_records<<<blocks_for(n_chunk), kNT, 0, st>>>(s->seg_chunk_row.p, s->seg_chunk_first.p, sp->off.p,
+                                                               sp->slot.p, (uint32_t)n_chunk, emax, s->seg_task.p);
+        PRGPU_LAUNCHED("seg_task_records");
+    }
     // runs of small pieces
     const uint32_t lo = nw, hi = nw + sp->n_sp;
     uint64_t np = 0;
@@ -758,6 +800,11 @@ void build_seg_tasks(prgpu_session* s) {
         s->seg_packed_r0.alloc(1);
     }
     s->seg_n_runs = (uint32_t)np;
+    s->seg_run_rec.alloc(std::max<uint64_t>(np, 1));
+    if (np) {
+        run_records<<<blocks_for(np), kNT, 0, st>>>(s->seg_packed_r0.p, sp->off.p, (uint32_t)np, s->seg_run_rec.p);
+        PRGPU_LAUNCHED("run_records");
+    }
     // piece partial sums: a slot per (row, segment), zero where a row has no piece
     s->pacc.alloc((size_t)sp->n_rows * S * s->KP);
     PRGPU_CUDA(cudaMemsetAsync(s->pacc.p, 0, s->pacc.bytes(), st));
@@ -767,6 +814,8 @@ void build_seg_tasks(prgpu_session* s) {
     P.seg_off = sp->off.p;
     P.seg_col = sp->col.p;
     P.seg_slot = sp->slot.p;
+    P.seg_task = s->seg_task.p;
+    P.seg_run_rec = s->seg_run_rec.p;
     P.seg_chunk_row = s->seg_chunk_row.p;
     P.seg_chunk_first = s->seg_chunk_first.p;
     P.seg_packed_r0 = s->seg_packed_r0.p;
@@ -1086,7 +1135,7 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
         cudaGetLastError();
         prgpu_session* q = s.get();
         q->seg = nullptr;
-        q->seg_chunk_row.reset(); q->seg_chunk_first.reset(); q->seg_packed_r0.reset();
+        q->seg_chunk_row.reset(); q->seg_chunk_first.reset(); q->seg_packed_r0.reset(); q->seg_task.reset(); q->seg_run_rec.reset();
         q->seg_chunk_acc.reset(); q->pacc.reset(); q->seg_row_cnt.reset();
         build_tasks(q); // packed runs over every packed row again
     }
@@ -1261,7 +1310,8 @@ prgpu_session* session_create(prgpu_graph* g, const prgpu_params* p, bool build_
                 PA.task_begin = t0;
                 PA.task_end = T1;
                 PA.seg_pre = s->seg_n_wchunk;
-                PA.seg_grab = 1;
+                PA.seg_grab = 2; // (measured: 1 / 2 / 4 -> C5 482.7 / 468.6 / 467.6 ms, RMAT-24 x 11 82.6 / 83.1 / 85.4)
+                if (const char* gr = std::getenv("PRGPU_SEG_GRABW")) PA.seg_grab = (uint32_t)std::min(32, std::max(1, std::atoi(gr)));
                 PA2.seg_grab = 4;
                 if (const char* gr = std::getenv("PRGPU_SEG_GRAB")) PA2.seg_grab = (uint32_t)std::max(1, std::atoi(gr));
                 PA.G = GA;
@@ -2414,7 +2464,7 @@ uint64_t session_device_bytes(const prgpu_session* s) {
                  s->chunk_acc.bytes() + s->hot_part.bytes() + s->lanes.bytes() + s->gs.bytes() +
                  s->chunk_row.bytes() + s->chunk_first.bytes() + s->packed_r0.bytes() + s->row_cnt.bytes() +
                  s->task_list.bytes() + s->row_owner.bytes() + s->rank_partials.bytes() + s->need.bytes() +
-                 s->ktime.bytes() + s->seg_chunk_row.bytes() + s->seg_chunk_first.bytes() +
+                 s->ktime.bytes() + s->seg_chunk_row.bytes() + s->seg_chunk_first.bytes() + s->seg_task.bytes() + s->seg_run_rec.bytes() + s->run_rec.bytes() +
                  s->seg_packed_r0.bytes() + s->seg_chunk_acc.bytes() + s->pacc.bytes() + s->seg_row_cnt.bytes();
     for (const auto& m : s->mode_contrib) b += m.bytes();
     return b;

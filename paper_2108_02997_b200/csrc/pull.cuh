@@ -215,6 +215,9 @@ struct Params {
     const uint64_t* seg_off;       // [pieces + 1] into seg_col (wide pieces first)
     const uint32_t* seg_col;
     const uint32_t* seg_slot;      // [pieces] row * seg_S + segment
+    const uint4* seg_task;         // [seg chunks] {edge lo, hi, edges, slot | multi-chunk flag} per task
+    const uint4* seg_run_rec;      // [runs] {first edge lo, hi, first piece, edges | pieces << 16} per run
+    const uint4* run_rec;          // [n_packed] the same for the packed rows' runs (null: not built)
     const uint32_t* seg_chunk_row; // [seg chunks] wide piece of each chunk task
     const uint32_t* seg_chunk_first; // [wide pieces + 1]
     const uint32_t* seg_packed_r0; // [runs + 1] piece ranges of the small-piece runs
@@ -928,6 +931,17 @@ struct Warp {
         if (lane == 0) T.cnt[row] = 0;
     }
 
+    // a whole wide piece in one chunk task: its record gives the edge range and the slot
+    __device__ __forceinline__ void piece_chunk(uint64_t lo, uint32_t len, uint32_t slot_id) {
+        double acc[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc[w] = 0.0;
+        if constexpr (LG > 1 && kBcast) accumulate_bcast(P.seg_col, lo, lo + len, acc);
+        else accumulate(P.seg_col, lo, lo + len, acc);
+        reduce_slots(acc);
+        if (lane < LG) piece_store(slot_id, slice, acc);
+    }
+
     // ---- epilogues of the segmented rows: a row's piece partials in segment order --------
     __device__ void combine_task(uint32_t t) {
         const uint32_t base = t * P.seg_cr;
@@ -1098,22 +1112,40 @@ struct Warp {
     // previous ranks before gathering the current one, so a row costs a
     // single gather round trip.
     template <bool PIECE = false>
-    __device__ void packed_pipe(uint32_t t, double* __restrict__ stage) {
+    __device__ void packed_pipe(uint32_t t, double* __restrict__ stage, bool have_rec = false,
+                                uint4 rec = make_uint4(0, 0, 0, 0)) {
         constexpr int WIN_ = C::EMAX / 2;
         const uint64_t sp = stream_policy(P);
         const uint32_t* __restrict__ pr = PIECE ? P.seg_packed_r0 : P.packed_r0;
         const uint64_t* __restrict__ roff = PIECE ? P.seg_off : P.row_off;
         const uint32_t* __restrict__ colp = PIECE ? P.seg_col : P.col;
-        const uint32_t r0 = pr[t], r1 = pr[t + 1];
-        const uint32_t R = r1 - r0; // <= 2*WIN / max(1, WIN/32) + 1
+        const uint4* __restrict__ recs = PIECE ? P.seg_run_rec : P.run_rec;
         uint64_t* s_off = reinterpret_cast<uint64_t*>(stage);                 // [kPackOff]
         uint32_t* s_col = reinterpret_cast<uint32_t*>(s_off + kPackOff);     // [2*WIN + 8]
-        for (uint32_t x = lane; x <= R; x += 32) s_off[x] = ld_stream_u64(roff + r0 + x, sp);
-        __syncwarp();
-        const uint64_t e0 = s_off[0];
-        const uint32_t ne_all = (uint32_t)(s_off[R] - e0);
-        for (uint32_t x = lane; x < ne_all; x += 32) s_col[x] = ld_stream_u32(colp + e0 + x, sp);
-        __syncwarp();
+        uint32_t r0, R, ne_all; // R <= 2*WIN / max(1, WIN/32) + 1
+        uint64_t e0;
+        if (recs != nullptr && !(kExp && P.split)) {
+            // the run's record {first edge, first row, edges | rows << 16}: the row
+            // offsets and the colidx are staged in ONE round trip instead of
+            // bounds -> offsets -> colidx
+            const uint4 rc = have_rec ? rec : __ldg(recs + t);
+            e0 = ((uint64_t)rc.y << 32) | rc.x;
+            r0 = rc.z;
+            ne_all = rc.w & 0xffffu;
+            R = rc.w >> 16;
+            for (uint32_t x = lane; x <= R; x += 32) s_off[x] = ld_stream_u64(roff + r0 + x, sp);
+            for (uint32_t x = lane; x < ne_all; x += 32) s_col[x] = ld_stream_u32(colp + e0 + x, sp);
+            __syncwarp();
+        } else {
+            r0 = pr[t];
+            R = pr[t + 1] - r0;
+            for (uint32_t x = lane; x <= R; x += 32) s_off[x] = ld_stream_u64(roff + r0 + x, sp);
+            __syncwarp();
+            e0 = s_off[0];
+            ne_all = (uint32_t)(s_off[R] - e0);
+            for (uint32_t x = lane; x < ne_all; x += 32) s_col[x] = ld_stream_u32(colp + e0 + x, sp);
+            __syncwarp();
+        }
         if (kExp && P.pf) // every row of the run in flight to L2 at once (the walk below is one row per slot)
             for (uint32_t x = lane; x < ne_all; x += 32) prefetch_row(s_col[x]);
         uint32_t i = slot;
@@ -1364,10 +1396,29 @@ __global__ void __launch_bounds__(kNT, (PATHS == 8 && PRGPU_A2_MINB) ? PRGPU_A2_
             b = __shfl_sync(0xffffffffu, b, 0);
             if (b >= pre) break;
             const uint32_t e = min(b + GRAB, pre);
-            for (uint32_t i = b; i < e; ++i) {
-                if constexpr ((PATHS & 4) != 0) w.template chunk_task<true>(i);
-                else if constexpr (C::STAGED) w.template packed_task<true>(i, sv);
-                else w.template packed_pipe<true>(i, sv);
+            if constexpr ((PATHS & 4) != 0) {
+                // the grabbed tasks' records in one round trip (lane i holds task b + i's)
+                uint4 rec = make_uint4(0, 0, 0, 0);
+                if (b + lane < e) rec = __ldg(P.seg_task + b + lane);
+                for (uint32_t i = b; i < e; ++i) {
+                    const uint32_t lo_l = __shfl_sync(0xffffffffu, rec.x, i - b), lo_h = __shfl_sync(0xffffffffu, rec.y, i - b);
+                    const uint32_t len = __shfl_sync(0xffffffffu, rec.z, i - b), sl = __shfl_sync(0xffffffffu, rec.w, i - b);
+                    if (sl & 0x80000000u) w.template chunk_task<true>(i); // a chunk of a multi-chunk piece: hand-off
+                    else w.piece_chunk(((uint64_t)lo_h << 32) | lo_l, len, sl);
+                }
+            } else {
+                if constexpr (C::STAGED) {
+                    for (uint32_t i = b; i < e; ++i) w.template packed_task<true>(i, sv);
+                } else { // the grabbed runs' records in one round trip (lane i holds run b + i's)
+                    const bool hr = P.seg_run_rec != nullptr;
+                    uint4 rec = make_uint4(0, 0, 0, 0);
+                    if (hr && b + lane < e) rec = __ldg(P.seg_run_rec + b + lane);
+                    for (uint32_t i = b; i < e; ++i) {
+                        const uint4 rc = make_uint4(__shfl_sync(0xffffffffu, rec.x, i - b), __shfl_sync(0xffffffffu, rec.y, i - b),
+                                                    __shfl_sync(0xffffffffu, rec.z, i - b), __shfl_sync(0xffffffffu, rec.w, i - b));
+                        w.template packed_pipe<true>(i, sv, hr, rc);
+                    }
+                }
             }
         }
     } else if constexpr ((PATHS & 16) != 0) { // combine tasks lead, then the round-robin carries on
