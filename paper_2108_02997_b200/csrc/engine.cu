@@ -729,8 +729,9 @@ void seg_choose_plan(prgpu_session* s, int nranks) {
     // a smaller T also segments packed rows (all their pieces are small)
     const uint32_t T = (uint32_t)std::max<uint64_t>(env_u("PRGPU_SEG_T", (uint64_t)win + 1), 2);
     // pieces longer than wmin edges are pulled by a whole warp (chunk tasks), the others by a lane group
-    // (measured: 3/4 of the packed window, C5 -1 %, RMAT-24 x 11 -1.4 %, C4 +-0; 1/2: +-0, 1/4: +3.5 %)
-    const uint32_t wmin = (uint32_t)std::min<uint64_t>(win, std::max<uint64_t>(1, env_u("PRGPU_SEG_WMIN", 3 * win / 4)));
+    // (measured with the one-load task records: half the packed window; C5 456.3 ms against 459.5 at 3/4
+    // and 471.3 at the whole window, RMAT-24 x 11 82.8 / 83.7, C4 111.8 / 112.2; a quarter: 460.2)
+    const uint32_t wmin = (uint32_t)std::min<uint64_t>(win, std::max<uint64_t>(1, env_u("PRGPU_SEG_WMIN", win / 2)));
     s->seg = graph_seg_plan(g, seg_src, S, T, wmin, pmin, st);
 }
 
