@@ -695,7 +695,7 @@ void build_tasks(prgpu_session* s) {
 // hub rows (same chunk size, same hand-off), small pieces are grouped into
 // runs exactly like packed rows; the rows' epilogues become combine tasks.
 // On by default when the contribution table is at least three segments long
-// (measured on B200: C5 620 -> 459 ms per
+// (measured on B200: C5 620 -> 457 ms per
 // sweep, RMAT-24 x 11 lanes -5 %, C4 -3 %; C2's 194 MB table +5 %, off).
 // PRGPU_SEG=0/1 forces it off/on, PRGPU_SEG_KB the segment size (KB of the
 // run's widest contribution rows), PRGPU_SEG_HOT the number of L2-sized
