@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "pull.cuh"
+#include "lane_cfg.cuh"
 
 namespace prgpu {
 
@@ -271,62 +272,6 @@ __global__ void norm_final(int kind, const double* __restrict__ parts, int npart
     }
 }
 
-// ============================================================================
-// Lane configurations: K lanes -> (LG threads per edge/row, W lanes per thread,
-// WIN edge window per packed task).  Shared memory per warp = 2*WIN*KP doubles.
-// ============================================================================
-using KernelFn = void (*)(const Params);
-
-struct LaneCfg {
-    int LG, W, WIN, KS; // KS: contribution row stride (doubles)
-    KernelFn fn;        // pull_kernel instance
-    int QM = kQmAll;
-    KernelFn fin = nullptr; // matching part_finalize_kernel (multi-GPU)
-    int paths = 3;          // task kinds compiled in (pull_kernel PATHS)
-    int KP() const { return LG * W; }
-    size_t smem() const {
-        const bool async = paths == 1 && kAsyncHub && LG > 1 && (KS == 2 || KS == 4); // pull.cuh async_hub
-        const bool packs = paths != 3 && (paths & (2 | 8)) != 0; // packed_pipe instances (pull.cuh PACKS)
-        const size_t staged = KP() == 1 ? (size_t)kWarps * 2 * WIN * sizeof(double) // STAGED
-                              : packs ? (size_t)kWarps *
-                                                 ((kStagedWide && LG == 4 && KS == 4) ? 2 * WIN * KS
-                                                                                     : kPackOff + (2 * WIN + 8) / 2) *
-                                                 sizeof(double)
-                              : async      ? (size_t)kWarps * 2 * kAsyncBlock * KS * sizeof(double)
-                                           : 0; // packed_pipe stage / cp.async ring
-        const bool smemp = W >= 6 || (paths != 3 && KP() > 1);
-        const size_t cols = smemp ? (size_t)popc_c(QM) * W * kNT * sizeof(double) : 0;     // Partials
-        return staged + cols;
-    }
-};
-
-// CTAs per SM the 11/12-lane instances are compiled for (tuning builds:
-// -DPRGPU_K12_MINB=5/6 trade registers for resident warps)
-#ifndef PRGPU_K12_MINB
-#define PRGPU_K12_MINB 4
-#endif
-constexpr int kMinb12 = PRGPU_K12_MINB;
-
-// packed-row window of the 3/4-lane instances (tuning builds: -DPRGPU_W4=64 / 32)
-#ifndef PRGPU_W4
-#define PRGPU_W4 128
-#endif
-constexpr int kW4 = PRGPU_W4;
-
-// per-mode instance alternatives (tuning only)
-inline int k_variant(const char* name) {
-    const char* v = std::getenv(name);
-    return v ? std::atoi(v) : 0;
-}
-
-// `all_q`: the run needs every partial (all norms / the reference trace);
-// otherwise only L1 + dangling (the damping sweep's stopping rule).
-template <int LG, int W, int WIN, int QJ, int MINB, int QM, int KS, int PATHS = 3>
-LaneCfg mk_cfg() {
-    return LaneCfg{LG, W, WIN, KS ? KS : LG * W, pull_kernel<LG, W, WIN, QJ, MINB, QM, KS, PATHS>, QM,
-                   part_finalize_kernel<LG, W, WIN, QJ, MINB, QM, KS>, PATHS};
-}
-
 template <int LG, int W, int WIN, int MINB, int KS = LG * W, int PATHS = 3>
 LaneCfg wide_cfg(bool all_q) {
     return all_q ? mk_cfg<LG, W, WIN, 0, MINB, kQmAll, KS, PATHS>()
@@ -339,7 +284,7 @@ LaneCfg wide_cfg(bool all_q) {
 // one double per thread (LG = KS).
 template <int PATHS>
 LaneCfg lane_cfg_t(int K, bool all_q) {
-    if (K == 1) return mk_cfg<1, 1, 256, 2, 3, kQmAll, 0, PATHS>();
+    if (K == 1) return k1_base(); // (PATHS 3: the only base configuration)
     if (K == 2) return wide_cfg<2, 1, 64, 4, 2, PATHS>(all_q);
     if (K <= 4) return wide_cfg<4, 1, kW4, 4, 4, PATHS>(all_q);
     if (K <= 8) return wide_cfg<4, 2, 128, 4, 8, PATHS>(all_q);
@@ -359,15 +304,8 @@ inline LaneCfg lane_cfg(int K, bool all_q) { return lane_cfg_t<3>(K, all_q); }
 // set: that kernel at 4 CTAs/SM instead of 3.
 template <int PATHS>
 bool mode_cfg(int KS, int kp, int win, bool all_q, LaneCfg& out, int k1_minb4 = 0) {
-    if (win == 256 && KS == 1 && kp == 1) {
-        if ((k1_minb4 >> (PATHS - 1)) & 1) out = mk_cfg<1, 1, 256, 2, 4, kQmAll, 1, PATHS>();
-        else out = mk_cfg<1, 1, 256, 2, 3, kQmAll, 1, PATHS>();
-        return true;
-    }
+    if (KS == 1 && kp == 1) return k1_mode(PATHS, win, all_q, ((k1_minb4 >> (PATHS - 1)) & 1) != 0, out);
     switch (KS * 100 + kp) {
-    case 101:
-        out = all_q ? mk_cfg<1, 1, 128, 2, 3, kQmAll, 1, PATHS>() : mk_cfg<1, 1, 128, 2, 3, kQmL1, 1, PATHS>();
-        return true;
     // two- and four-lane modes: one 8-byte lane per thread (LG = kp), measured
     // -9% per C5 sweep against two lanes per thread (PRGPU_K4CFG=1 /
     // PRGPU_K2CFG=1 select the two-lane-per-thread instances: tuning only)

@@ -1536,7 +1536,7 @@ __global__ void __launch_bounds__(kNT, (PATHS == 8 && PRGPU_A2_MINB) ? PRGPU_A2_
 // Mode change (Params::mode_id): copy the current contributions (parity of
 // this iteration) of lanes [0, mode_ks[m]) from the buffer of the mode that
 // wrote them into this mode's narrower buffer.  A no-op launch otherwise.
-__global__ void __launch_bounds__(kNT) repack_kernel(const Params P, uint32_t nsrc) {
+static __global__ void __launch_bounds__(kNT) repack_kernel(const Params P, uint32_t nsrc) {
     __shared__ int s_go, s_from, s_par;
     if (threadIdx.x == 0) {
         const int mode = P.gs->mode, from = P.gs->layout;
