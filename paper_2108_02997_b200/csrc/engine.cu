@@ -304,8 +304,11 @@ inline LaneCfg lane_cfg(int K, bool all_q) { return lane_cfg_t<3>(K, all_q); }
 // set: that kernel at 4 CTAs/SM instead of 3.
 template <int PATHS>
 bool mode_cfg(int KS, int kp, int win, bool all_q, LaneCfg& out, int k1_minb4 = 0) {
-    if (KS == 1 && kp == 1) return k1_mode(PATHS, win, all_q, ((k1_minb4 >> (PATHS - 1)) & 1) != 0, out);
+    if (win == 256 && KS == 1 && kp == 1) return k1_mode(PATHS, win, all_q, ((k1_minb4 >> (PATHS - 1)) & 1) != 0, out);
     switch (KS * 100 + kp) {
+    case 101:
+        out = all_q ? mk_cfg<1, 1, 128, 2, 3, kQmAll, 1, PATHS>() : mk_cfg<1, 1, 128, 2, 3, kQmL1, 1, PATHS>();
+        return true;
     // two- and four-lane modes: one 8-byte lane per thread (LG = kp), measured
     // -9% per C5 sweep against two lanes per thread (PRGPU_K4CFG=1 /
     // PRGPU_K2CFG=1 select the two-lane-per-thread instances: tuning only)

@@ -1,5 +1,5 @@
-// engine_k1.cu — the one-lane pull_kernel instances (LG = 1, W = 1: staged
-// packed runs), in a translation unit of their own (lane_cfg.cuh).
+// engine_k1.cu — the pull_kernel instances of one-lane runs (LG = 1, W = 1,
+// window 256: staged packed runs), in a translation unit of their own (lane_cfg.cuh).
 #include "lane_cfg.cuh"
 
 namespace prgpu {
@@ -14,8 +14,7 @@ bool k1_mode_t(int win, bool all_q, bool minb4, LaneCfg& out) {
         else out = mk_cfg<1, 1, 256, 2, 3, kQmAll, 1, PATHS>();
         return true;
     }
-    out = all_q ? mk_cfg<1, 1, 128, 2, 3, kQmAll, 1, PATHS>() : mk_cfg<1, 1, 128, 2, 3, kQmL1, 1, PATHS>();
-    return true;
+    return false; // (the one-lane mode of a wider run, win 128: engine.cu)
 }
 } // namespace
 

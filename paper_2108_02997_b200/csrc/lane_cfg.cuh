@@ -70,7 +70,7 @@ LaneCfg mk_cfg() {
 // the one-lane (LG = 1, W = 1) instances, engine_k1.cu.  k1_base: the run's
 // base configuration (one kernel per iteration); k1_mode: the kernels of a
 // split iteration (paths: pull_kernel PATHS), win 256 (minb4: 4 CTAs/SM
-// instead of 3) or the one-lane mode of a wider run (win 128; all_q as mode_cfg)
+// instead of 3); false for another window (the one-lane mode of a wider run is engine.cu's)
 LaneCfg k1_base();
 bool k1_mode(int paths, int win, bool all_q, bool minb4, LaneCfg& out);
 
